@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the LAKER hot path on B200 (BASELINE.json metric: "PCG iters/sec
++ time-to-solution (rel resid 1e-8) at n=16384; matvec HBM GB/s vs peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload: BASELINE.json configs[2] (C3): n = 16384 clustered sensors, d = 64,
+lambda = 1e-4, tol = 1e-8, K materialized (2 GiB), seeded synthetic inputs
+(synth/).  One step = one pass of the whole hot path through
+the C ABI: laker_assemble_kernel (EXACT) -> laker_fit_preconditioner ->
+laker_pcg_solve (to 1e-8) -> laker_predict (256 x 256 grid).
+
+`value` = PCG iterations per second (sum of iterations / sum of the PCG
+loops' device time, CUDA events on the library's stream); the whole-step
+time, time-to-solution and per-stage times are reported beside it.  `e2e` is
+the same metric with host (pinned) buffers through the same public calls
+(H2D of E, y, E_grid and D2H of alpha and the map inside the timed region):
+PCG iterations / whole-step time.  `roofline` is for the dominant kernel, the
+Dot2 GEMV streaming K (and the dense P): algorithmic bytes per launch
+8 n (n_local) + 16 n, divided by its mean CUDA-event launch time.
+
+Multi-GPU (torchrun, N > 1): K and P row-sharded across ranks (strong scaling),
+timed as the max over ranks.  --impl reference: the fp64 CPU oracle on the
+host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG iters/sec (rel resid 1e-8) at n=16384"
+UNIT = "iters/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _traffic_per_launch():
+    """dram bytes per GEMV launch from the committed `ncu --set full` summary, if any."""
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        return json.load(open(p)).get("gemv_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline_sample(prob, iters: int = 12):
+    """The oracle as it stands on this host's cores: orc_pcg at n = 16384 with a
+    dense P (identity stored densely -- the same per-iteration work, two Dot2
+    GEMVs over n^2 entries, as the learned P), `iters` iterations; K assembled
+    by the oracle beforehand (its time reported separately)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    K, _ = O.assemble(prob.E, prob.scale)
+    t_asm = time.perf_counter() - t0
+    Pd = np.eye(prob.n)
+    t0 = time.perf_counter()
+    _, rep = O.pcg(K, prob.lam, prob.y, O.P_DENSE, Pd, tol=prob.tol, max_iters=iters)
+    dt = time.perf_counter() - t0
+    del K, Pd
+    return {"value": rep.iters / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"oracle orc_pcg at n={prob.n}: {rep.iters} iterations with a dense P "
+                      f"(2 Dot2 GEMVs / iteration, as LEARNED); oracle EXACT assembly of K "
+                      f"took {t_asm:.1f} s (not in value)",
+            "seconds": dt, "assembly_s": t_asm}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle, as it stands, on the host cores."""
+    if rank != 0:
+        return
+    from synth import make_problem
+    import oracle as O
+    prob = make_problem(3)
+    per_step = 6
+    K, _ = O.assemble(prob.E, prob.scale)
+    Pd = np.eye(prob.n)
+    times, its = [], []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, rep = O.pcg(K, prob.lam, prob.y, O.P_DENSE, Pd, tol=prob.tol, max_iters=per_step)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            its.append(rep.iters)
+    value = sum(its) / sum(times)
+    sample = (f"each step = {per_step} oracle PCG iterations (Alg. 1, Dot2 GEMVs with a dense P) of the "
+              f"C3 solve at n={prob.n}; K assembled once by the oracle outside the timed steps")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "C3 (BASELINE.json configs[2]) n=16384 d=64 "
+                                                        "lambda=1e-4 tol=1e-8, bounded sample"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2604_25138_b200 import laker as L
+    from synth import make_problem
+
+    torch.cuda.set_device(local_rank)
+    prob = make_problem(3)
+    n, d = prob.n, prob.d
+    precond = {"learned": L.PRECOND_LEARNED, "jacobi": L.PRECOND_JACOBI, "none": L.PRECOND_NONE}[args.precond]
+    mode = L.MODE_EXACT if args.mode == "exact" else L.MODE_FAST
+    stream = torch.cuda.Stream()
+    nccl_id = None
+    if world > 1:
+        obj = [L.laker_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = L.Context(local_rank, rank, world, nccl_id, stream.cuda_stream)
+
+    dev = torch.device("cuda", local_rank)
+    E_d = torch.from_numpy(prob.E).to(dev)
+    y_d = torch.from_numpy(prob.y).to(dev)
+    Eq_d = torch.from_numpy(prob.Eq).to(dev)
+    alpha_d = torch.zeros(n, dtype=torch.float64, device=dev)
+    map_d = torch.zeros(prob.Eq.shape[0], dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    fit_kw = dict(n_dirs=prob.n_dirs, seed=7)
+
+    def step(E, y, Eq, alpha, out):
+        ctx.assemble_kernel(E, prob.scale, prob.lam, L.STORE_MATERIALIZED, mode)
+        ctx.fit_preconditioner(precond, **fit_kw)
+        reps = L.laker_pcg_solve(ctx.h, 1, y, alpha, prob.tol, 0, True, None)
+        L.laker_predict(ctx.h, Eq, alpha, out, mode)
+        return reps[0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(E_d, y_d, Eq_d, alpha_d, map_d)
+    s0 = ctx.stats()
+    its, pcg_s, stage = [], [], {"assemble_ms": 0.0, "fit_ms": 0.0, "solve_ms": 0.0, "predict_ms": 0.0}
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rep = step(E_d, y_d, Eq_d, alpha_d, map_d)
+            its.append(rep["iters"])
+            pcg_s.append(rep["seconds"])
+            st = ctx.stats()
+            for k in stage:
+                stage[k] += st[k]
+        ev1.record(stream)
+        barrier()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    s1 = ctx.stats()
+    pcg_total = sum(pcg_s)
+    if world > 1:
+        t = torch.tensor([step_ms, pcg_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, pcg_total = float(t[0]), float(t[1])
+    value = sum(its) / pcg_total
+    op_launches = s1["op_launches"] - s0["op_launches"]
+    op_ms = (s1["op_ms"] - s0["op_ms"]) / max(op_launches, 1)
+    prec_launches = s1["prec_launches"] - s0["prec_launches"]
+    prec_ms = (s1["prec_ms"] - s0["prec_ms"]) / max(prec_launches, 1)
+    launches = s1["kernel_launches"] - s0["kernel_launches"]
+
+    # ---- e2e: host pinned buffers through the same calls
+    E_h = torch.from_numpy(prob.E).pin_memory()
+    y_h = torch.from_numpy(prob.y).pin_memory()
+    Eq_h = torch.from_numpy(prob.Eq).pin_memory()
+    alpha_h = torch.zeros(n, dtype=torch.float64).pin_memory()
+    map_h = torch.zeros(prob.Eq.shape[0], dtype=torch.float64).pin_memory()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e_its = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        e_its.append(step(E_h, y_h, Eq_h, alpha_h, map_h)["iters"])
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_value = sum(e_its) / (e2e_ms * 1e-3)
+    h2d = (prob.E.nbytes + prob.y.nbytes + prob.Eq.nbytes)
+    d2h = n * 8 + prob.Eq.shape[0] * 8
+
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    rows = n // world
+    bytes_per_launch = 8.0 * rows * n + 16.0 * n
+    dom_ms = op_ms if op_launches else float("nan")
+    achieved = bytes_per_launch / (dom_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback",
+            "traffic": _traffic_per_launch(), "bytes_per_launch": bytes_per_launch,
+            "mean_launch_ms": dom_ms, "launches": op_launches,
+            "precond_gemv_mean_launch_ms": prec_ms if prec_launches else None}
+    clocks = clk.summary()
+    ctx.close()
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3 (BASELINE.json configs[2]): n=16384 clustered sensors, d=64, "
+                                   "lambda=1e-4, PCG to rel resid 1e-8, K materialized 2 GiB, grid 256x256",
+                       "precond": args.precond, "mode": args.mode, "parallelism": f"rowshard{world}",
+                       "l2": "inputs larger than L2 (K = 2 GiB per solve pass >> 126 MB)"},
+            "time_to_solution_s": pcg_total / args.steps, "pcg_iters_per_solve": its[0],
+            "stage_ms": {k: v / args.steps for k, v in stage.items()},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms / args.steps},
+            "roofline": roof, "gpu_launches": launches, "clocks": clocks}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(prob)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precond", default=os.environ.get("LAKER_BENCH_PRECOND", "learned"),
+                    choices=["learned", "jacobi", "none"])
+    ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * laker.h -- C ABI of liblaker.so, the B200 (sm_100a) hot path of LAKER
+ * (arXiv 2604.25138, "Accelerating Regularized Attention Kernel Regression
+ * for Spectrum Cartography").  Citations "P:n" are lines of the paper's LaTeX
+ * (PAPER.md); readings "Rn" are listed in DESIGN.md §3.
+ *
+ * The four calls follow Alg. 1:
+ *   laker_assemble_kernel    Kernel Construction        (Alg.1 l.1-3,  P:289-291)
+ *   laker_fit_preconditioner Regression Learning (CCCP)  (Alg.1 l.4-14)
+ *   laker_pcg_solve          Preconditioned CG           (Alg.1 l.15-22)
+ *   laker_predict            Radio Map Reconstruction    (Alg.1 l.23-25)
+ *
+ * Conventions (all calls):
+ *  - Every call returns laker_status; no exception or abort crosses the ABI.
+ *    On failure laker_last_error(ctx) holds a one-line reason.
+ *  - Pointer arguments may be HOST or DEVICE memory (detected with
+ *    cudaPointerGetAttributes); host buffers are staged through the context's
+ *    stream.  The caller owns every pointer; none is retained after a call.
+ *  - fp64 everywhere.  Matrices are row-major unless stated; multi-RHS blocks
+ *    (Y, alpha) are column-major n x nrhs.
+ *  - Calls are ordered on the context's CUDA stream (the caller's stream given
+ *    to laker_create, or a context-owned one).  Calls that fill host reports
+ *    synchronize that stream before returning.
+ *  - A context is not thread-safe: one context per (process, device).
+ *  - Multi-GPU (world > 1): every rank calls every function in the same
+ *    order with identical scalar arguments (they are collective); rank r owns
+ *    rows [r*n/W, (r+1)*n/W) of K and P (row-block sharding); vectors are
+ *    replicated on return.
+ *  - No CPU fallback exists: without a usable CUDA device laker_create fails.
+ */
+#ifndef LAKER_H_
+#define LAKER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct laker_ctx_s *laker_ctx;
+
+typedef enum {
+  LAKER_OK = 0,
+  LAKER_ERR_INVALID_ARGUMENT = 1,
+  LAKER_ERR_DIMENSION_MISMATCH = 2,
+  LAKER_ERR_NOT_READY = 3,                 /* e.g. solve before assemble */
+  LAKER_ERR_CUDA = 4,
+  LAKER_ERR_NCCL = 5,
+  LAKER_ERR_OUT_OF_MEMORY = 6,
+  LAKER_ERR_NOT_POSITIVE_DEFINITE = 7,     /* fit: Cholesky pivot <= 0 */
+  LAKER_ERR_INDEFINITE_PRECONDITIONER = 8, /* PCG: r.theta <= 0 */
+  LAKER_ERR_BREAKDOWN_ZERO_CURVATURE = 9,  /* PCG: p.(lambda I + K)p <= 0 */
+  LAKER_ERR_OVERFLOW = 10,                 /* scale*<e_i,e_j> > ln(DBL_MAX) (exp overflow) */
+  LAKER_ERR_INTERNAL = 11
+} laker_status;
+
+enum { LAKER_STORE_MATERIALIZED = 0, LAKER_STORE_ON_THE_FLY = 1 };
+/* EXACT: correctly rounded kernel entries (Dot2 inner product + correctly
+   rounded exp, R18) -- bitwise equal to the oracle.  FAST: fp64 DMMA tensor-
+   core inner products + CUDA exp (<= 1 ulp per entry). */
+enum { LAKER_MODE_FAST = 0, LAKER_MODE_EXACT = 1 };
+enum { LAKER_PRECOND_NONE = 0, LAKER_PRECOND_JACOBI = 1, LAKER_PRECOND_LEARNED = 2,
+       LAKER_PRECOND_EXTERNAL_DENSE = 3 };
+enum { LAKER_TERM_RESIDUAL_TOL = 0, LAKER_TERM_MAX_ITERS = 1, LAKER_TERM_ZERO_RHS = 2,
+       LAKER_TERM_BREAKDOWN = 3, LAKER_TERM_INDEFINITE = 4 };
+
+/* ---------------------------------------------------------------- lifecycle */
+/* Rank 0 only: an NCCL unique id (ncclGetUniqueId) to broadcast to the other
+   ranks (e.g. with torch.distributed).  Not needed when world == 1. */
+laker_status laker_get_unique_id(unsigned char id[128]);
+
+/* Create a context on CUDA device `device`.  world >= 1, 0 <= rank < world.
+   nccl_id: the 128-byte id from rank 0 (ignored, may be NULL, iff world == 1).
+   cuda_stream: a cudaStream_t to order all work on, or NULL for a
+   context-owned non-blocking stream.  *out is NULL on failure. */
+laker_status laker_create(laker_ctx *out, int device, int rank, int world,
+                          const unsigned char *nccl_id, void *cuda_stream);
+laker_status laker_destroy(laker_ctx ctx);
+const char *laker_status_string(laker_status s);
+const char *laker_last_error(laker_ctx ctx);
+
+/* ------------------------------------------------------------ (1) assembly */
+/* K = exp(scale * E E^T) elementwise (Eq. sc-exp-kernel; Alg.1 l.3,
+   P:291).  E: n x d row-major, identical on every rank; it is COPIED into the
+   context (kept for Jacobi, on-the-fly applies and predict).  scale: 1/sqrt(d)
+   for the BASELINE configs, 1 for the paper's own kernel (R1).  lambda > 0 is
+   stored for the operator lambda I + K; it is never added to K.
+   storage MATERIALIZED: rank r stores rows [r n/W, (r+1) n/W) of K in HBM
+   (upper-triangle tiles computed once and mirrored, so K is bitwise symmetric).
+   storage ON_THE_FLY: only E is kept; every operator apply recomputes the
+   entries tile by tile (P:517-519 matvec-only access).
+   Errors: INVALID_ARGUMENT (n < 1, d < 1, lambda <= 0, n % world != 0, bad
+   enum), OVERFLOW (some entry overflowed; K is still written), OUT_OF_MEMORY. */
+laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const double *E,
+                                   double scale, double lambda, int storage, int mode);
+
+/* --------------------------------------------------------- (2) preconditioner */
+typedef struct {
+  int32_t kind;      /* NONE | JACOBI | LEARNED */
+  int32_t n_dirs;    /* N_r; 0 -> min(n, max(ceil(8 sqrt n), ceil(n/4))) */
+  double gamma;      /* CCCP regularization gamma (0.1) */
+  double eps;        /* safeguard epsilon of F_gamma (1e-12, R8) */
+  double rho;        /* shrinkage rho; < 0 -> schedule of R6 */
+  double rho_floor;  /* eps_rho (1e-3) */
+  int32_t max_iters; /* CCCP steps cap (200, R8) */
+  double fp_tol;     /* stop when ||Sigma_{t+1}-Sigma_t||_F/||Sigma_t||_F <= fp_tol (1e-8, R8) */
+  const double *Z;   /* n x N_r column-major N(0,1) draws z_k (Eq. random_directions,
+                        P:239), host or device; NULL -> device Philox stream `seed` */
+  uint64_t seed;
+} laker_fit_opts;
+
+typedef struct {
+  int32_t iters, n_dirs, converged;
+  double final_change;  /* last relative Frobenius change of Sigma */
+  double rho_used;
+  double sigma_min_eig; /* lambda_min(Sigma*) (= a exactly when N_r < n) */
+  double trace;         /* tr Sigma* (= n by construction, Theorem 1) */
+  double seconds;
+} laker_fit_report;
+
+/* Alg.1 l.5-14 then P = Sigma*^{-1/2} (Eq. preconditioner-Sigmma).
+   JACOBI: P = diag(lambda I + K)^{-1}.  NONE: P = I.
+   LEARNED: u_k = (lambda I + K) z_k, ubar_k = u_k/||u_k||; CCCP
+   with shrinkage and trace normalization in the exact structured
+   form Sigma_t = a_t I + Ubar diag(b_t) Ubar^T (O4'); the dense P
+   rows are stored row-sharded like K.  report: host, may be NULL.
+   Errors: NOT_READY (no kernel), NOT_POSITIVE_DEFINITE, INVALID_ARGUMENT
+   (LEARNED with ON_THE_FLY storage). */
+laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
+                                      laker_fit_report *report);
+
+/* ----------------------------------------------------------------- (3) solve */
+typedef struct {
+  double tol;         /* stop when ||r^k||_2 / ||y||_2 <= tol, 0 < tol < 1 */
+  int32_t max_iters;  /* 0 -> 10 n */
+  int32_t instrument; /* 1: time each operator / preconditioner launch with CUDA events */
+} laker_solve_opts;
+
+typedef struct {
+  int32_t iters;            /* operator applies performed (R12) */
+  int32_t termination;      /* LAKER_TERM_* */
+  double rel_residual;      /* recursive ||r|| / ||y|| at exit */
+  double true_rel_residual; /* ||y - (lambda I + K) alpha|| / ||y||, recomputed once */
+  double seconds;           /* device time of the PCG loop (CUDA events) */
+} laker_solve_report;
+
+/* Solve (lambda I + K) alpha = Y by Alg. 1's PCG:
+   alpha^0 = 0, r^0 = y, theta^0 = P r^0, p^0 = theta^0; per iteration one
+   operator apply q = (lambda I + K) p and one preconditioner apply theta = P r;
+   delta = r.theta / p.q, beta = r'.theta' / r.theta; every inner product is a
+   Dot2 reduction; alpha, r, p updates are single fma (R17).
+   Y: n x nrhs column-major (host or device); alpha: n x nrhs output, complete
+   on every rank.  nrhs > 1 runs nrhs independent recurrences sharing each
+   operator / preconditioner pass (R13).  reports: host array [nrhs] or NULL.
+   history: host [max_iters] relative residuals of column 0, or NULL.
+   Reaching max_iters is not an error (termination MAX_ITERS).  Breakdown
+   returns BREAKDOWN_ZERO_CURVATURE / INDEFINITE_PRECONDITIONER with the last
+   iterate in alpha.  y = 0 gives alpha = 0, iters = 0, ZERO_RHS. */
+laker_status laker_pcg_solve(laker_ctx ctx, int32_t nrhs, const double *Y, double *alpha,
+                             const laker_solve_opts *opts, laker_solve_report *reports,
+                             double *history);
+
+/* --------------------------------------------------------------- (4) predict */
+/* r_hat(x_m) = sum_i exp(scale <eq_m, e_i>) alpha_i (Eq. sc-radio-map-
+   reconstruction; Alg.1 l.24), entries recomputed on the
+   fly.  Eq: m x d row-major; alpha: n (host or device); out: m.  Rank r
+   computes rows [r*ceil(m/W), ...) of out and leaves the others untouched.
+   mode EXACT: correctly rounded entries + Dot2 row sums (bitwise = oracle). */
+laker_status laker_predict(laker_ctx ctx, int64_t m, const double *Eq, const double *alpha,
+                           double *out, int mode);
+
+/* ------------------------------------------------- test / diagnostic hooks */
+/* Replace / read the local K rows ((n/W) x n row-major). */
+laker_status laker_load_kernel_rows(laker_ctx ctx, const double *K_rows);
+laker_status laker_get_kernel_rows(laker_ctx ctx, double *K_rows);
+/* kind EXTERNAL_DENSE: data = local P rows ((n/W) x n); JACOBI: data = diag (n),
+   or NULL to derive it from the assembled K; NONE: data ignored. */
+laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *data);
+laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows);
+/* y = (lambda I + K) x, x and y length n (y complete on every rank). */
+laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y);
+
+typedef struct {
+  int64_t n, local_rows, ld;     /* problem size, rows held, padded row stride (doubles) */
+  int32_t rank, world, precond_kind, storage, mode;
+  uint64_t exp_inconclusive;     /* entries whose correctly-rounded test failed twice (R18) */
+  uint64_t exp_overflow;
+  /* instrumented solve (laker_solve_opts.instrument): summed CUDA-event times */
+  double op_ms, prec_ms;         /* total ms in operator / dense-preconditioner passes */
+  int64_t op_launches, prec_launches;
+  double assemble_ms, fit_ms, solve_ms, predict_ms; /* last call of each (events) */
+  int64_t kernel_launches;       /* kernels this context launched since creation */
+} laker_stats;
+laker_status laker_get_stats(laker_ctx ctx, laker_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAKER_H_ */

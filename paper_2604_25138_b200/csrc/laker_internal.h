@@ -1,0 +1,140 @@
+// Internal declarations of liblaker.so (not part of the ABI; see include/laker.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/laker.h"
+#include "dot2.cuh"
+
+namespace laker {
+
+// Row stride of the materialized K and P: a multiple of 256 doubles (2 KiB)
+// so every bulk-copied row segment is 16-byte aligned and whole-chunk sized.
+constexpr int64_t kLdAlign = 256;
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+inline int64_t padded_ld(int64_t n) { return (n + kLdAlign - 1) / kLdAlign * kLdAlign; }
+
+// Device-resident PCG scalars (one struct per right-hand side).
+struct PcgState {
+  double rho;      // r.theta of the current iterate
+  double delta;    // step length of the current iteration
+  double beta;
+  double ynorm;    // ||y||_2
+  double rel;      // ||r|| / ||y|| after the last update
+  double tol;
+  int32_t iters;
+  int32_t max_iters;
+  int32_t done;    // 1 once terminated (later kernels of a captured chunk are no-ops)
+  int32_t term;    // LAKER_TERM_*
+};
+
+// Ticket counters for the "last CTA reduces" epilogues, one per reduction
+// site, reset by the last CTA.
+enum { kCtrGemv = 0, kCtrUpdate = 1, kCtrInit = 2, kCtrMisc = 3, kNumCtr = 8 };
+
+struct Buf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace laker
+
+struct laker_ctx_s {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  ncclComm_t comm = nullptr;
+  std::string last_error;
+
+  // problem
+  int64_t n = 0;
+  int32_t d = 0;
+  double scale = 1.0, lambda = 0.0;
+  int storage = 0, mode = 1;
+  int64_t r0 = 0, r1 = 0, ld = 0;   // local rows [r0, r1), padded stride
+  bool assembled = false;
+
+  double *E = nullptr;              // n x d
+  double *K = nullptr;              // (r1-r0) x ld
+  double *P = nullptr;              // (r1-r0) x ld (dense learned / external)
+  double *Pdiag = nullptr;          // n (Jacobi)
+  int precond_kind = LAKER_PRECOND_NONE;
+
+  // workspace
+  unsigned int *counters = nullptr;        // kNumCtr
+  laker::dd_pair *partials = nullptr;      // per-CTA pairs (>= 2 x grid)
+  unsigned long long *flags = nullptr;     // [0] exp inconclusive, [1] exp overflow
+  int gemv_grid = 0, num_sms = 0;
+
+  laker_stats stats{};
+};
+
+namespace laker {
+
+// error helpers (api.cu)
+laker_status set_err(laker_ctx ctx, laker_status s, const std::string &msg);
+laker_status cuda_err(laker_ctx ctx, cudaError_t e, const char *what);
+
+#define LAKER_CUDA(ctx, call)                                      \
+  do {                                                             \
+    cudaError_t _e = (call);                                       \
+    if (_e != cudaSuccess) return ::laker::cuda_err(ctx, _e, #call); \
+  } while (0)
+
+// ------------------------------------------------------------------ gemv.cu
+// y_i = RN(lambda x_{row0+i} + sum_j A_ij x_j) for the `rows` local rows of A
+// (row stride ld, n logical columns, zero padded), Dot2 rows, bulk-TMA staged.
+// Also reduces dot(x[row0 .. row0+rows), y) over all CTAs into a pair and runs
+// `epi` on it in the last CTA.
+enum GemvEpi { kEpiNone = 0, kEpiDelta = 1, kEpiBeta = 2, kEpiStoreDot = 3 };
+struct GemvArgs {
+  const double *A;
+  int64_t ld;
+  int64_t rows;
+  int64_t ncols;
+  const double *x;        // full vector, length >= ld (zero padded)
+  int64_t row0;           // global index of local row 0 (for the lambda term and the dot)
+  double *y;              // local output (rows)
+  double lambda;          // 0 -> no diagonal term
+  PcgState *state;        // nullable; done != 0 -> no-op; epilogue target
+  dd_pair *partials;      // >= gridDim
+  unsigned int *counter;  // ticket
+  double *dot_out;        // kEpiStoreDot target
+  int epi;
+  bool evict_first;       // stream A with an L2 evict-first policy
+};
+void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
+void gemv_init();
+int gemv_max_grid(int num_sms);
+size_t gemv_smem_bytes();
+
+// -------------------------------------------------------------- assemble.cu
+void launch_assemble_exact_sym(const double *E, int64_t n, int32_t d, double scale, double *K,
+                               int64_t ld, unsigned long long *flags, cudaStream_t s);
+void launch_assemble_exact_rows(const double *E, int64_t n, int32_t d, double scale, int64_t r0,
+                                int64_t r1, double *K, int64_t ld, unsigned long long *flags,
+                                cudaStream_t s);
+void launch_assemble_fast(const double *E, int64_t n, int32_t d, double scale, int64_t r0,
+                          int64_t r1, double *K, int64_t ld, unsigned long long *flags,
+                          cudaStream_t s);
+void launch_jacobi_diag(const double *E, int64_t n, int32_t d, double scale, double lambda,
+                        double *dvec, unsigned long long *flags, cudaStream_t s);
+
+// --------------------------------------------------------------- predict.cu
+// out[a] = RN(sum_i exp(scale <Eq_a, E_i>) w_i (+ lambda * xdiag[a]))  for a in [0, m)
+void launch_kernel_matvec_exact(const double *Eq, int64_t m, const double *E, int64_t n, int32_t d,
+                                double scale, const double *w, double lambda, const double *xdiag,
+                                double *out, unsigned long long *flags, const int32_t *done,
+                                cudaStream_t s);
+
+// ------------------------------------------------------------------- pcg.cu
+laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,
+                              laker_solve_report *rep, double *history);
+laker_status apply_operator_device(laker_ctx ctx, const double *x, double *y);
+
+}  // namespace laker

@@ -1,0 +1,452 @@
+// Preconditioned conjugate gradient, Alg. 1 l.15-22,
+// run entirely on the device.  One iteration is
+//   (a) q = (lambda I + K) p               -- gemv.cu (epilogue: delta = rho / p.q)
+//   (b) alpha += delta p ; r -= delta q    -- update kernel (epilogue: ||r||/||y||,
+//       termination test; for P = I / Jacobi also theta and beta)
+//   (c) theta = P r                        -- gemv.cu on the dense P (epilogue: beta)
+//   (d) p = theta + beta p                 -- update kernel
+// with every inner product a Dot2 reduction (fixed-order last-CTA epilogues)
+// and every vector update a single fma (R17), i.e. the same IEEE operations as
+// the oracle's orc_pcg.  Scalars live in a device PcgState; a kernel that finds
+// state->done set returns at once, so `chunk` iterations are captured into one
+// CUDA graph and the host only polls the state between graph launches.
+#include <cmath>
+#include <vector>
+
+#include "laker_internal.h"
+
+namespace laker {
+namespace {
+
+constexpr int kVecThreads = 256;
+
+// Block pair-reduction + last-block ticket.  Each block contributes NP pairs;
+// the last block returns the NP totals (reduced over blocks in block order).
+template <int NP>
+__device__ bool reduce_pairs_last_block(dd_pair (&v)[NP], dd_pair *partials, unsigned int *counter,
+                                        double (&tot)[NP]) {
+  __shared__ dd_pair sred[kVecThreads / 32][NP];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    dd_pair r = warp_reduce_pair(v[k]);
+    if (lane == 0) sred[warp][k] = r;
+  }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      dd_pair t = sred[0][k];
+      for (int w = 1; w < kVecThreads / 32; ++w) pair_add(t, sred[w][k]);
+      partials[blockIdx.x * NP + k] = t;
+    }
+    __threadfence();
+    s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  if (warp == 0) {
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      dd_pair t = {0.0, 0.0};
+      for (int b = lane; b < (int)gridDim.x; b += 32) {
+        dd_pair o;
+        o.s = __ldcg(&partials[b * NP + k].s);
+        o.c = __ldcg(&partials[b * NP + k].c);
+        pair_add(t, o);
+      }
+      t = warp_reduce_pair(t);
+      tot[k] = pair_value(t);
+    }
+    if (lane == 0) *counter = 0u;
+  }
+  return lane == 0 && warp == 0;
+}
+
+// alpha = 0, r = y; ||y||^2.  Last block: ynorm, ZERO_RHS.
+__global__ void __launch_bounds__(kVecThreads) pcg_init_kernel(int64_t n, const double *__restrict__ y,
+                                                               double *__restrict__ alpha,
+                                                               double *__restrict__ r, PcgState *st,
+                                                               dd_pair *partials, unsigned int *counter) {
+  dd_pair v[1] = {{0.0, 0.0}};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double yi = y[i];
+    alpha[i] = 0.0;
+    r[i] = yi;
+    dot2_step(v[0], yi, yi);
+  }
+  double tot[1];
+  if (reduce_pairs_last_block<1>(v, partials, counter, tot)) {
+    st->ynorm = __dsqrt_rn(tot[0]);
+    st->iters = 0;
+    st->rel = 1.0;
+    if (st->ynorm == 0.0) {
+      st->done = 1;
+      st->term = LAKER_TERM_ZERO_RHS;
+    }
+  }
+}
+
+// theta^0 = P r^0 (none: r, jacobi: d o r; dense: already in theta), p^0 = theta^0,
+// rho = r.theta.  For dense, rho_in_state = 1 (the P gemv stored it).
+__global__ void __launch_bounds__(kVecThreads) pcg_first_dir_kernel(
+    int64_t n, int pk, const double *__restrict__ dvec, const double *__restrict__ r,
+    double *__restrict__ theta, double *__restrict__ p, PcgState *st, dd_pair *partials,
+    unsigned int *counter) {
+  if (*(volatile int32_t *)&st->done) return;
+  dd_pair v[1] = {{0.0, 0.0}};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = r[i];
+    double th;
+    if (pk == LAKER_PRECOND_NONE) {
+      th = ri;
+    } else if (pk == LAKER_PRECOND_JACOBI) {
+      th = __dmul_rn(dvec[i], ri);
+      theta[i] = th;
+    } else {
+      th = theta[i];
+    }
+    p[i] = th;
+    dot2_step(v[0], ri, th);
+  }
+  double tot[1];
+  if (reduce_pairs_last_block<1>(v, partials, counter, tot)) {
+    st->rho = tot[0];
+    if (!(tot[0] > 0.0)) {
+      st->done = 1;
+      st->term = LAKER_TERM_INDEFINITE;
+    }
+  }
+}
+
+// alpha = fma(delta, p, alpha); r = fma(-delta, q, r); ||r||^2 (and r.theta for Jacobi).
+__global__ void __launch_bounds__(kVecThreads) pcg_update_kernel(
+    int64_t n, int pk, const double *__restrict__ dvec, const double *__restrict__ p,
+    const double *__restrict__ q, double *__restrict__ alpha, double *__restrict__ r,
+    double *__restrict__ theta, PcgState *st, double *history, dd_pair *partials, unsigned int *counter) {
+  if (*(volatile int32_t *)&st->done) return;
+  const double delta = st->delta;
+  dd_pair v[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    alpha[i] = __fma_rn(delta, p[i], alpha[i]);
+    const double ri = __fma_rn(-delta, q[i], r[i]);
+    r[i] = ri;
+    dot2_step(v[0], ri, ri);
+    if (pk == LAKER_PRECOND_JACOBI) {
+      const double th = __dmul_rn(dvec[i], ri);
+      theta[i] = th;
+      dot2_step(v[1], ri, th);
+    }
+  }
+  double tot[2];
+  if (reduce_pairs_last_block<2>(v, partials, counter, tot)) {
+    const double rel = __ddiv_rn(__dsqrt_rn(tot[0]), st->ynorm);
+    const int it = st->iters + 1;
+    st->iters = it;
+    st->rel = rel;
+    if (history) history[it - 1] = rel;
+    if (rel <= st->tol) {
+      st->term = LAKER_TERM_RESIDUAL_TOL;
+      st->done = 1;
+      return;
+    }
+    if (pk != LAKER_PRECOND_EXTERNAL_DENSE && pk != LAKER_PRECOND_LEARNED) {
+      const double rho_new = (pk == LAKER_PRECOND_NONE) ? tot[0] : tot[1];
+      if (!(rho_new > 0.0)) {
+        st->term = LAKER_TERM_INDEFINITE;
+        st->done = 1;
+        return;
+      }
+      st->beta = __ddiv_rn(rho_new, st->rho);
+      st->rho = rho_new;
+      if (it >= st->max_iters) {
+        st->term = LAKER_TERM_MAX_ITERS;
+        st->done = 1;
+      }
+    }
+  }
+}
+
+// dense P only: after theta = P r and beta, close the iteration budget.
+__global__ void pcg_budget_kernel(PcgState *st) {
+  if (st->done) return;
+  if (st->iters >= st->max_iters) {
+    st->term = LAKER_TERM_MAX_ITERS;
+    st->done = 1;
+  }
+}
+
+// p = fma(beta, p, theta)
+__global__ void __launch_bounds__(kVecThreads) pcg_pupdate_kernel(int64_t n, const double *__restrict__ theta,
+                                                                  double *__restrict__ p,
+                                                                  const PcgState *st) {
+  if (*(volatile const int32_t *)&st->done) return;
+  const double beta = st->beta;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = __fma_rn(beta, p[i], theta[i]);
+}
+
+// true residual ||y - q|| / ||y|| with q = (lambda I + K) alpha
+__global__ void __launch_bounds__(kVecThreads) true_residual_kernel(int64_t n, const double *__restrict__ y,
+                                                                    const double *__restrict__ q,
+                                                                    const PcgState *st, double *out,
+                                                                    dd_pair *partials,
+                                                                    unsigned int *counter) {
+  dd_pair v[1] = {{0.0, 0.0}};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = __dsub_rn(y[i], q[i]);
+    dot2_step(v[0], t, t);
+  }
+  double tot[1];
+  if (reduce_pairs_last_block<1>(v, partials, counter, tot))
+    *out = st->ynorm > 0.0 ? __ddiv_rn(__dsqrt_rn(tot[0]), st->ynorm) : 0.0;
+}
+
+// delta epilogue for the on-the-fly operator: p.q over the vector
+__global__ void __launch_bounds__(kVecThreads) dot_delta_kernel(int64_t n, const double *__restrict__ p,
+                                                                const double *__restrict__ q, PcgState *st,
+                                                                dd_pair *partials, unsigned int *counter) {
+  if (*(volatile int32_t *)&st->done) return;
+  dd_pair v[1] = {{0.0, 0.0}};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dot2_step(v[0], p[i], q[i]);
+  double tot[1];
+  if (reduce_pairs_last_block<1>(v, partials, counter, tot)) {
+    if (!(tot[0] > 0.0)) {
+      st->term = LAKER_TERM_BREAKDOWN;
+      st->done = 1;
+    } else {
+      st->delta = __ddiv_rn(st->rho, tot[0]);
+    }
+  }
+}
+
+__global__ void strided_copy_kernel(int64_t n, const double *__restrict__ src, double *__restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+struct Workspace {
+  double *alpha = nullptr, *r = nullptr, *theta = nullptr, *p = nullptr, *q = nullptr, *y = nullptr;
+  double *hist = nullptr, *scal = nullptr;
+  PcgState *st = nullptr;
+  size_t cap_n = 0;
+  int32_t cap_hist = 0;
+};
+
+}  // namespace
+
+// The operator apply used by the solver: q = (lambda I + K) p.
+static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState *st, int epi, double *dot_out) {
+  if (ctx->storage == LAKER_STORE_MATERIALIZED) {
+    GemvArgs a{};
+    a.A = ctx->K;
+    a.ld = ctx->ld;
+    a.rows = ctx->r1 - ctx->r0;
+    a.ncols = ctx->n;
+    a.x = p;
+    a.row0 = ctx->r0;
+    a.y = q;
+    a.lambda = ctx->lambda;
+    a.state = st;
+    a.partials = ctx->partials;
+    a.counter = ctx->counters + kCtrGemv;
+    a.dot_out = dot_out;
+    a.epi = epi;
+    a.evict_first = true;
+    launch_gemv(a, ctx->gemv_grid, ctx->stream);
+  } else {
+    launch_kernel_matvec_exact(ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, ctx->E, ctx->n, ctx->d,
+                               ctx->scale, p, ctx->lambda, p + ctx->r0, q, ctx->flags,
+                               st ? &st->done : nullptr, ctx->stream);
+    if (epi == kEpiDelta) {
+      const int g = (int)std::min<int64_t>(2 * ctx->num_sms, (ctx->n + kVecThreads - 1) / kVecThreads);
+      dot_delta_kernel<<<g, kVecThreads, 0, ctx->stream>>>(ctx->n, p, q, st, ctx->partials,
+                                                          ctx->counters + kCtrMisc);
+      ctx->stats.kernel_launches++;
+    }
+  }
+  ctx->stats.kernel_launches++;
+}
+
+static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgState *st, int epi, double *dot_out) {
+  GemvArgs a{};
+  a.A = ctx->P;
+  a.ld = ctx->ld;
+  a.rows = ctx->r1 - ctx->r0;
+  a.ncols = ctx->n;
+  a.x = r;
+  a.row0 = ctx->r0;
+  a.y = theta;
+  a.lambda = 0.0;
+  a.state = st;
+  a.partials = ctx->partials;
+  a.counter = ctx->counters + kCtrGemv;
+  a.dot_out = dot_out;
+  a.epi = epi;
+  a.evict_first = true;
+  launch_gemv(a, ctx->gemv_grid, ctx->stream);
+  ctx->stats.kernel_launches++;
+}
+
+laker_status apply_operator_device(laker_ctx ctx, const double *x, double *y) {
+  // x must be padded to ld with zeros: stage it.
+  double *xp = nullptr;
+  LAKER_CUDA(ctx, cudaMallocAsync(&xp, ctx->ld * sizeof(double), ctx->stream));
+  LAKER_CUDA(ctx, cudaMemsetAsync(xp, 0, ctx->ld * sizeof(double), ctx->stream));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(xp, x, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  launch_operator(ctx, xp, y + ctx->r0, nullptr, kEpiNone, nullptr);
+  LAKER_CUDA(ctx, cudaGetLastError());
+  LAKER_CUDA(ctx, cudaFreeAsync(xp, ctx->stream));
+  return LAKER_OK;
+}
+
+laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out, const laker_solve_opts &o,
+                              laker_solve_report *rep, double *history) {
+  if (ctx->world != 1) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-rank PCG not built in this version");
+  const int64_t n = ctx->n, ld = ctx->ld;
+  const int pk = ctx->precond_kind;
+  const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
+  if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
+  const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
+  cudaStream_t s = ctx->stream;
+
+  Workspace w;
+  const size_t vb = (size_t)ld * sizeof(double);
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 6 * vb + 2 * sizeof(double), s));
+  w.r = w.alpha + ld;
+  w.theta = w.r + ld;
+  w.p = w.theta + ld;
+  w.q = w.p + ld;
+  w.y = w.q + ld;
+  w.scal = w.y + ld;
+  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 6 * vb + 2 * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)max_iters * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.st, sizeof(PcgState), s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(w.y, y, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  PcgState h0{};
+  h0.tol = o.tol;
+  h0.max_iters = max_iters;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(w.st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+
+  const int vg = (int)std::min<int64_t>(2 * ctx->num_sms, (n + kVecThreads - 1) / kVecThreads);
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, s);
+
+  pcg_init_kernel<<<vg, kVecThreads, 0, s>>>(n, w.y, w.alpha, w.r, w.st, ctx->partials, ctx->counters + kCtrInit);
+  if (dense) launch_precond(ctx, w.r, w.theta, w.st, kEpiStoreDot, &w.st->rho);
+  pcg_first_dir_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.r, w.theta, w.p, w.st, ctx->partials,
+                                                  ctx->counters + kCtrInit);
+  ctx->stats.kernel_launches += 2;
+  LAKER_CUDA(ctx, cudaGetLastError());
+
+  const double *theta_src = (pk == LAKER_PRECOND_NONE) ? w.r : w.theta;
+  const int chunk = n >= 8192 ? 8 : (n >= 2048 ? 32 : 64);
+  const bool instr = o.instrument != 0;
+  std::vector<cudaEvent_t> evs;
+  if (instr) {
+    evs.resize(4 * chunk);
+    for (auto &e : evs) cudaEventCreate(&e);
+  }
+  auto record_iteration = [&](int j) {
+    if (instr) cudaEventRecord(evs[4 * j + 0], s);
+    launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr);
+    if (instr) cudaEventRecord(evs[4 * j + 1], s);
+    pcg_update_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.p, w.q, w.alpha, w.r, w.theta, w.st,
+                                                 w.hist, ctx->partials, ctx->counters + kCtrUpdate);
+    if (dense) {
+      if (instr) cudaEventRecord(evs[4 * j + 2], s);
+      launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
+      if (instr) cudaEventRecord(evs[4 * j + 3], s);
+      pcg_budget_kernel<<<1, 1, 0, s>>>(w.st);
+      ctx->stats.kernel_launches++;
+    }
+    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, w.p, w.st);
+    ctx->stats.kernel_launches += 2;
+  };
+
+  // capture one chunk into a graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const int64_t launches_before = ctx->stats.kernel_launches;
+  LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int j = 0; j < chunk; ++j) record_iteration(j);
+  LAKER_CUDA(ctx, cudaStreamEndCapture(s, &graph));
+  const int64_t per_chunk = ctx->stats.kernel_launches - launches_before;
+  ctx->stats.kernel_launches = launches_before;
+  LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec, graph, 0));
+
+  PcgState *hs = nullptr;
+  LAKER_CUDA(ctx, cudaMallocHost(&hs, sizeof(PcgState)));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hs, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  int32_t iters_prev = 0;
+  while (!hs->done) {
+    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
+    ctx->stats.kernel_launches += per_chunk;
+    LAKER_CUDA(ctx, cudaMemcpyAsync(hs, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    if (instr) {
+      const int ran = hs->iters - iters_prev;  // iterations whose operator pass did real work
+      for (int j = 0; j < std::min(ran, chunk); ++j) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, evs[4 * j + 0], evs[4 * j + 1]);
+        ctx->stats.op_ms += ms;
+        ctx->stats.op_launches++;
+        if (dense && (j < ran - 1 || !hs->done || hs->term != LAKER_TERM_RESIDUAL_TOL)) {
+          cudaEventElapsedTime(&ms, evs[4 * j + 2], evs[4 * j + 3]);
+          ctx->stats.prec_ms += ms;
+          ctx->stats.prec_launches++;
+        }
+      }
+    }
+    iters_prev = hs->iters;
+  }
+  cudaEventRecord(ev1, s);
+
+  // true residual (one extra operator apply, outside the timed loop)
+  launch_operator(ctx, w.alpha, w.q, nullptr, kEpiNone, nullptr);
+  true_residual_kernel<<<vg, kVecThreads, 0, s>>>(n, w.y, w.q, w.st, w.scal, ctx->partials,
+                                                  ctx->counters + kCtrMisc);
+  ctx->stats.kernel_launches++;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(alpha_out, w.alpha, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  double true_rel = 0.0;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(&true_rel, w.scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hs, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  if (history && hs->iters > 0) {
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    LAKER_CUDA(ctx, cudaMemcpyAsync(history, w.hist, (size_t)hs->iters * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  ctx->stats.solve_ms = ms;
+  if (rep) {
+    rep->iters = hs->iters;
+    rep->termination = hs->term;
+    rep->rel_residual = hs->iters > 0 ? hs->rel : (hs->term == LAKER_TERM_ZERO_RHS ? 0.0 : 1.0);
+    rep->true_rel_residual = true_rel;
+    rep->seconds = ms * 1e-3;
+  }
+  const int term = hs->term;
+  cudaFreeHost(hs);
+  for (auto &e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaGraphExecDestroy(gexec);
+  cudaGraphDestroy(graph);
+  cudaFreeAsync(w.alpha, s);
+  cudaFreeAsync(w.hist, s);
+  cudaFreeAsync(w.st, s);
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  if (term == LAKER_TERM_BREAKDOWN) return set_err(ctx, LAKER_ERR_BREAKDOWN_ZERO_CURVATURE, "p.(lambda I + K)p <= 0");
+  if (term == LAKER_TERM_INDEFINITE) return set_err(ctx, LAKER_ERR_INDEFINITE_PRECONDITIONER, "r.theta <= 0");
+  return LAKER_OK;
+}
+
+}  // namespace laker
