@@ -354,15 +354,15 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     for (auto &e : evs) cudaEventCreate(&e);
   }
   auto record_iteration = [&](int j) {
-    if (instr) cudaEventRecord(evs[4 * j + 0], s);
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
     launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr);
-    if (instr) cudaEventRecord(evs[4 * j + 1], s);
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
     pcg_update_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.p, w.q, w.alpha, w.r, w.theta, w.st,
                                                  w.hist, ctx->partials, ctx->counters + kCtrUpdate);
     if (dense) {
-      if (instr) cudaEventRecord(evs[4 * j + 2], s);
+      if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
       launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
-      if (instr) cudaEventRecord(evs[4 * j + 3], s);
+      if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
       pcg_budget_kernel<<<1, 1, 0, s>>>(w.st);
       ctx->stats.kernel_launches++;
     }
