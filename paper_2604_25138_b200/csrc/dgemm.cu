@@ -1,0 +1,164 @@
+// fp64 tensor-core GEMM for the dense contractions of the CCCP fit
+// (U = (lambda I + K) Z, Gram matrices of the
+// directions, T = a I + R diag(b) R^T, Newton-Schulz products, P formation)
+// and the multi-RHS operator (row a10).
+//
+//   C = alpha * A op(B) + beta * Cin + diag * [row - col == diag_offset]
+//   A: M x K row-major (k contiguous); op(B): B_KN ? B is K x N row-major
+//   (n contiguous) : B is N x K row-major (k contiguous, i.e. A B^T).
+//
+// mma.sync m8n8k4 .f64 (SASS DMMA) -- tcgen05 has no fp64 kind on sm_100a.
+// 128 x 128 x 16 CTA tile, 8 warps (2 x 4) of 64 x 32, 3-stage cp.async
+// pipeline, shared-memory strides chosen so every fragment load is
+// conflict-free (row stride = 8 words mod 32 for the 4 x 4 lane pattern of a
+// half warp).  M and N may be ragged (zero-filled loads, masked stores);
+// K must be a multiple of 16 (callers keep operands zero padded).
+#include "laker_internal.h"
+
+namespace laker {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, ST = 3;
+constexpr int AS = BK + 4;       // As[m][k] row stride (doubles)
+constexpr int BS_NK = BK + 4;    // Bs[n][k]
+constexpr int BS_KN = BN + 4;    // Bs[k][n]
+constexpr int A_ELEMS = BM * AS;
+constexpr int B_ELEMS_NK = BN * BS_NK;
+constexpr int B_ELEMS_KN = BK * BS_KN;
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <bool B_KN>
+__global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
+  const int bm = blockIdx.y, bn = blockIdx.x;
+  if (g.lower_only && bn > bm) return;
+  extern __shared__ __align__(16) double sm[];
+  double *As = sm;
+  double *Bs = sm + ST * A_ELEMS;
+  constexpr int BSZ = B_KN ? B_ELEMS_KN : B_ELEMS_NK;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int64_t row0 = (int64_t)bm * BM, col0 = (int64_t)bn * BN;
+
+  auto load_stage = [&](int st, int k0) {
+    double *as = As + st * A_ELEMS;
+    double *bs = Bs + st * BSZ;
+#pragma unroll
+    for (int c = tid; c < BM * BK / 2; c += 256) {
+      const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
+      const bool ok = row0 + r < g.M;
+      cp_async16(as + r * AS + cc, g.A + (ok ? (row0 + r) : 0) * g.lda + k0 + cc, ok);
+    }
+    if (B_KN) {
+#pragma unroll
+      for (int c = tid; c < BK * BN / 2; c += 256) {
+        const int r = c / (BN / 2), cc = (c % (BN / 2)) * 2;
+        const bool ok = col0 + cc < g.N;
+        cp_async16(bs + r * BS_KN + cc, g.B + (int64_t)(k0 + r) * g.ldb + (ok ? col0 + cc : 0), ok);
+      }
+    } else {
+#pragma unroll
+      for (int c = tid; c < BN * BK / 2; c += 256) {
+        const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
+        const bool ok = col0 + r < g.N;
+        cp_async16(bs + r * BS_NK + cc, g.B + (ok ? (col0 + r) : 0) * g.ldb + k0 + cc, ok);
+      }
+    }
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = g.K / BK;
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < KT) load_stage(s, s * BK);
+    cp_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<ST - 2>();
+    __syncthreads();
+    const int nk = kt + ST - 1;
+    if (nk < KT) load_stage(nk % ST, nk * BK);
+    cp_commit();
+    const double *as = As + (kt % ST) * A_ELEMS;
+    const double *bs = Bs + (kt % ST) * BSZ;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = as[(wm + 8 * i + fr) * AS + kk + fk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        b[j] = B_KN ? bs[(kk + fk) * BS_KN + wn + 8 * j + fr] : bs[(wn + 8 * j + fr) * BS_NK + kk + fk];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = row0 + wm + 8 * i + fr;
+    if (r >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = col0 + wn + 8 * j + 2 * fk;
+      if (c >= g.N) continue;
+      double v0 = g.alpha * acc[i][j][0], v1 = g.alpha * acc[i][j][1];
+      if (g.beta != 0.0) {
+        const double2 ci = *reinterpret_cast<const double2 *>(g.Cin + r * g.ldcin + c);
+        v0 = v0 + g.beta * ci.x;
+        v1 = v1 + g.beta * ci.y;
+      }
+      if (g.diag != 0.0) {
+        if (r - c == g.diag_offset) v0 = v0 + g.diag;
+        if (r - (c + 1) == g.diag_offset) v1 = v1 + g.diag;
+      }
+      *reinterpret_cast<double2 *>(g.C + r * g.ldc + c) = make_double2(v0, v1);
+    }
+  }
+}
+
+constexpr size_t smem_bytes(bool kn) { return (size_t)ST * (A_ELEMS + (kn ? B_ELEMS_KN : B_ELEMS_NK)) * 8; }
+
+}  // namespace
+
+void dgemm_init() {
+  cudaFuncSetAttribute(dgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(false));
+  cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(true));
+}
+
+void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0) return;
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
+  if (b_kn)
+    dgemm_kernel<true><<<grid, 256, smem_bytes(true), s>>>(g);
+  else
+    dgemm_kernel<false><<<grid, 256, smem_bytes(false), s>>>(g);
+}
+
+}  // namespace laker

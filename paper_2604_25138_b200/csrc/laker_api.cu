@@ -166,6 +166,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   c->gemv_grid = laker::gemv_max_grid(c->num_sms);
   laker::gemv_init();
+  laker::dgemm_init();
   const size_t npart = 4096;
   if (cudaMalloc(&c->counters, laker::kNumCtr * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&c->partials, npart * sizeof(laker::dd_pair)) != cudaSuccess ||
@@ -295,7 +296,12 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
     case LAKER_PRECOND_LEARNED:
       if (ctx->storage != LAKER_STORE_MATERIALIZED)
         return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: LEARNED needs MATERIALIZED storage");
-      return set_err(ctx, LAKER_ERR_NOT_READY, "fit: LEARNED is not built in this version");
+      {
+        laker_status st = laker::fit_learned(ctx, *opts, report);
+        if (st != LAKER_OK) return st;
+        LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        return LAKER_OK;
+      }
     default:
       return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: unknown kind");
   }

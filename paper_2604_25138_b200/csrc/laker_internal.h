@@ -132,6 +132,38 @@ void launch_kernel_matvec_exact(const double *Eq, int64_t m, const double *E, in
                                 double *out, unsigned long long *flags, const int32_t *done,
                                 cudaStream_t s);
 
+// ----------------------------------------------------------------- dgemm.cu
+struct GemmArgs {
+  int64_t M, N, K;        // K % 16 == 0; N even (or ldc/ldcin padded)
+  const double *A;        // M x K row-major
+  int64_t lda;
+  const double *B;        // b_kn ? K x N : N x K (row-major)
+  int64_t ldb;
+  double *C;
+  int64_t ldc;
+  double alpha, beta;     // C = alpha A op(B) + beta Cin (+ diag on row - col == diag_offset)
+  const double *Cin;
+  int64_t ldcin;
+  double diag;
+  int64_t diag_offset;
+  bool lower_only;        // skip CTA tiles strictly above the block diagonal
+};
+void dgemm_init();
+void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s);
+
+// ------------------------------------------------------------- dense_la.cu
+// In-place lower Cholesky of the n x n SPD matrix A (row-major, lda; n % 64 == 0);
+// strict upper triangle zeroed.  *flag (device) set to 1 on a pivot <= 0.
+void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s, int64_t *launches);
+// B <- L^{-1} B  (L n x n lower, n % 64 == 0; B n x ncols row-major, ldb).
+void trsm_lower_left(const double *L, int64_t ldl, int64_t n, double *B, int64_t ldb, int64_t ncols,
+                     cudaStream_t s, int64_t *launches);
+void launch_transpose(const double *A, int64_t rows, int64_t cols, int64_t lda, double *B, int64_t ldb,
+                      cudaStream_t s);
+
+// ------------------------------------------------------------------- fit.cu
+laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_report *rep);
+
 // ------------------------------------------------------------------- pcg.cu
 laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,
                               laker_solve_report *rep, double *history);

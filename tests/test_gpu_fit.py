@@ -1,0 +1,110 @@
+"""GPU CCCP fit (laker_fit_preconditioner, LEARNED) against the oracle's
+structured fit on the same Z (DESIGN.md §6 parity protocol step 3: P within
+1e-8 relative Frobenius, CCCP steps +-1), plus properties at full size."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from synth import make_problem, make_directions  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2604_25138_b200 import laker
+    return laker
+
+
+@pytest.fixture(scope="module")
+def ctx(L):
+    c = L.Context(0)
+    yield c
+    c.close()
+
+
+def _fit_both(ctx, L, cid, n=None):
+    P = make_problem(cid, n=n)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    K, _ = O.assemble(P.E, P.scale)
+    Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
+    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    Pg = ctx.get_preconditioner_rows()
+    Po, ro, st = O.cccp_fit_structured(K, P.lam, Z)
+    return P, K, Pg, rep, Po, ro, st
+
+
+@pytest.mark.parametrize("cid,n", [(1, None), (2, None), (3, 2048), (3, 1000)])
+def test_fit_matches_oracle(ctx, L, cid, n):
+    P, K, Pg, rep, Po, ro, st = _fit_both(ctx, L, cid, n)
+    assert rep["converged"] == 1 and ro.converged
+    assert abs(rep["iters"] - ro.iters) <= 1
+    assert abs(rep["sigma_min_eig"] / ro.sigma_min_eig - 1) <= 1e-8
+    assert abs(rep["trace"] / P.n - 1) <= 1e-8
+    assert rep["rho_used"] == ro.rho_used
+    assert (Pg == Pg.T).all()
+    assert np.linalg.norm(Pg - Po) / np.linalg.norm(Po) <= 1e-8
+
+
+@pytest.mark.parametrize("cid,n", [(1, None), (2, None)])
+def test_learned_pcg_end_to_end(ctx, L, cid, n):
+    """End-to-end (own fit, own K): alpha within 1e-6 of Cholesky (R14), iteration
+    count within the envelope of the oracle (R15 iii), fewer than Jacobi (T21)."""
+    P, K, Pg, rep, Po, ro, st = _fit_both(ctx, L, cid, n)
+    ag, reps, _ = ctx.pcg_solve(P.y, P.tol)
+    ao, rpo = O.pcg(K, P.lam, P.y, O.P_DENSE, Po, tol=P.tol)
+    ref = O.reference_solve(K, P.lam, P.y)
+    assert reps[0]["termination"] == L.TERM_RESIDUAL_TOL
+    assert np.linalg.norm(ag - ref) / np.linalg.norm(ref) <= 1e-6
+    # envelope: the oracle PCG with its own P perturbed by +-1 ulp (8 seeds)
+    r = np.random.default_rng(0)
+    its = [rpo.iters]
+    for s in range(8 if P.n <= 256 else 3):
+        Pp = Po * (1 + r.choice([-1.0, 0.0, 1.0], Po.shape) * 2.0 ** -52)
+        Pp = np.triu(Pp) + np.triu(Pp, 1).T
+        its.append(O.pcg(K, P.lam, P.y, O.P_DENSE, Pp, tol=P.tol)[1].iters)
+    assert min(its) - 2 <= reps[0]["iters"] <= max(its) + 2, (reps[0]["iters"], its)
+    ctx.set_preconditioner(L.PRECOND_JACOBI)
+    _, rj, _ = ctx.pcg_solve(P.y, P.tol)
+    assert reps[0]["iters"] < rj[0]["iters"]
+
+
+def test_fit_device_rng_and_invariants(ctx, L):
+    P = make_problem(2)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, seed=123)
+    assert rep["converged"] == 1 and rep["n_dirs"] == O.nr_schedule(P.n)
+    Pg = ctx.get_preconditioner_rows()
+    assert (Pg == Pg.T).all()
+    w = np.linalg.eigvalsh(Pg)
+    assert w[0] > 0
+    # P = Sigma^{-1/2} with Sigma ~ (lambda I + K)^2 up to scale: kappa(P A) << kappa(A)
+    K, _ = O.assemble(P.E, P.scale)
+    A = K + P.lam * np.eye(P.n)
+    assert O.cond_precond(Pg, A) <= O.cond_spd(A) / 50
+    rep2 = ctx.fit_preconditioner(L.PRECOND_LEARNED, seed=123)
+    assert (ctx.get_preconditioner_rows() == Pg).all() and rep2["iters"] == rep["iters"]   # deterministic
+
+
+def test_fit_c3_full_size(ctx, L):
+    """C3 (n = 16384, N_r = 4096): GPU fit vs the oracle's structured fit on the
+    same Z, sampled rows of P; then LEARNED PCG converges in fewer iterations
+    than Jacobi."""
+    P = make_problem(3)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    Z = np.asfortranarray(make_directions(3, P.n, P.n_dirs))
+    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    assert rep["converged"] == 1
+    Pg = ctx.get_preconditioner_rows()
+    K, _ = O.assemble(P.E, P.scale)
+    Po, ro, _ = O.cccp_fit_structured(K, P.lam, Z)
+    assert abs(rep["iters"] - ro.iters) <= 1
+    assert abs(rep["sigma_min_eig"] / ro.sigma_min_eig - 1) <= 1e-8
+    rows = np.array([0, 1, 4097, 8191, P.n - 1])
+    assert np.linalg.norm(Pg[rows] - Po[rows]) / np.linalg.norm(Po[rows]) <= 1e-8
+    del Po
+    _, rl, _ = ctx.pcg_solve(P.y, P.tol)
+    ctx.set_preconditioner(L.PRECOND_JACOBI)
+    _, rj, _ = ctx.pcg_solve(P.y, P.tol)
+    assert rl[0]["termination"] == rj[0]["termination"] == L.TERM_RESIDUAL_TOL
+    assert rl[0]["iters"] < rj[0]["iters"]
