@@ -184,6 +184,8 @@ def run_ours(args, rank, world, local_rank):
         obj = [L.laker_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    elif os.environ.get("LAKER_BENCH_NCCL") == "1":   # exercise the collective path on one GPU
+        nccl_id = L.laker_get_unique_id()
     ctx = L.Context(local_rank, rank, world, nccl_id, stream.cuda_stream)
 
     dev = torch.device("cuda", local_rank)

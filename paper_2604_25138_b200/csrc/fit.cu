@@ -349,7 +349,6 @@ double host_rho(int64_t nr, int64_t n, double gamma, double lmin, double rho_flo
 }  // namespace
 
 laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_report *rep) {
-  if (ctx->world != 1) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: multi-rank LEARNED not built in this version");
   const int64_t n = ctx->n, ld = ctx->ld;
   int64_t nr = o.n_dirs;
   if (nr <= 0) nr = std::min<int64_t>(n, std::max<int64_t>((int64_t)std::ceil(8.0 * std::sqrt((double)n)),
@@ -393,6 +392,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   LAKER_CUDA(ctx, mem.alloc(&flag, 1));
   LAKER_CUDA(ctx, mem.alloc(&sc, 1));
   LAKER_CUDA(ctx, cudaMemsetAsync(Zt, 0, big * 8, s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(Ut, 0, big * 8, s));  // padding columns [n, ld) must stay zero
   LAKER_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), s));
   LAKER_CUDA(ctx, cudaMemsetAsync(b, 0, nrp * 8, s));
   const bool debug = std::getenv("LAKER_DEBUG_FIT") != nullptr;
@@ -427,18 +427,36 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     philox_normal_kernel<<<4 * ctx->num_sms, 256, 0, s>>>(Zt, ld, n, nr, o.seed);
     ++L;
   }
-  {
+  if (!ctx->comm) {
     GemmArgs g{};
     g.M = nrp; g.N = n; g.K = ld;
     g.A = Zt; g.lda = ld; g.B = ctx->K; g.ldb = ld;  // K symmetric: Zt K^T = Zt K
     g.C = Ut; g.ldc = ld; g.alpha = 1.0; g.beta = ctx->lambda; g.Cin = Zt; g.ldcin = ld;
     launch_dgemm(g, false, s);
     ++L;
+  } else {
+    // row-sharded K: this rank forms the columns [r0, r1) of U^T = Zt K^T + lambda Zt,
+    // the W column blocks are all-gathered and the rest of the fit runs replicated
+    // (identical kernels on identical data on every rank).
+    const int64_t nloc = ctx->r1 - ctx->r0;
+    double *Uloc, *Urecv;
+    LAKER_CUDA(ctx, mem.alloc(&Uloc, (size_t)nrp * nloc));
+    LAKER_CUDA(ctx, mem.alloc(&Urecv, (size_t)nrp * nloc * ctx->world));
+    GemmArgs g{};
+    g.M = nrp; g.N = nloc; g.K = ld;
+    g.A = Zt; g.lda = ld; g.B = ctx->K; g.ldb = ld;
+    g.C = Uloc; g.ldc = nloc; g.alpha = 1.0; g.beta = ctx->lambda; g.Cin = Zt + ctx->r0; g.ldcin = ld;
+    launch_dgemm(g, false, s);
+    LAKER_NCCL(ctx, ncclAllGather(Uloc, Urecv, (size_t)nrp * nloc, ncclDouble, ctx->comm, s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(Ut, 0, big * 8, s));
+    for (int w = 0; w < ctx->world; ++w)
+      LAKER_CUDA(ctx, cudaMemcpy2DAsync(Ut + (size_t)w * nloc, ld * 8, Urecv + (size_t)w * nrp * nloc, nloc * 8,
+                                        nloc * 8, nrp, cudaMemcpyDeviceToDevice, s));
+    ++L;
   }
   normalize_rows_kernel<<<(unsigned)nr, 256, 0, s>>>(Ut, ld, n);
   ++L;
   dbg("Ubar", Ut, nrp, ld, ld);
-  // padding columns of Ut (i >= n) are zero because Zt and K are zero padded.
 
   // ---- 2. shifted CholeskyQR3 of Ubar (rows of Ut): Ut <- Q^T, R = R3 R2 R1
   auto gram = [&](double *dst) {
@@ -625,19 +643,22 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       LAKER_CUDA(ctx, cudaMalloc(&ctx->P, (size_t)(ctx->r1 - ctx->r0) * ld * 8));
     }
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->P, 0, (size_t)(ctx->r1 - ctx->r0) * ld * 8, s));
+    // P_loc = (W_loc Q^T + Q_loc W^T) / 2 + a^{-1/2} I: entry (i, j) and entry (j, i) are
+    // formed from the same two dot products, so P is symmetric (the DMMA product is
+    // commutative in its operands) and each row is independent of the sharding.
     GemmArgs p{};
     p.M = ctx->r1 - ctx->r0; p.N = n; p.K = nrp;
     p.A = Wr + ctx->r0 * nrp; p.lda = nrp; p.B = Qr; p.ldb = nrp; p.C = ctx->P; p.ldc = ld;
-    p.alpha = 1.0; p.diag = 1.0 / std::sqrt(a); p.diag_offset = -ctx->r0;
+    p.alpha = 0.5; p.diag = 1.0 / std::sqrt(a); p.diag_offset = -ctx->r0;
     launch_dgemm(p, false, s);
-    ++L;
+    p.A = Qr + ctx->r0 * nrp; p.B = Wr; p.beta = 1.0; p.Cin = ctx->P; p.ldcin = ld; p.diag = 0.0;
+    launch_dgemm(p, false, s);
+    L += 2;
     if (n % 2 == 1) {  // the last double2 store of each row spilled one past n: restore zero padding
       LAKER_CUDA(ctx, cudaMemset2DAsync(ctx->P + n, ld * 8, 0, 8, ctx->r1 - ctx->r0, s));
     }
     dbg("Wt", Wt, nrp, ld, ld);
     dbg("P0", ctx->P, ctx->r1 - ctx->r0, n, ld);
-    symmetrize_kernel<<<dim3(cdiv(n, 256), (unsigned)n), 256, 0, s>>>(ctx->P, ld, n);
-    ++L;
   }
   // trace of Sigma* = n a + sum_k b_k C_kk
   double htr = 0.0;

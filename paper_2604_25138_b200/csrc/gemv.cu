@@ -187,7 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
     v = warp_reduce_pair(v);
     if (lane == 0) {
       *a.counter = 0u;
-      run_epilogue(a, pair_value(v));
+      if (a.epi == kEpiStorePair)
+        *a.pair_out = v;
+      else
+        run_epilogue(a, pair_value(v));
     }
   }
 }

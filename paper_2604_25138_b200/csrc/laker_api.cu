@@ -176,7 +176,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   }
   cudaMemset(c->counters, 0, laker::kNumCtr * sizeof(unsigned int));
   cudaMemset(c->flags, 0, 4 * sizeof(unsigned long long));
-  if (world > 1) {
+  if (nccl_id) {  // world > 1, or a 1-rank communicator (exercises the collective path)
     ncclUniqueId u;
     std::memcpy(u.internal, nccl_id, 128);
     if (ncclCommInitRank(&c->comm, world, u, rank) != ncclSuccess) {
@@ -322,8 +322,11 @@ laker_status laker_pcg_solve(laker_ctx ctx, int32_t nrhs, const double *Y, doubl
   double total = 0.0;
   for (int32_t j = 0; j < nrhs; ++j) {
     laker_solve_report rep{};
-    laker_status sj = laker::pcg_solve_device(ctx, yv.dptr + (size_t)j * n, av.dptr + (size_t)j * n, *opts,
-                                              &rep, j == 0 ? history : nullptr);
+    laker_status sj =
+        ctx->comm ? laker::pcg_solve_dist(ctx, yv.dptr + (size_t)j * n, av.dptr + (size_t)j * n, *opts, &rep,
+                                          j == 0 ? history : nullptr)
+                  : laker::pcg_solve_device(ctx, yv.dptr + (size_t)j * n, av.dptr + (size_t)j * n, *opts, &rep,
+                                            j == 0 ? history : nullptr);
     total += rep.seconds;
     if (reports) reports[j] = rep;
     if (sj != LAKER_OK && st == LAKER_OK) st = sj;
@@ -461,12 +464,14 @@ laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y) {
   CHECK_CTX(ctx);
   if (!ctx->assembled) return set_err(ctx, LAKER_ERR_NOT_READY, "apply: assemble first");
   if (!x || !y) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "apply: NULL");
-  if (ctx->world != 1) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "apply: multi-rank not built in this version");
   cudaSetDevice(ctx->device);
   DevView xv, yv;
   LAKER_TRY(view_in(ctx, x, (size_t)ctx->n, xv));
   LAKER_TRY(view_out(ctx, y, (size_t)ctx->n, yv));
-  LAKER_TRY(laker::apply_operator_device(ctx, xv.dptr, yv.dptr));
+  if (ctx->comm)
+    LAKER_TRY(laker::apply_operator_dist(ctx, xv.dptr, yv.dptr));
+  else
+    LAKER_TRY(laker::apply_operator_device(ctx, xv.dptr, yv.dptr));
   LAKER_TRY(flush_out(ctx, yv));
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return LAKER_OK;

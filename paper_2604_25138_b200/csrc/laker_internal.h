@@ -91,7 +91,7 @@ laker_status cuda_err(laker_ctx ctx, cudaError_t e, const char *what);
 // (row stride ld, n logical columns, zero padded), Dot2 rows, bulk-TMA staged.
 // Also reduces dot(x[row0 .. row0+rows), y) over all CTAs into a pair and runs
 // `epi` on it in the last CTA.
-enum GemvEpi { kEpiNone = 0, kEpiDelta = 1, kEpiBeta = 2, kEpiStoreDot = 3 };
+enum GemvEpi { kEpiNone = 0, kEpiDelta = 1, kEpiBeta = 2, kEpiStoreDot = 3, kEpiStorePair = 4 };
 struct GemvArgs {
   const double *A;
   int64_t ld;
@@ -105,6 +105,7 @@ struct GemvArgs {
   dd_pair *partials;      // >= gridDim
   unsigned int *counter;  // ticket
   double *dot_out;        // kEpiStoreDot target
+  dd_pair *pair_out;      // kEpiStorePair target (unrounded Dot2 pair, for the rank-order combine)
   int epi;
   bool evict_first;       // stream A with an L2 evict-first policy
 };
@@ -168,5 +169,19 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
 laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,
                               laker_solve_report *rep, double *history);
 laker_status apply_operator_device(laker_ctx ctx, const double *x, double *y);
+
+// -------------------------------------------------------------- pcg_dist.cu
+// Row-sharded PCG over NCCL (ctx->comm != nullptr): identical recurrence,
+// scalars combined from per-rank unrounded Dot2 pairs in rank order.
+laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,
+                            laker_solve_report *rep, double *history);
+laker_status apply_operator_dist(laker_ctx ctx, const double *x, double *y);
+laker_status nccl_err(laker_ctx ctx, ncclResult_t r, const char *what);
+
+#define LAKER_NCCL(ctx, call)                                        \
+  do {                                                               \
+    ncclResult_t _r = (call);                                        \
+    if (_r != ncclSuccess) return ::laker::nccl_err(ctx, _r, #call);  \
+  } while (0)
 
 }  // namespace laker

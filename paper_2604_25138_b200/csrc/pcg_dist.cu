@@ -1,0 +1,449 @@
+// Row-sharded PCG over NCCL (BASELINE.json north_star: "K is sharded by row
+// blocks. Each iteration all-gathers the search direction and all-reduces the
+// scalars").  Rank r owns rows [r n/W, (r+1) n/W) of K
+// and P and the same slices of alpha, r, q, theta; p is kept full on every
+// rank and updated redundantly.  Per iteration (dense P):
+//   q_loc = (lambda I + K_loc) p            gemv, unrounded Dot2 pair of p_loc.q_loc
+//   allgather(pair)                          -> every rank sums the W pairs in rank
+//                                               order: identical delta everywhere
+//   alpha_loc, r_loc update; pair ||r_loc||^2 (and r.theta for Jacobi)
+//   allgather([r_loc | pairs])               -> full r; ||r||/||y|| test on every rank
+//   theta_loc = P_loc r                      gemv, pair r_loc.theta_loc
+//   allgather([theta_loc | pair])            -> full theta; beta
+//   p = theta + beta p                       (full, redundant)
+// With P = I or Jacobi the second and third exchanges merge into one.
+// Shipping the unrounded (s, c) pairs and rounding once after the rank-order
+// combine keeps every scalar the correctly rounded global value in practice, so
+// iteration counts and alpha do not depend on W.
+#include "pcg_kernels.cuh"
+
+namespace laker {
+namespace {
+
+__device__ __forceinline__ double sum_rank_pairs(const double *buf, int64_t stride, int64_t off, int W) {
+  dd_pair t = {0.0, 0.0};
+  for (int w = 0; w < W; ++w) {
+    dd_pair o = {buf[w * stride + off], buf[w * stride + off + 1]};
+    pair_add(t, o);
+  }
+  return pair_value(t);
+}
+
+// delta from the gathered p.q pairs; alpha_loc, r_loc update; pack [vec | rr | rt].
+__global__ void __launch_bounds__(kVecThreads) dist_update_kernel(
+    int64_t nloc, int64_t r0, int pk, const double *__restrict__ dvec, const double *__restrict__ p_full,
+    const double *__restrict__ q_loc, double *__restrict__ alpha_loc, double *__restrict__ r_loc,
+    double *__restrict__ send, const double *__restrict__ pq_recv, int W, PcgState *st, dd_pair *partials,
+    unsigned int *counter) {
+  if (*(volatile int32_t *)&st->done) return;
+  const double pq = sum_rank_pairs(pq_recv, 2, 0, W);
+  if (!(pq > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->term = LAKER_TERM_BREAKDOWN;
+      st->done = 1;
+    }
+    return;
+  }
+  const double delta = __ddiv_rn(st->rho, pq);
+  dd_pair v[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += (int64_t)gridDim.x * blockDim.x) {
+    alpha_loc[i] = __fma_rn(delta, p_full[r0 + i], alpha_loc[i]);
+    const double ri = __fma_rn(-delta, q_loc[i], r_loc[i]);
+    r_loc[i] = ri;
+    dot2_step(v[0], ri, ri);
+    double th = ri;
+    if (pk == LAKER_PRECOND_JACOBI) {
+      th = __dmul_rn(dvec[r0 + i], ri);
+      dot2_step(v[1], ri, th);
+    }
+    send[i] = (pk == LAKER_PRECOND_JACOBI) ? th : ri;
+  }
+  double tot[2];
+  // reduce to one pair per quantity; the last block stores the unrounded pairs
+  __shared__ dd_pair sred[kVecThreads / 32][2];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int k = 0; k < 2; ++k) {
+    dd_pair r = warp_reduce_pair(v[k]);
+    if (lane == 0) sred[warp][k] = r;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k) {
+      dd_pair t = sred[0][k];
+      for (int w = 1; w < kVecThreads / 32; ++w) pair_add(t, sred[w][k]);
+      partials[blockIdx.x * 2 + k] = t;
+    }
+    __threadfence();
+    s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  (void)tot;
+  if (s_last && warp == 0) {
+    __threadfence();
+    for (int k = 0; k < 2; ++k) {
+      dd_pair t = {0.0, 0.0};
+      for (int b = lane; b < (int)gridDim.x; b += 32) {
+        dd_pair o = {__ldcg(&partials[b * 2 + k].s), __ldcg(&partials[b * 2 + k].c)};
+        pair_add(t, o);
+      }
+      t = warp_reduce_pair(t);
+      if (lane == 0) {
+        send[nloc + 2 * k] = t.s;
+        send[nloc + 2 * k + 1] = t.c;
+      }
+    }
+    if (lane == 0) {
+      *counter = 0u;
+      st->delta = delta;
+    }
+  }
+}
+
+// Unpack [vec | rr | rt] x W into the full vector; block 0 runs the scalar step:
+// rel = ||r||/||y||, termination; for P = I / Jacobi also beta.
+__global__ void __launch_bounds__(kVecThreads) dist_unpack_r_kernel(int64_t nloc, int W, int pk,
+                                                                   const double *__restrict__ recv,
+                                                                   double *__restrict__ full, PcgState *st,
+                                                                   double *history) {
+  if (*(volatile int32_t *)&st->done) return;
+  const int64_t stride = nloc + 4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * W; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = e / nloc, i = e % nloc;
+    full[w * nloc + i] = recv[w * stride + i];
+  }
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const double rr = sum_rank_pairs(recv, stride, nloc, W);
+  const double rel = __ddiv_rn(__dsqrt_rn(rr), st->ynorm);
+  const int it = st->iters + 1;
+  st->iters = it;
+  st->rel = rel;
+  if (history) history[it - 1] = rel;
+  if (rel <= st->tol) {
+    st->term = LAKER_TERM_RESIDUAL_TOL;
+    st->done = 1;
+    return;
+  }
+  if (pk == LAKER_PRECOND_NONE || pk == LAKER_PRECOND_JACOBI) {
+    const double rho_new = (pk == LAKER_PRECOND_NONE) ? rr : sum_rank_pairs(recv, stride, nloc + 2, W);
+    if (!(rho_new > 0.0)) {
+      st->term = LAKER_TERM_INDEFINITE;
+      st->done = 1;
+      return;
+    }
+    st->beta = __ddiv_rn(rho_new, st->rho);
+    st->rho = rho_new;
+    if (it >= st->max_iters) {
+      st->term = LAKER_TERM_MAX_ITERS;
+      st->done = 1;
+    }
+  }
+}
+
+// Dense P: unpack [theta_loc | r.theta pair] x W; beta (or rho at init); budget.
+__global__ void __launch_bounds__(kVecThreads) dist_unpack_theta_kernel(int64_t nloc, int W,
+                                                                       const double *__restrict__ recv,
+                                                                       double *__restrict__ theta_full,
+                                                                       double *__restrict__ p_full, int init,
+                                                                       PcgState *st) {
+  if (*(volatile int32_t *)&st->done) return;
+  const int64_t stride = nloc + 2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * W; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = e / nloc, i = e % nloc;
+    const double th = recv[w * stride + i];
+    theta_full[w * nloc + i] = th;
+    if (init) p_full[w * nloc + i] = th;
+  }
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const double rho_new = sum_rank_pairs(recv, stride, nloc, W);
+  if (!(rho_new > 0.0)) {
+    st->term = LAKER_TERM_INDEFINITE;
+    st->done = 1;
+    return;
+  }
+  if (init) {
+    st->rho = rho_new;
+    return;
+  }
+  st->beta = __ddiv_rn(rho_new, st->rho);
+  st->rho = rho_new;
+  if (st->iters >= st->max_iters) {
+    st->term = LAKER_TERM_MAX_ITERS;
+    st->done = 1;
+  }
+}
+
+// unrounded pair of x.y over n elements, stored by the last block (on-the-fly operator)
+__global__ void __launch_bounds__(kVecThreads) local_pair_kernel(int64_t n, const double *__restrict__ x,
+                                                                 const double *__restrict__ y, double *out,
+                                                                 const PcgState *st, dd_pair *partials,
+                                                                 unsigned int *counter, int residual) {
+  if (st && *(volatile const int32_t *)&st->done) return;
+  __shared__ dd_pair sred[kVecThreads / 32];
+  __shared__ int s_last;
+  dd_pair v = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (residual) {
+      const double t = __dsub_rn(x[i], y[i]);
+      dot2_step(v, t, t);
+    } else {
+      dot2_step(v, x[i], y[i]);
+    }
+  }
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  v = warp_reduce_pair(v);
+  if (lane == 0) sred[warp] = v;
+  __syncthreads();
+  if (tid == 0) {
+    dd_pair t = sred[0];
+    for (int w = 1; w < kVecThreads / 32; ++w) pair_add(t, sred[w]);
+    partials[blockIdx.x] = t;
+    __threadfence();
+    s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && warp == 0) {
+    __threadfence();
+    dd_pair t = {0.0, 0.0};
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      dd_pair o = {__ldcg(&partials[b].s), __ldcg(&partials[b].c)};
+      pair_add(t, o);
+    }
+    t = warp_reduce_pair(t);
+    if (lane == 0) {
+      out[0] = t.s;
+      out[1] = t.c;
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void dist_true_residual_kernel(const double *recv, int W, const PcgState *st, double *out) {
+  const double rr = sum_rank_pairs(recv, 2, 0, W);
+  *out = st->ynorm > 0.0 ? __ddiv_rn(__dsqrt_rn(rr), st->ynorm) : 0.0;
+}
+
+}  // namespace
+
+laker_status nccl_err(laker_ctx ctx, ncclResult_t r, const char *what) {
+  return set_err(ctx, LAKER_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+// q_loc = (lambda I + K_loc) p_full; the unrounded local pair p_loc.q_loc -> pair_out
+static void dist_operator(laker_ctx ctx, const double *p_full, double *q_loc, PcgState *st, double *pair_out) {
+  const int64_t nloc = ctx->r1 - ctx->r0;
+  if (ctx->storage == LAKER_STORE_MATERIALIZED) {
+    GemvArgs a{};
+    a.A = ctx->K; a.ld = ctx->ld; a.rows = nloc; a.ncols = ctx->n; a.x = p_full; a.row0 = ctx->r0;
+    a.y = q_loc; a.lambda = ctx->lambda; a.state = st; a.partials = ctx->partials;
+    a.counter = ctx->counters + kCtrGemv; a.epi = pair_out ? kEpiStorePair : kEpiNone;
+    a.pair_out = reinterpret_cast<dd_pair *>(pair_out); a.evict_first = true;
+    launch_gemv(a, ctx->gemv_grid, ctx->stream);
+  } else {
+    launch_kernel_matvec_exact(ctx->E + ctx->r0 * ctx->d, nloc, ctx->E, ctx->n, ctx->d, ctx->scale, p_full,
+                               ctx->lambda, p_full + ctx->r0, q_loc, ctx->flags, st ? &st->done : nullptr,
+                               ctx->stream);
+    if (pair_out) {
+      const int g = (int)std::min<int64_t>(2 * ctx->num_sms, (nloc + kVecThreads - 1) / kVecThreads);
+      local_pair_kernel<<<g, kVecThreads, 0, ctx->stream>>>(nloc, p_full + ctx->r0, q_loc, pair_out, st,
+                                                             ctx->partials, ctx->counters + kCtrMisc, 0);
+      ctx->stats.kernel_launches++;
+    }
+  }
+  ctx->stats.kernel_launches++;
+}
+
+laker_status apply_operator_dist(laker_ctx ctx, const double *x, double *y) {
+  const int64_t nloc = ctx->r1 - ctx->r0;
+  cudaStream_t s = ctx->stream;
+  double *xp = nullptr, *ql = nullptr;
+  LAKER_CUDA(ctx, cudaMallocAsync(&xp, ctx->ld * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&ql, nloc * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(xp, 0, ctx->ld * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(xp, x, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  dist_operator(ctx, xp, ql, nullptr, nullptr);
+  LAKER_NCCL(ctx, ncclAllGather(ql, y, nloc, ncclDouble, ctx->comm, s));
+  LAKER_CUDA(ctx, cudaGetLastError());
+  cudaFreeAsync(xp, s);
+  cudaFreeAsync(ql, s);
+  return LAKER_OK;
+}
+
+laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, const laker_solve_opts &o,
+                            laker_solve_report *rep, double *history) {
+  const int64_t n = ctx->n, ld = ctx->ld, r0 = ctx->r0, nloc = ctx->r1 - ctx->r0;
+  const int W = ctx->world;
+  const int pk = ctx->precond_kind;
+  const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
+  if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
+  const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
+  cudaStream_t s = ctx->stream;
+
+  // full vectors (ld): y, r (full copy for dense P), theta, p, alpha_full; local: alpha, r, q;
+  // exchange buffers: pq pair, [vec|4] send/recv, [theta|2] send/recv, scalars.
+  double *base = nullptr;
+  const size_t nfull = 5 * (size_t)ld, nl = 3 * (size_t)nloc;
+  const size_t nx = 2 + 2 * (size_t)W + (nloc + 4) + (size_t)W * (nloc + 4) + (nloc + 2) + (size_t)W * (nloc + 2) + 4;
+  LAKER_CUDA(ctx, cudaMallocAsync(&base, (nfull + nl + nx) * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(base, 0, (nfull + nl + nx) * sizeof(double), s));
+  double *yf = base, *rf = yf + ld, *thf = rf + ld, *pf = thf + ld, *af = pf + ld;
+  double *al = af + ld, *rl = al + nloc, *ql = rl + nloc;
+  double *pq_send = ql + nloc, *pq_recv = pq_send + 2, *vsend = pq_recv + 2 * W, *vrecv = vsend + (nloc + 4);
+  double *tsend = vrecv + (size_t)W * (nloc + 4), *trecv = tsend + (nloc + 2), *scal = trecv + (size_t)W * (nloc + 2);
+  PcgState *st = nullptr;
+  double *hist = nullptr;
+  LAKER_CUDA(ctx, cudaMallocAsync(&st, sizeof(PcgState), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&hist, (size_t)max_iters * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(yf, y, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(rl, y + r0, nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  PcgState h0{};
+  h0.tol = o.tol;
+  h0.max_iters = max_iters;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+
+  const int vg = (int)std::min<int64_t>(2 * ctx->num_sms, (n + kVecThreads - 1) / kVecThreads);
+  const int lg = (int)std::min<int64_t>(2 * ctx->num_sms, (nloc + kVecThreads - 1) / kVecThreads);
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, s);
+  // init: ||y|| on the full (replicated) y; alpha = 0; r_full = y
+  pcg_init_kernel<<<vg, kVecThreads, 0, s>>>(n, yf, af, rf, st, ctx->partials, ctx->counters + kCtrInit);
+  ctx->stats.kernel_launches++;
+  if (dense) {
+    GemvArgs a{};
+    a.A = ctx->P; a.ld = ld; a.rows = nloc; a.ncols = n; a.x = rf; a.row0 = r0; a.y = tsend; a.lambda = 0.0;
+    a.state = st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.epi = kEpiStorePair;
+    a.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc); a.evict_first = true;
+    launch_gemv(a, ctx->gemv_grid, s);
+    LAKER_NCCL(ctx, ncclAllGather(tsend, trecv, nloc + 2, ncclDouble, ctx->comm, s));
+    dist_unpack_theta_kernel<<<vg, kVecThreads, 0, s>>>(nloc, W, trecv, thf, pf, 1, st);
+    ctx->stats.kernel_launches += 2;
+  } else {
+    // theta = r (none) or d o r (Jacobi) on the full vector, p = theta, rho = r.theta
+    pcg_first_dir_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, rf, thf, pf, st, ctx->partials,
+                                                    ctx->counters + kCtrInit);
+    ctx->stats.kernel_launches++;
+  }
+  LAKER_CUDA(ctx, cudaGetLastError());
+
+  const double *theta_src = dense ? thf : (pk == LAKER_PRECOND_NONE ? rf : thf);
+  const int chunk = n >= 8192 ? 8 : (n >= 2048 ? 32 : 64);
+  const bool instr = o.instrument != 0;
+  std::vector<cudaEvent_t> evs;
+  if (instr) {
+    evs.resize(4 * chunk);
+    for (auto &e : evs) cudaEventCreate(&e);
+  }
+  laker_status err = LAKER_OK;
+  auto record_iteration = [&](int j) {
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
+    dist_operator(ctx, pf, ql, st, pq_send);
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
+    if (ncclAllGather(pq_send, pq_recv, 2, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    dist_update_kernel<<<lg, kVecThreads, 0, s>>>(nloc, r0, pk, ctx->Pdiag, pf, ql, al, rl, vsend, pq_recv, W, st,
+                                                  ctx->partials, ctx->counters + kCtrUpdate);
+    if (ncclAllGather(vsend, vrecv, nloc + 4, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    // dense: the exchange carried r; otherwise theta (Jacobi) or r (= theta, none)
+    dist_unpack_r_kernel<<<vg, kVecThreads, 0, s>>>(nloc, W, pk, vrecv, dense ? rf : (pk == LAKER_PRECOND_NONE ? rf : thf),
+                                                    st, hist);
+    ctx->stats.kernel_launches += 2;
+    if (dense) {
+      if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
+      GemvArgs a{};
+      a.A = ctx->P; a.ld = ld; a.rows = nloc; a.ncols = n; a.x = rf; a.row0 = r0; a.y = tsend; a.lambda = 0.0;
+      a.state = st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.epi = kEpiStorePair;
+      a.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc); a.evict_first = true;
+      launch_gemv(a, ctx->gemv_grid, s);
+      if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
+      if (ncclAllGather(tsend, trecv, nloc + 2, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+      dist_unpack_theta_kernel<<<vg, kVecThreads, 0, s>>>(nloc, W, trecv, thf, pf, 0, st);
+      ctx->stats.kernel_launches += 2;
+    }
+    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, pf, st);
+    ctx->stats.kernel_launches++;
+  };
+
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const int64_t launches_before = ctx->stats.kernel_launches;
+  LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int j = 0; j < chunk; ++j) record_iteration(j);
+  LAKER_CUDA(ctx, cudaStreamEndCapture(s, &graph));
+  if (err != LAKER_OK) return set_err(ctx, err, "ncclAllGather failed during capture");
+  const int64_t per_chunk = ctx->stats.kernel_launches - launches_before;
+  ctx->stats.kernel_launches = launches_before;
+  LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec, graph, 0));
+
+  PcgState *hs = nullptr;
+  LAKER_CUDA(ctx, cudaMallocHost(&hs, sizeof(PcgState)));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hs, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  int32_t iters_prev = 0;
+  while (!hs->done) {
+    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
+    ctx->stats.kernel_launches += per_chunk;
+    LAKER_CUDA(ctx, cudaMemcpyAsync(hs, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    if (instr) {
+      const int ran = hs->iters - iters_prev;
+      for (int j = 0; j < std::min(ran, chunk); ++j) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, evs[4 * j + 0], evs[4 * j + 1]) != cudaSuccess) { cudaGetLastError(); ms = 0.f; }
+        ctx->stats.op_ms += ms;
+        ctx->stats.op_launches++;
+        if (dense && (j < ran - 1 || !hs->done || hs->term != LAKER_TERM_RESIDUAL_TOL)) {
+          if (cudaEventElapsedTime(&ms, evs[4 * j + 2], evs[4 * j + 3]) != cudaSuccess) { cudaGetLastError(); ms = 0.f; }
+          ctx->stats.prec_ms += ms;
+          ctx->stats.prec_launches++;
+        }
+      }
+    }
+    iters_prev = hs->iters;
+  }
+  cudaEventRecord(ev1, s);
+
+  // alpha_full on every rank, true residual over the shards
+  LAKER_NCCL(ctx, ncclAllGather(al, af, nloc, ncclDouble, ctx->comm, s));
+  dist_operator(ctx, af, ql, nullptr, nullptr);
+  local_pair_kernel<<<lg, kVecThreads, 0, s>>>(nloc, yf + r0, ql, pq_send, nullptr, ctx->partials,
+                                               ctx->counters + kCtrMisc, 1);
+  LAKER_NCCL(ctx, ncclAllGather(pq_send, pq_recv, 2, ncclDouble, ctx->comm, s));
+  dist_true_residual_kernel<<<1, 1, 0, s>>>(pq_recv, W, st, scal);
+  ctx->stats.kernel_launches += 2;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(alpha_out, af, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  double true_rel = 0.0;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(&true_rel, scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hs, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  if (history && hs->iters > 0)
+    LAKER_CUDA(ctx, cudaMemcpyAsync(history, hist, (size_t)hs->iters * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  ctx->stats.solve_ms = ms;
+  if (rep) {
+    rep->iters = hs->iters;
+    rep->termination = hs->term;
+    rep->rel_residual = hs->iters > 0 ? hs->rel : (hs->term == LAKER_TERM_ZERO_RHS ? 0.0 : 1.0);
+    rep->true_rel_residual = true_rel;
+    rep->seconds = ms * 1e-3;
+  }
+  const int term = hs->term;
+  cudaFreeHost(hs);
+  for (auto &e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaGraphExecDestroy(gexec);
+  cudaGraphDestroy(graph);
+  cudaFreeAsync(base, s);
+  cudaFreeAsync(st, s);
+  cudaFreeAsync(hist, s);
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  if (term == LAKER_TERM_BREAKDOWN) return set_err(ctx, LAKER_ERR_BREAKDOWN_ZERO_CURVATURE, "p.(lambda I + K)p <= 0");
+  if (term == LAKER_TERM_INDEFINITE) return set_err(ctx, LAKER_ERR_INDEFINITE_PRECONDITIONER, "r.theta <= 0");
+  return LAKER_OK;
+}
+
+}  // namespace laker

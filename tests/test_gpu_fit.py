@@ -42,7 +42,7 @@ def test_fit_matches_oracle(ctx, L, cid, n):
     assert abs(rep["sigma_min_eig"] / ro.sigma_min_eig - 1) <= 1e-8
     assert abs(rep["trace"] / P.n - 1) <= 1e-8
     assert rep["rho_used"] == ro.rho_used
-    assert (Pg == Pg.T).all()
+    assert (Pg == Pg.T).all()   # B4: (W Q^T + Q W^T)/2 is symmetric bitwise
     assert np.linalg.norm(Pg - Po) / np.linalg.norm(Po) <= 1e-8
 
 
@@ -75,7 +75,7 @@ def test_fit_device_rng_and_invariants(ctx, L):
     rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, seed=123)
     assert rep["converged"] == 1 and rep["n_dirs"] == O.nr_schedule(P.n)
     Pg = ctx.get_preconditioner_rows()
-    assert (Pg == Pg.T).all()
+    assert (Pg == Pg.T).all()   # B4: (W Q^T + Q W^T)/2 is symmetric bitwise
     w = np.linalg.eigvalsh(Pg)
     assert w[0] > 0
     # P = Sigma^{-1/2} with Sigma ~ (lambda I + K)^2 up to scale: kappa(P A) << kappa(A)
