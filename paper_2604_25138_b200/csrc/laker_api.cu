@@ -320,6 +320,15 @@ laker_status laker_pcg_solve(laker_ctx ctx, int32_t nrhs, const double *Y, doubl
   LAKER_TRY(view_out(ctx, alpha, (size_t)n * nrhs, av));
   laker_status st = LAKER_OK;
   double total = 0.0;
+  if (nrhs > 1 && !ctx->comm && ctx->storage == LAKER_STORE_MATERIALIZED && nrhs <= 256) {
+    // block solve: one GEMM-shaped pass over K (and P) per iteration for all columns
+    laker_status sb = laker::pcg_solve_block(ctx, nrhs, yv.dptr, av.dptr, *opts, reports, history);
+    if (sb == LAKER_OK || sb == LAKER_ERR_BREAKDOWN_ZERO_CURVATURE || sb == LAKER_ERR_INDEFINITE_PRECONDITIONER) {
+      LAKER_TRY(flush_out(ctx, av));
+      LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return sb;
+  }
   for (int32_t j = 0; j < nrhs; ++j) {
     laker_solve_report rep{};
     laker_status sj =

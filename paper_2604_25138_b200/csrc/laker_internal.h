@@ -176,6 +176,11 @@ laker_status apply_operator_device(laker_ctx ctx, const double *x, double *y);
 laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,
                             laker_solve_report *rep, double *history);
 laker_status apply_operator_dist(laker_ctx ctx, const double *x, double *y);
+
+// ------------------------------------------------------------- pcg_block.cu
+// nrhs independent recurrences sharing GEMM-shaped applies (multi-RHS, C4).
+laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *alpha,
+                             const laker_solve_opts &o, laker_solve_report *reps, double *history);
 laker_status nccl_err(laker_ctx ctx, ncclResult_t r, const char *what);
 
 #define LAKER_NCCL(ctx, call)                                        \

@@ -1,0 +1,448 @@
+// Multi-RHS PCG (BASELINE config C4: 64 independent radio
+// maps, reading R13): m independent Alg. 1 recurrences that share
+// every pass over K and P, so each operator / preconditioner apply is a GEMM
+// Q = (lambda I + K) X, Theta = P R with X, R, Q, Theta n x m row-major
+// (m contiguous RHS per row).
+//
+//  * EXACT: `gemm_dot2_kernel` -- one Dot2 pair per output entry, so column c
+//    of every apply equals the single-RHS Dot2 GEMV bitwise and the block
+//    solve reproduces the single-RHS solves column by column (T18).  fp64 ALU
+//    bound (10 flops per K-element and RHS).
+//  * FAST: the DMMA GEMM (dgemm.cu), K-element reuse m-fold: fp64 tensor bound.
+//
+// Per-column scalars (delta, beta, termination) come from fixed-order Dot2
+// column reductions; a converged column is frozen (its delta/beta are not
+// applied) while the others continue; the loop ends when every column is done.
+#include "pcg_kernels.cuh"
+
+namespace laker {
+namespace {
+
+constexpr int kBR = 32;   // rows of A per CTA
+constexpr int kBK = 32;   // k chunk
+constexpr int kBM = 64;   // RHS per CTA (columns)
+
+// Q[i][c] = RN(lambda X[row0+i][c] + sum_j A[i][j] X[j][c]), Dot2 per entry.
+__global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict__ A, int64_t lda, int64_t rows,
+                                                        int64_t kdim, const double *__restrict__ X, int64_t ldx,
+                                                        int64_t m, double *__restrict__ Q, int64_t ldq,
+                                                        double lambda, int64_t row0,
+                                                        const int32_t *__restrict__ all_done) {
+  if (all_done && *(volatile const int32_t *)all_done) return;
+  __shared__ double As[kBR][kBK + 1];
+  __shared__ __align__(16) double Xs[kBK][kBM];
+  const int tid = threadIdx.x;
+  const int tr = (tid >> 4) * 2;       // 2 rows
+  const int tc = (tid & 15) * 4;       // 4 columns
+  const int64_t R0 = (int64_t)blockIdx.x * kBR;
+  const int64_t C0 = (int64_t)blockIdx.y * kBM;
+  dd_pair acc[2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = dd_pair{0.0, 0.0};
+  if (lambda != 0.0) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (R0 + tr + a < rows && C0 + tc + b < m)
+          dot2_step(acc[a][b], lambda, X[(row0 + R0 + tr + a) * ldx + C0 + tc + b]);
+  }
+  for (int64_t k0 = 0; k0 < kdim; k0 += kBK) {
+    __syncthreads();
+    for (int e = tid; e < kBR * kBK; e += 256) {
+      const int r = e / kBK, c = e % kBK;
+      As[r][c] = (R0 + r < rows && k0 + c < kdim) ? A[(R0 + r) * lda + k0 + c] : 0.0;
+    }
+    for (int e = tid; e < kBK * kBM; e += 256) {
+      const int r = e / kBM, c = e % kBM;
+      Xs[r][c] = (k0 + r < kdim && C0 + c < m) ? X[(k0 + r) * ldx + C0 + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int j = 0; j < kBK; ++j) {
+      const double a0 = As[tr][j], a1 = As[tr + 1][j];
+      const double2 x01 = *reinterpret_cast<const double2 *>(&Xs[j][tc]);
+      const double2 x23 = *reinterpret_cast<const double2 *>(&Xs[j][tc + 2]);
+      dot2_step(acc[0][0], a0, x01.x);
+      dot2_step(acc[0][1], a0, x01.y);
+      dot2_step(acc[0][2], a0, x23.x);
+      dot2_step(acc[0][3], a0, x23.y);
+      dot2_step(acc[1][0], a1, x01.x);
+      dot2_step(acc[1][1], a1, x01.y);
+      dot2_step(acc[1][2], a1, x23.x);
+      dot2_step(acc[1][3], a1, x23.y);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (R0 + tr + a < rows && C0 + tc + b < m) Q[(R0 + tr + a) * ldq + C0 + tc + b] = pair_value(acc[a][b]);
+}
+
+enum ColMode { kColInit = 0, kColDelta = 1, kColUpdate = 2, kColBeta = 3, kColTrue = 4 };
+
+struct BlockArgs {
+  int64_t n, m, ldv;   // rows, RHS count, row stride of the n x m blocks
+  int mode, pk;
+  const double *Y;
+  double *alpha, *r, *theta, *p, *q;
+  const double *dvec;
+  PcgState *st;        // [m]
+  double *hist;        // [max_iters] column 0
+  int32_t *all_done;
+  double *true_rel;    // [m]
+  dd_pair *partials;   // [grid][m][2]
+  unsigned int *counter;
+};
+
+__device__ void column_epilogue(const BlockArgs &a, int col);
+
+// Column Dot2 reductions over the n x m blocks with the per-element work and
+// the per-column scalar logic of each PCG phase.  Block b owns a contiguous
+// row range; thread = (column c = tid % m, row lane = tid / m).
+__global__ void __launch_bounds__(256) block_col_kernel(const BlockArgs a) {
+  if (a.mode != kColTrue && a.all_done && *(volatile int32_t *)a.all_done) return;
+  const int64_t m = a.m;
+  const int lanes = 256 / (int)m;
+  const int c = threadIdx.x % m, ln = threadIdx.x / m;
+  const bool act = ln < lanes;
+  const int64_t rows_per = (a.n + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * rows_per, i1 = imin64(a.n, i0 + rows_per);
+  PcgState &st = a.st[c];
+  const bool col_done = st.done != 0;
+  double delta = 0.0;
+  if (a.mode == kColUpdate && !col_done) delta = st.delta;
+  dd_pair v0 = {0.0, 0.0}, v1 = {0.0, 0.0};
+  if (act && (!col_done || a.mode == kColInit || a.mode == kColTrue)) {
+    for (int64_t i = i0 + ln; i < i1; i += lanes) {
+      const int64_t e = i * a.ldv + c;
+      switch (a.mode) {
+        case kColInit: {  // alpha = 0, r = y, ||y||^2; theta^0 = P r (none/jacobi), p = theta, rho
+          const double yi = a.Y[i + c * a.n];
+          a.alpha[e] = 0.0;
+          a.r[e] = yi;
+          dot2_step(v0, yi, yi);
+          if (a.pk != LAKER_PRECOND_EXTERNAL_DENSE && a.pk != LAKER_PRECOND_LEARNED) {
+            const double th = (a.pk == LAKER_PRECOND_JACOBI) ? __dmul_rn(a.dvec[i], yi) : yi;
+            a.theta[e] = th;
+            a.p[e] = th;
+            dot2_step(v1, yi, th);
+          }
+          break;
+        }
+        case kColDelta:  // p.q
+          dot2_step(v0, a.p[e], a.q[e]);
+          break;
+        case kColUpdate: {
+          a.alpha[e] = __fma_rn(delta, a.p[e], a.alpha[e]);
+          const double ri = __fma_rn(-delta, a.q[e], a.r[e]);
+          a.r[e] = ri;
+          dot2_step(v0, ri, ri);
+          if (a.pk == LAKER_PRECOND_JACOBI) {
+            const double th = __dmul_rn(a.dvec[i], ri);
+            a.theta[e] = th;
+            dot2_step(v1, ri, th);
+          } else if (a.pk == LAKER_PRECOND_NONE) {
+            a.theta[e] = ri;
+          }
+          break;
+        }
+        case kColBeta:  // r.theta (dense P); kColInit for dense also lands here via rho0
+          dot2_step(v0, a.r[e], a.theta[e]);
+          break;
+        case kColTrue: {
+          const double t = __dsub_rn(a.Y[i + c * a.n], a.q[e]);
+          dot2_step(v0, t, t);
+          break;
+        }
+      }
+    }
+  }
+  // reduce over the row lanes of this block (fixed order), then over blocks
+  __shared__ dd_pair red[256][2];
+  red[threadIdx.x][0] = v0;
+  red[threadIdx.x][1] = v1;
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x < m) {
+    dd_pair t0 = red[threadIdx.x][0], t1 = red[threadIdx.x][1];
+    for (int l = 1; l < lanes; ++l) {
+      pair_add(t0, red[l * m + threadIdx.x][0]);
+      pair_add(t1, red[l * m + threadIdx.x][1]);
+    }
+    a.partials[((int64_t)blockIdx.x * m + threadIdx.x) * 2] = t0;
+    a.partials[((int64_t)blockIdx.x * m + threadIdx.x) * 2 + 1] = t1;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  const bool last = s_last != 0;
+  if (last && threadIdx.x < m) column_epilogue(a, threadIdx.x);
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    int all = 1;
+    for (int k = 0; k < (int)m; ++k) all &= a.st[k].done != 0;
+    *a.all_done = all;
+    *a.counter = 0u;
+  }
+}
+
+__device__ void column_epilogue(const BlockArgs &a, int col) {
+  const int64_t m = a.m;
+  __threadfence();
+  dd_pair t0 = {0.0, 0.0}, t1 = {0.0, 0.0};
+  for (unsigned b = 0; b < gridDim.x; ++b) {
+    const dd_pair *pp = a.partials + ((int64_t)b * m + col) * 2;
+    dd_pair o0 = {__ldcg(&pp[0].s), __ldcg(&pp[0].c)}, o1 = {__ldcg(&pp[1].s), __ldcg(&pp[1].c)};
+    pair_add(t0, o0);
+    pair_add(t1, o1);
+  }
+  const double s0 = pair_value(t0), s1 = pair_value(t1);
+  PcgState &S = a.st[col];
+  switch (a.mode) {
+    case kColInit:
+      S.ynorm = __dsqrt_rn(s0);
+      S.iters = 0;
+      S.rel = 1.0;
+      if (S.ynorm == 0.0) {
+        S.done = 1;
+        S.term = LAKER_TERM_ZERO_RHS;
+      } else if (a.pk != LAKER_PRECOND_EXTERNAL_DENSE && a.pk != LAKER_PRECOND_LEARNED) {
+        S.rho = s1;
+        if (!(s1 > 0.0)) {
+          S.done = 1;
+          S.term = LAKER_TERM_INDEFINITE;
+        }
+      }
+      break;
+    case kColDelta:
+      if (!S.done) {
+        if (!(s0 > 0.0)) {
+          S.done = 1;
+          S.term = LAKER_TERM_BREAKDOWN;
+          S.delta = 0.0;
+        } else {
+          S.delta = __ddiv_rn(S.rho, s0);
+        }
+      }
+      break;
+    case kColUpdate:
+      if (!S.done) {
+        const double rel = __ddiv_rn(__dsqrt_rn(s0), S.ynorm);
+        const int it = S.iters + 1;
+        S.iters = it;
+        S.rel = rel;
+        if (col == 0 && a.hist) a.hist[it - 1] = rel;
+        if (rel <= S.tol) {
+          S.term = LAKER_TERM_RESIDUAL_TOL;
+          S.done = 1;
+        } else if (a.pk == LAKER_PRECOND_NONE || a.pk == LAKER_PRECOND_JACOBI) {
+          const double rho_new = (a.pk == LAKER_PRECOND_NONE) ? s0 : s1;
+          if (!(rho_new > 0.0)) {
+            S.term = LAKER_TERM_INDEFINITE;
+            S.done = 1;
+          } else {
+            S.beta = __ddiv_rn(rho_new, S.rho);
+            S.rho = rho_new;
+            if (it >= S.max_iters) {
+              S.term = LAKER_TERM_MAX_ITERS;
+              S.done = 1;
+            }
+          }
+        }
+      }
+      break;
+    case kColBeta:
+      if (!S.done) {
+        if (!(s0 > 0.0)) {
+          S.term = LAKER_TERM_INDEFINITE;
+          S.done = 1;
+        } else if (S.iters == 0 && S.rho == 0.0) {  // initial rho for dense P
+          S.rho = s0;
+        } else {
+          S.beta = __ddiv_rn(s0, S.rho);
+          S.rho = s0;
+          if (S.iters >= S.max_iters) {
+            S.term = LAKER_TERM_MAX_ITERS;
+            S.done = 1;
+          }
+        }
+      }
+      break;
+    case kColTrue:
+      a.true_rel[col] = S.ynorm > 0.0 ? __ddiv_rn(__dsqrt_rn(s0), S.ynorm) : 0.0;
+      break;
+  }
+}
+
+// p = theta + beta p for active columns; p = theta at init (dense)
+__global__ void block_pupdate_kernel(int64_t n, int64_t m, int64_t ldv, const double *__restrict__ theta,
+                                     double *__restrict__ p, const PcgState *st, int init,
+                                     const int32_t *all_done) {
+  if (*(volatile const int32_t *)all_done) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, c = e % m;
+    if (st[c].done) continue;
+    const int64_t k = i * ldv + c;
+    p[k] = init ? theta[k] : __fma_rn(st[c].beta, p[k], theta[k]);
+  }
+}
+
+}  // namespace
+
+laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *alpha_out,
+                             const laker_solve_opts &o, laker_solve_report *reps, double *history) {
+  if (ctx->world != 1 || ctx->comm) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS: single rank only in this version");
+  if (ctx->storage != LAKER_STORE_MATERIALIZED) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS needs MATERIALIZED");
+  if (m > 256) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS: nrhs <= 256");
+  const int64_t n = ctx->n, ld = ctx->ld;
+  const int pk = ctx->precond_kind;
+  const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
+  if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
+  const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
+  const int64_t mp = (m + 1) / 2 * 2;  // even row stride for the DMMA epilogue
+  cudaStream_t s = ctx->stream;
+  double *base = nullptr;
+  const size_t blk = (size_t)ld * mp;
+  LAKER_CUDA(ctx, cudaMallocAsync(&base, 5 * blk * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(base, 0, 5 * blk * sizeof(double), s));
+  double *al = base, *rr = al + blk, *th = rr + blk, *pp = th + blk, *qq = pp + blk;
+  PcgState *st = nullptr;
+  double *hist = nullptr, *trel = nullptr;
+  int32_t *all_done = nullptr;
+  dd_pair *parts = nullptr;
+  const int cg = (int)std::min<int64_t>(2 * ctx->num_sms, (n + 63) / 64);
+  LAKER_CUDA(ctx, cudaMallocAsync(&st, m * sizeof(PcgState), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&hist, (size_t)max_iters * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&trel, m * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&all_done, sizeof(int32_t), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&parts, (size_t)cg * m * 2 * sizeof(dd_pair), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(all_done, 0, sizeof(int32_t), s));
+  std::vector<PcgState> h0(m);
+  for (auto &x : h0) {
+    x = PcgState{};
+    x.tol = o.tol;
+    x.max_iters = max_iters;
+  }
+  LAKER_CUDA(ctx, cudaMemcpyAsync(st, h0.data(), m * sizeof(PcgState), cudaMemcpyHostToDevice, s));
+
+  BlockArgs ba{};
+  ba.n = n; ba.m = m; ba.ldv = mp; ba.pk = pk; ba.Y = Y; ba.alpha = al; ba.r = rr; ba.theta = th; ba.p = pp;
+  ba.q = qq; ba.dvec = ctx->Pdiag; ba.st = st; ba.hist = hist; ba.all_done = all_done; ba.true_rel = trel;
+  ba.partials = parts; ba.counter = ctx->counters + kCtrMisc;
+  auto col = [&](int mode) {
+    BlockArgs b = ba;
+    b.mode = mode;
+    block_col_kernel<<<cg, 256, 0, s>>>(b);
+    ctx->stats.kernel_launches++;
+  };
+  const bool exact = ctx->mode == LAKER_MODE_EXACT;
+  auto apply = [&](const double *Amat, double lam, const double *X, double *Out, bool gated = true) {
+    if (exact) {
+      dim3 grid((unsigned)((n + kBR - 1) / kBR), (unsigned)((m + kBM - 1) / kBM));
+      gemm_dot2_kernel<<<grid, 256, 0, s>>>(Amat, ld, n, ld, X, mp, m, Out, mp, lam, 0, gated ? all_done : nullptr);
+    } else {
+      GemmArgs g{};
+      g.M = n; g.N = mp; g.K = ld; g.A = Amat; g.lda = ld; g.B = X; g.ldb = mp; g.C = Out; g.ldc = mp;
+      g.alpha = 1.0; g.beta = lam; g.Cin = X; g.ldcin = mp;
+      launch_dgemm(g, true, s);
+    }
+    ctx->stats.kernel_launches++;
+  };
+  const int vg = 2 * ctx->num_sms;
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, s);
+  col(kColInit);
+  if (dense) {
+    apply(ctx->P, 0.0, rr, th);
+    col(kColBeta);  // initial rho = r.theta
+    block_pupdate_kernel<<<vg, 256, 0, s>>>(n, m, mp, th, pp, st, 1, all_done);
+    ctx->stats.kernel_launches++;
+  }
+  const double *theta_src = th;
+  const int chunk = 4;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const int64_t before = ctx->stats.kernel_launches;
+  LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int j = 0; j < chunk; ++j) {
+    apply(ctx->K, ctx->lambda, pp, qq);
+    col(kColDelta);
+    col(kColUpdate);
+    if (dense) {
+      apply(ctx->P, 0.0, rr, th);
+      col(kColBeta);
+    }
+    block_pupdate_kernel<<<vg, 256, 0, s>>>(n, m, mp, theta_src, pp, st, 0, all_done);
+    ctx->stats.kernel_launches++;
+  }
+  LAKER_CUDA(ctx, cudaStreamEndCapture(s, &graph));
+  const int64_t per_chunk = ctx->stats.kernel_launches - before;
+  ctx->stats.kernel_launches = before;
+  LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec, graph, 0));
+  int32_t *hd = nullptr;
+  LAKER_CUDA(ctx, cudaMallocHost(&hd, sizeof(int32_t)));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hd, all_done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  while (!*hd) {
+    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
+    ctx->stats.kernel_launches += per_chunk;
+    LAKER_CUDA(ctx, cudaMemcpyAsync(hd, all_done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  }
+  cudaEventRecord(ev1, s);
+  // true residuals, alpha out (column-major n x m)
+  apply(ctx->K, ctx->lambda, al, qq, false);
+  col(kColTrue);
+  LAKER_CUDA(ctx, cudaMemcpy2DAsync(alpha_out, sizeof(double), al, mp * sizeof(double), sizeof(double), n,
+                                    cudaMemcpyDeviceToDevice, s));
+  for (int32_t c = 1; c < m; ++c)
+    LAKER_CUDA(ctx, cudaMemcpy2DAsync(alpha_out + (size_t)c * n, sizeof(double), al + c, mp * sizeof(double),
+                                      sizeof(double), n, cudaMemcpyDeviceToDevice, s));
+  std::vector<PcgState> hs(m);
+  std::vector<double> htr(m);
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hs.data(), st, m * sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(htr.data(), trel, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  if (history && hs[0].iters > 0)
+    LAKER_CUDA(ctx, cudaMemcpyAsync(history, hist, (size_t)hs[0].iters * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  ctx->stats.solve_ms = ms;
+  int worst = LAKER_TERM_RESIDUAL_TOL;
+  for (int32_t c = 0; c < m; ++c) {
+    if (reps) {
+      reps[c].iters = hs[c].iters;
+      reps[c].termination = hs[c].term;
+      reps[c].rel_residual = hs[c].iters > 0 ? hs[c].rel : (hs[c].term == LAKER_TERM_ZERO_RHS ? 0.0 : 1.0);
+      reps[c].true_rel_residual = htr[c];
+      reps[c].seconds = ms * 1e-3;
+    }
+    if (hs[c].term == LAKER_TERM_BREAKDOWN || hs[c].term == LAKER_TERM_INDEFINITE) worst = hs[c].term;
+  }
+  cudaFreeHost(hd);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaGraphExecDestroy(gexec);
+  cudaGraphDestroy(graph);
+  cudaFreeAsync(base, s);
+  cudaFreeAsync(st, s);
+  cudaFreeAsync(hist, s);
+  cudaFreeAsync(trel, s);
+  cudaFreeAsync(all_done, s);
+  cudaFreeAsync(parts, s);
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  if (worst == LAKER_TERM_BREAKDOWN) return set_err(ctx, LAKER_ERR_BREAKDOWN_ZERO_CURVATURE, "p.(lambda I + K)p <= 0");
+  if (worst == LAKER_TERM_INDEFINITE) return set_err(ctx, LAKER_ERR_INDEFINITE_PRECONDITIONER, "r.theta <= 0");
+  return LAKER_OK;
+}
+
+}  // namespace laker
