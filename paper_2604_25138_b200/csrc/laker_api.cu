@@ -167,6 +167,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   c->gemv_grid = laker::gemv_max_grid(c->num_sms);
   laker::gemv_init();
   laker::dgemm_init();
+  laker::otf_fast_init();
   const size_t npart = 4096;
   if (cudaMalloc(&c->counters, laker::kNumCtr * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&c->partials, npart * sizeof(laker::dd_pair)) != cudaSuccess ||
@@ -372,7 +373,7 @@ laker_status laker_predict(laker_ctx ctx, int64_t m, const double *Eq, const dou
   cudaEventCreate(&e1);
   cudaEventRecord(e0, ctx->stream);
   if (a1 > a0)
-    laker::launch_kernel_matvec_exact(ev.dptr + a0 * ctx->d, a1 - a0, ctx->E, ctx->n, ctx->d, ctx->scale,
+    laker::launch_kernel_matvec(mode, ev.dptr + a0 * ctx->d, a1 - a0, ctx->E, ctx->n, ctx->d, ctx->scale,
                                       alv.dptr, 0.0, nullptr, ov.dptr + a0, ctx->flags, nullptr, ctx->stream);
   ctx->stats.kernel_launches++;
   LAKER_CUDA(ctx, cudaGetLastError());

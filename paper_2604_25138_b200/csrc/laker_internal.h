@@ -133,6 +133,22 @@ void launch_kernel_matvec_exact(const double *Eq, int64_t m, const double *E, in
                                 double *out, unsigned long long *flags, const int32_t *done,
                                 cudaStream_t s);
 
+// -------------------------------------------------------------- otf_fast.cu
+// FAST (DMMA + CUDA exp) version of launch_kernel_matvec_exact; d <= 128.
+void launch_kernel_matvec_fast(const double *Eq, int64_t m, const double *E, int64_t n, int32_t d, double scale,
+                               const double *w, double lambda, const double *xdiag, double *out,
+                               const int32_t *done, cudaStream_t s);
+void otf_fast_init();
+// mode dispatch for the on-the-fly matvec (EXACT: correctly rounded entries + Dot2)
+inline void launch_kernel_matvec(int mode, const double *Eq, int64_t m, const double *E, int64_t n, int32_t d,
+                                 double scale, const double *w, double lambda, const double *xdiag, double *out,
+                                 unsigned long long *flags, const int32_t *done, cudaStream_t s) {
+  if (mode == LAKER_MODE_FAST && d <= 128)
+    launch_kernel_matvec_fast(Eq, m, E, n, d, scale, w, lambda, xdiag, out, done, s);
+  else
+    launch_kernel_matvec_exact(Eq, m, E, n, d, scale, w, lambda, xdiag, out, flags, done, s);
+}
+
 // ----------------------------------------------------------------- dgemm.cu
 struct GemmArgs {
   int64_t M, N, K;        // K % 16 == 0; N even (or ldc/ldcin padded)

@@ -36,7 +36,7 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
     a.evict_first = true;
     launch_gemv(a, ctx->gemv_grid, ctx->stream);
   } else {
-    launch_kernel_matvec_exact(ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, ctx->E, ctx->n, ctx->d,
+    launch_kernel_matvec(ctx->mode, ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, ctx->E, ctx->n, ctx->d,
                                ctx->scale, p, ctx->lambda, p + ctx->r0, q, ctx->flags,
                                st ? &st->done : nullptr, ctx->stream);
     if (epi == kEpiDelta) {

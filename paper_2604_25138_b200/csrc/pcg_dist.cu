@@ -240,7 +240,7 @@ static void dist_operator(laker_ctx ctx, const double *p_full, double *q_loc, Pc
     a.pair_out = reinterpret_cast<dd_pair *>(pair_out); a.evict_first = true;
     launch_gemv(a, ctx->gemv_grid, ctx->stream);
   } else {
-    launch_kernel_matvec_exact(ctx->E + ctx->r0 * ctx->d, nloc, ctx->E, ctx->n, ctx->d, ctx->scale, p_full,
+    launch_kernel_matvec(ctx->mode, ctx->E + ctx->r0 * ctx->d, nloc, ctx->E, ctx->n, ctx->d, ctx->scale, p_full,
                                ctx->lambda, p_full + ctx->r0, q_loc, ctx->flags, st ? &st->done : nullptr,
                                ctx->stream);
     if (pair_out) {
