@@ -3,14 +3,15 @@
 //
 // Layout: A is the local row block of K (or P), row-major with a padded stride
 // `ld` (multiple of 256 doubles, zero padding).  Work unit = a group of 8 rows
-// x one 1024-column chunk (64 KiB).  One persistent CTA per SM owns a
-// contiguous range of row groups.  A producer warp streams the units into a
-// 3-stage shared-memory ring with 1-D bulk copies (cp.async.bulk, TMA engine,
-// L2 evict-first); 8 consumer warps read the ring, each thread 4 columns x 8
-// rows, with the x chunk held in registers (x is read from L2 once per 8 rows).
-// Each thread keeps one Dot2 pair per row; rows are reduced warp -> CTA in a
-// fixed order, so y_i = RN(lambda x_i + sum_j A_ij x_j) is correctly rounded
-// in practice and bitwise equal to the oracle's sequential Dot2.
+// x one 1024-column chunk (64 KiB) plus the matching 1024-entry chunk of x
+// (8 KiB).  One persistent CTA per SM owns a contiguous range of row groups.
+// A producer warp streams the units into a 3-stage shared-memory ring with
+// 1-D bulk copies (cp.async.bulk, TMA engine; A with an L2 evict-first policy,
+// x evict-last) signalled on mbarriers; 16 consumer warps read the ring, each
+// thread 2 columns x 8 rows, so the x chunk never costs a dependent global
+// load.  Each thread keeps one Dot2 pair per row; rows are reduced warp ->
+// CTA in a fixed order, so y_i = RN(lambda x_i + sum_j A_ij x_j) is correctly
+// rounded in practice and bitwise equal to the oracle's sequential Dot2.
 // The CTA also accumulates dot(x_local, y) as a Dot2 pair; the last CTA to
 // finish reduces the per-CTA pairs in CTA order and runs the PCG scalar
 // epilogue (delta = rho / p.q, or beta = rho'/rho) in the same kernel.
@@ -21,13 +22,14 @@ namespace laker {
 namespace {
 
 constexpr int kRows = 8;
-constexpr int kCPT = 4;
-constexpr int kConsumers = 256;
+constexpr int kCPT = 2;
+constexpr int kConsumers = 512;
+constexpr int kWarps = kConsumers / 32;
 constexpr int kChunk = kConsumers * kCPT;  // 1024 doubles
 constexpr int kStages = 3;
 constexpr int kThreads = kConsumers + 32;
-constexpr size_t kStageDoubles = (size_t)kRows * kChunk;
-constexpr size_t kSmem = kStages * kStageDoubles * sizeof(double) + 8 * kRows * sizeof(dd_pair) +
+constexpr size_t kStageDoubles = (size_t)(kRows + 1) * kChunk;  // 8 rows of A + the x chunk
+constexpr size_t kSmem = kStages * kStageDoubles * sizeof(double) + kWarps * kRows * sizeof(dd_pair) +
                          2 * kStages * sizeof(uint64_t) + 16;
 
 __device__ __forceinline__ void run_epilogue(const GemvArgs &a, double v) {
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   extern __shared__ __align__(128) unsigned char smem[];
   double *ring = reinterpret_cast<double *>(smem);
   dd_pair *red = reinterpret_cast<dd_pair *>(smem + kStages * kStageDoubles * sizeof(double));
-  uint64_t *full = reinterpret_cast<uint64_t *>(red + 8 * kRows);
+  uint64_t *full = reinterpret_cast<uint64_t *>(red + kWarps * kRows);
   uint64_t *empty = full + kStages;
   __shared__ int s_last;
 
@@ -77,16 +79,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers / 32);
+      mbar_init(&empty[s], kWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kConsumers / 32) {
+  if (warp == kWarps) {
     // ---------------- producer warp: one elected lane issues the bulk copies
     if (lane == 0) {
-      const uint64_t pol = a.evict_first ? l2_policy_evict_first() : l2_policy_evict_last();
+      const uint64_t pol_a = a.evict_first ? l2_policy_evict_first() : l2_policy_evict_last();
+      const uint64_t pol_x = l2_policy_evict_last();
       int64_t it = 0;
       for (int64_t g = g0; g < g1; ++g) {
         const int64_t rb = g * kRows;
@@ -97,10 +100,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
           const int64_t col0 = c * kChunk;
           const int width = (int)imin64(kChunk, ncp - col0);
           const uint32_t bytes = (uint32_t)width * 8u;
-          mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nr);
+          mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)(nr + 1));
           double *dst = ring + slot * kStageDoubles;
+          bulk_g2s(dst + kRows * kChunk, a.x + col0, bytes, &full[slot], pol_x);
           for (int r = 0; r < nr; ++r)
-            bulk_g2s(dst + r * kChunk, a.A + (rb + r) * a.ld + col0, bytes, &full[slot], pol);
+            bulk_g2s(dst + r * kChunk, a.A + (rb + r) * a.ld + col0, bytes, &full[slot], pol_a);
         }
       }
     }
@@ -128,25 +132,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       const int64_t col0 = c * kChunk;
       const int width = (int)imin64(kChunk, ncp - col0);
       if (cb < width) {
-        const double2 x0 = __ldg(reinterpret_cast<const double2 *>(a.x + col0 + cb));
-        const double2 x1 = __ldg(reinterpret_cast<const double2 *>(a.x + col0 + cb + 2));
         const double *sp = ring + slot * kStageDoubles + cb;
+        const double2 x0 = *reinterpret_cast<const double2 *>(sp + kRows * kChunk);
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
           if (r < nr) {
             const double2 v0 = *reinterpret_cast<const double2 *>(sp + r * kChunk);
-            const double2 v1 = *reinterpret_cast<const double2 *>(sp + r * kChunk + 2);
             dot2_step(acc[r], v0.x, x0.x);
             dot2_step(acc[r], v0.y, x0.y);
-            dot2_step(acc[r], v1.x, x1.x);
-            dot2_step(acc[r], v1.y, x1.y);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
-    // rows: warp butterfly, then the 8 warp pairs in warp order
+    // rows: warp butterfly, then the warp pairs in warp order
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
       const dd_pair v = warp_reduce_pair(acc[r]);
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
     if (warp == 0 && lane < nr) {
       dd_pair t = red[lane];
 #pragma unroll
-      for (int w = 1; w < kConsumers / 32; ++w) pair_add(t, red[w * kRows + lane]);
+      for (int w = 1; w < kWarps; ++w) pair_add(t, red[w * kRows + lane]);
       const double yv = pair_value(t);
       a.y[rb + lane] = yv;
       dot2_step(part, a.x[a.row0 + rb + lane], yv);
