@@ -108,6 +108,13 @@ struct GemvArgs {
   dd_pair *pair_out;      // kEpiStorePair target (unrounded Dot2 pair, for the rank-order combine)
   int epi;
   bool evict_first;       // stream A with an L2 evict-first policy
+  // fused PCG modes (gemv.cu): 0 none, 1 = K (x = fma(beta, xa, xb)), 2 = P (x = fma(-delta, xa, xb))
+  int fuse;
+  const double *xa, *xb;  // sources of the on-the-fly x (full vectors)
+  double *xown;           // own rows of the formed x are written here
+  double *alpha;          // P mode: alpha = fma(delta, pcur, alpha) on own rows
+  const double *pcur;
+  double *hist;           // P mode: residual history
 };
 void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
 void gemv_init();

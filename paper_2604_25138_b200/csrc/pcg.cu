@@ -12,6 +12,8 @@
 // CUDA graph and the host only polls the state between graph launches.
 
 
+#include <cstdlib>
+
 #include "pcg_kernels.cuh"
 
 namespace laker {
@@ -94,14 +96,15 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
 
   Workspace w;
   const size_t vb = (size_t)ld * sizeof(double);
-  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 6 * vb + 2 * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 8 * vb + 2 * sizeof(double), s));
   w.r = w.alpha + ld;
   w.theta = w.r + ld;
   w.p = w.theta + ld;
   w.q = w.p + ld;
   w.y = w.q + ld;
-  w.scal = w.y + ld;
-  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 6 * vb + 2 * sizeof(double), s));
+  double *p2 = w.y + ld, *r2 = p2 + ld;  // ping-pong partners for the fused iteration
+  w.scal = r2 + ld;
+  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 8 * vb + 2 * sizeof(double), s));
   LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)max_iters * sizeof(double), s));
   LAKER_CUDA(ctx, cudaMallocAsync(&w.st, sizeof(PcgState), s));
   LAKER_CUDA(ctx, cudaMemcpyAsync(w.y, y, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -131,7 +134,38 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     evs.resize(4 * chunk);
     for (auto &e : evs) cudaEventCreate(&e);
   }
+  // Dense P on one rank: the whole iteration is two kernels (gemv.cu fused
+  // modes) -- p = theta + beta p folded into the K pass, r = r - delta q,
+  // alpha += delta p, ||r|| and the termination test folded into the P pass.
+  // Measured on B200 (profiles/r01_*): the fused pair runs 0.367 + 0.371 ms vs 2 x 0.353 ms
+  // unfused (the second staged vector chunk costs more than the removed small kernels),
+  // so the unfused iteration stays the default; LAKER_FUSED=1 selects the fused one.
+  const bool fused = dense && ctx->storage == LAKER_STORE_MATERIALIZED && std::getenv("LAKER_FUSED") != nullptr;
+  auto record_fused = [&](int j) {
+    double *p_old = (j % 2 == 0) ? w.p : p2, *p_new = (j % 2 == 0) ? p2 : w.p;
+    double *r_old = (j % 2 == 0) ? w.r : r2, *r_new = (j % 2 == 0) ? r2 : w.r;
+    GemvArgs a{};
+    a.A = ctx->K; a.ld = ld; a.rows = n; a.ncols = n; a.row0 = 0; a.y = w.q; a.lambda = ctx->lambda;
+    a.state = w.st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.epi = kEpiDelta;
+    a.evict_first = true; a.fuse = 1; a.xa = p_old; a.xb = w.theta; a.xown = p_new;
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
+    launch_gemv(a, ctx->gemv_grid, s);
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
+    GemvArgs b{};
+    b.A = ctx->P; b.ld = ld; b.rows = n; b.ncols = n; b.row0 = 0; b.y = w.theta; b.lambda = 0.0;
+    b.state = w.st; b.partials = ctx->partials; b.counter = ctx->counters + kCtrGemv; b.epi = kEpiNone;
+    b.evict_first = true; b.fuse = 2; b.xa = w.q; b.xb = r_old; b.xown = r_new; b.alpha = w.alpha; b.pcur = p_new;
+    b.hist = w.hist;
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
+    launch_gemv(b, ctx->gemv_grid, s);
+    if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
+    ctx->stats.kernel_launches += 2;
+  };
   auto record_iteration = [&](int j) {
+    if (fused) {
+      record_fused(j);
+      return;
+    }
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
     launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr);
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);

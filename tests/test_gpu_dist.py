@@ -47,3 +47,21 @@ def test_collective_path_equals_single(L, cid, n, kind):
         dv = O.jacobi_diag(P.E, P.scale, P.lam) if kind == "jacobi" else None
         ao, ro = O.pcg(K, P.lam, P.y, pk, dv, tol=P.tol)
         assert ro.iters == r1["iters"] and (ao == a1).all()
+
+
+def test_fused_iteration_equals_unfused(L):
+    """gemv.cu's fused two-kernel iteration (LAKER_FUSED=1) is the same recurrence."""
+    import os
+    P = make_problem(2)
+    c = L.Context(0)
+    c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    Z = np.asfortranarray(make_directions(2, P.n, P.n_dirs))
+    c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    a0, r0, h0 = c.pcg_solve(P.y, P.tol, want_history=True)
+    os.environ["LAKER_FUSED"] = "1"
+    try:
+        a1, r1, h1 = c.pcg_solve(P.y, P.tol, want_history=True)
+    finally:
+        del os.environ["LAKER_FUSED"]
+    c.close()
+    assert r0[0]["iters"] == r1[0]["iters"] and (h0 == h1).all() and (a0 == a1).all()
