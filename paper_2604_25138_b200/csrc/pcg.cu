@@ -113,7 +113,8 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   h0.max_iters = max_iters;
   LAKER_CUDA(ctx, cudaMemcpyAsync(w.st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
 
-  const int vg = (int)std::min<int64_t>(2 * ctx->num_sms, (n + kVecThreads - 1) / kVecThreads);
+  // vector kernels: ~4 elements per thread (n = 16384 -> 16 CTAs) keeps the last-CTA reduction short
+  const int vg = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (n + 4 * kVecThreads - 1) / (4 * kVecThreads)));
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
   cudaEventCreate(&ev1);
@@ -175,10 +176,8 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
       launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
-      pcg_budget_kernel<<<1, 1, 0, s>>>(w.st);
-      ctx->stats.kernel_launches++;
     }
-    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, w.p, w.st);
+    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0);
     ctx->stats.kernel_launches += 2;
   };
 

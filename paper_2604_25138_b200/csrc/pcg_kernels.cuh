@@ -170,14 +170,19 @@ __global__ void pcg_budget_kernel(PcgState *st) {
   }
 }
 
-// p = fma(beta, p, theta)
+// p = fma(beta, p, theta); with budget = 1 (dense P, single rank) the last block
+// also closes the iteration budget (MAX_ITERS after the last allowed update).
 __global__ void __launch_bounds__(kVecThreads) pcg_pupdate_kernel(int64_t n, const double *__restrict__ theta,
-                                                                  double *__restrict__ p,
-                                                                  const PcgState *st) {
+                                                                  double *__restrict__ p, PcgState *st,
+                                                                  int budget = 0) {
   if (*(volatile const int32_t *)&st->done) return;
   const double beta = st->beta;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = __fma_rn(beta, p[i], theta[i]);
+  if (budget && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0 && st->iters >= st->max_iters) {
+    st->term = LAKER_TERM_MAX_ITERS;
+    st->done = 1;
+  }
 }
 
 // true residual ||y - q|| / ||y|| with q = (lambda I + K) alpha
