@@ -48,6 +48,8 @@ template <bool B_KN>
 __global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
   const int bm = blockIdx.y, bn = blockIdx.x;
   if (g.lower_only && bn > bm) return;
+  if (g.tri == 1 && (int64_t)bm * BM + BM - 1 + g.tri_off < (int64_t)bn * BN) return;
+  if (g.tri == 2 && (int64_t)bm * BM + g.tri_off >= (int64_t)bn * BN + BN - 1) return;
   extern __shared__ __align__(16) double sm[];
   double *As = sm;
   double *Bs = sm + ST * A_ELEMS;
@@ -138,14 +140,43 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
         if (r - c == g.diag_offset) v0 = v0 + g.diag;
         if (r - (c + 1) == g.diag_offset) v1 = v1 + g.diag;
       }
-      *reinterpret_cast<double2 *>(g.C + r * g.ldc + c) = make_double2(v0, v1);
+      if (g.tri == 0) {
+        *reinterpret_cast<double2 *>(g.C + r * g.ldc + c) = make_double2(v0, v1);
+      } else {
+        const int64_t gr = r + g.tri_off;
+        const bool k0 = g.tri == 1 ? gr >= c : gr < c;
+        const bool k1 = g.tri == 1 ? gr >= c + 1 : gr < c + 1;
+        if (k0) g.C[r * g.ldc + c] = v0;
+        if (k1 && c + 1 < g.N) g.C[r * g.ldc + c + 1] = v1;
+      }
     }
   }
 }
 
 constexpr size_t smem_bytes(bool kn) { return (size_t)ST * (A_ELEMS + (kn ? B_ELEMS_KN : B_ELEMS_NK)) * 8; }
 
+__global__ void mirror_lower_kernel(double *A, int64_t lda, int64_t n) {
+  __shared__ double t[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;  // tile (bi, bj) with bj > bi: upper tile <- lower tile (bj, bi)
+  if (bj < bi) return;
+  const int64_t r0 = bj * 32, c0 = bi * 32;  // source lower tile rows r0.., cols c0..
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    t[k][threadIdx.x] = (r < n && c < n) ? A[r * lda + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = c0 + k, c = r0 + threadIdx.x;  // A[r][c] = A[c][r] for c > r
+    if (r < n && c < n && c > r) A[r * lda + c] = t[threadIdx.x][k];
+  }
+}
+
 }  // namespace
+
+void launch_mirror_lower(double *A, int64_t lda, int64_t n, cudaStream_t s) {
+  const unsigned nt = (unsigned)((n + 31) / 32);
+  mirror_lower_kernel<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(A, lda, n);
+}
 
 void dgemm_init() {
   cudaFuncSetAttribute(dgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(false));

@@ -101,16 +101,25 @@ __global__ void scale_cols_sqrt_kernel(const double *R, double *S, int64_t ld, i
     S[r * ld + c] = R[r * ld + c] * __dsqrt_rn(b[c]);
 }
 
-// qf[k] = sum_i X[i][k]^2 (Dot2), k < nr
+// qf[k] = sum_i X[i][k]^2 (Dot2), k < nr; block (32 columns x 8 row lanes),
+// lanes combined in a fixed order.
 __global__ void col_sumsq_kernel(const double *X, int64_t ld, int64_t rows, int64_t nr, double *qf) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nr) return;
+  __shared__ dd_pair red[8][32];
+  const int64_t k = (int64_t)blockIdx.x * 32 + threadIdx.x;
   dd_pair acc = {0.0, 0.0};
-  for (int64_t i = 0; i < rows; ++i) {
-    const double v = X[i * ld + k];
-    dot2_step(acc, v, v);
+  if (k < nr) {
+    for (int64_t i = threadIdx.y; i < rows; i += 8) {
+      const double v = X[i * ld + k];
+      dot2_step(acc, v, v);
+    }
   }
-  qf[k] = pair_value(acc);
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && k < nr) {
+    dd_pair t = red[0][threadIdx.x];
+    for (int l = 1; l < 8; ++l) pair_add(t, red[l][threadIdx.x]);
+    qf[k] = pair_value(t);
+  }
 }
 
 struct CccpScalars {
@@ -396,8 +405,9 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   LAKER_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), s));
   LAKER_CUDA(ctx, cudaMemsetAsync(b, 0, nrp * 8, s));
   const bool debug = std::getenv("LAKER_DEBUG_FIT") != nullptr;
+  const bool dump = debug && std::getenv("LAKER_DEBUG_FIT")[0] == '2';
   auto dbg = [&](const char *name, const double *p, int64_t rows, int64_t cols, int64_t ldm) {
-    if (!debug) return;
+    if (!dump) return;
     std::vector<double> h((size_t)rows * ldm);
     cudaMemcpyAsync(h.data(), p, h.size() * 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
@@ -413,6 +423,23 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
                  (long long)rows, (long long)cols, (long long)nan, mx, std::sqrt(fro), h[0],
                  cudaGetErrorString(cudaGetLastError()));
   };
+
+  cudaEvent_t tk_prev = nullptr;
+  auto tick = [&](const char *what) {  // LAKER_DEBUG_FIT: device time of each fit phase
+    if (!debug) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    cudaEventSynchronize(e);
+    if (tk_prev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tk_prev, e);
+      std::fprintf(stderr, "[fit] phase %-12s %9.3f ms\n", what, ms);
+      cudaEventDestroy(tk_prev);
+    }
+    tk_prev = e;
+  };
+  tick("start");
 
   // ---- 1. directions: Zt (N_r x n, row k = z_k), U^T = Zt K^T + lambda Zt
   if (o.Z) {
@@ -458,13 +485,15 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   ++L;
   dbg("Ubar", Ut, nrp, ld, ld);
 
+  tick("directions");
   // ---- 2. shifted CholeskyQR3 of Ubar (rows of Ut): Ut <- Q^T, R = R3 R2 R1
-  auto gram = [&](double *dst) {
+  auto gram = [&](double *dst) {  // SYRK: lower triangle on the tensor cores, mirrored
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = ld;
-    g.A = Ut; g.lda = ld; g.B = Ut; g.ldb = ld; g.C = dst; g.ldc = nrp; g.alpha = 1.0;
+    g.A = Ut; g.lda = ld; g.B = Ut; g.ldb = ld; g.C = dst; g.ldc = nrp; g.alpha = 1.0; g.tri = 1;
     launch_dgemm(g, false, s);
-    ++L;
+    launch_mirror_lower(dst, nrp, nrp, s);
+    L += 2;
   };
   gram(Cg);  // C = Ubar^T Ubar (kept for the Frobenius change)
   copy_diag_kernel<<<cdiv(nr, 256), 256, 0, s>>>(Cg, nrp, nr, cd);
@@ -508,6 +537,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   LAKER_CUDA(ctx, cudaStreamSynchronize(s));
   if (hflag) return set_err(ctx, LAKER_ERR_NOT_POSITIVE_DEFINITE, "fit: CholeskyQR of the directions failed");
 
+  tick("cholqr3");
   // ---- 3. CCCP iteration on (a, b)
   CccpScalars hs{};
   hs.a = 1.0;
@@ -528,12 +558,12 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     scale_cols_sqrt_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(R, S, nrp, nrp, b);
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.A = S; g.lda = nrp; g.B = S; g.ldb = nrp; g.C = T; g.ldc = nrp;
-    g.alpha = 1.0; g.diag = a;
+    g.alpha = 1.0; g.diag = a; g.tri = 1;  // the Cholesky reads the lower triangle only
     launch_dgemm(g, false, s);
     cholesky_lower(T, nrp, nrp, flag, s, &L);
     LAKER_CUDA(ctx, cudaMemcpyAsync(X, R, sq * 8, cudaMemcpyDeviceToDevice, s));
     trsm_lower_left(T, nrp, nrp, X, nrp, nrp, s, &L);
-    col_sumsq_kernel<<<cdiv(nr, 128), 128, 0, s>>>(X, nrp, nrp, nr, qf);
+    col_sumsq_kernel<<<dim3(cdiv(nr, 32)), dim3(32, 8), 0, s>>>(X, nrp, nrp, nr, qf);
     cccp_update_kernel<<<1, 1024, 0, s>>>(qf, cd, b, bo, db, nr, sc);
     const int qg = (int)std::min<int64_t>(2 * ctx->num_sms, (nr + 7) / 8);
     cccp_quadform_kernel<<<qg, 256, 0, s>>>(Cg, nrp, nr, db, bo, ctx->partials, ctx->counters + kCtrMisc, sc);
@@ -552,16 +582,18 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     }
   }
 
+  tick("cccp");
   // ---- 4. T^{-1/2} of the final T = a I + R diag(b) R^T (coupled Newton-Schulz)
   {
     scale_cols_sqrt_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(R, S, nrp, nrp, b);
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.A = S; g.lda = nrp; g.B = S; g.ldb = nrp; g.C = T; g.ldc = nrp;
-    g.alpha = 1.0; g.diag = a;
+    g.alpha = 1.0; g.diag = a; g.tri = 1;
     launch_dgemm(g, false, s);
-    symmetrize_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(T, nrp, nrp);
+    launch_mirror_lower(T, nrp, nrp, s);
     L += 3;
   }
+  tick("T_build");
   // lambda_max(T) by power iteration (x0 = ones), c = 1.1 * estimate
   double cscale = 1.0;
   {
@@ -583,42 +615,71 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     if (debug) std::fprintf(stderr, "[fit] lambda_max(T) ~ %.6e a = %.6e\n", hn, a);
     dbg("T", T, nrp, nrp, nrp);
   }
-  double *Y = S, *Zm = X, *W = G, *Tmp = L1;
+  tick("power_iter");
+  double *Y = S, *Zm = X, *W = G, *Tmp = L1, *Zsave = L2;
   LAKER_CUDA(ctx, cudaMemcpyAsync(Y, T, sq * 8, cudaMemcpyDeviceToDevice, s));
   scale_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(Y, nrp, nrp, nrp, 1.0 / cscale);
   set_identity_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(Zm, nrp, nrp);
   L += 2;
-  // W_k = (3I - Z_k Y_k)/2, Y_{k+1} = Y_k W_k, Z_{k+1} = W_k Z_k (exact NN products);
-  // the residual ||W_k - I|| = ||I - Z_k Y_k||/2 is checked before each update and
-  // the iteration stops at the tolerance or as soon as it stops contracting
-  // (rounding floor), keeping the last contracting iterate.
+  // Coupled Newton-Schulz with a per-step scalar scaling (Chen & Chow-style):
+  // with s_k^2 = sigma_k, W_k = (3I - sigma_k Z_k Y_k)/2, Y_{k+1} = s_k Y_k W_k,
+  // Z_{k+1} = s_k W_k Z_k keeps Y_k = (T/c) Z_k, so Z_k -> (T/c)^{-1/2} as
+  // Z_k Y_k -> I.  The eigenvalues of Z_k Y_k lie in [l_k, u_k] (l_0 = a/c is
+  // a lower bound of lambda_min(T)/c, u_0 = 1); sigma_k equalizes
+  // f(sigma l) = f(sigma u) for f(x) = x (3 - x)^2 / 4, giving
+  // l_{k+1} = f(sigma_k l_k), u_{k+1} = 1: ~3x faster growth of the small
+  // eigenvalues than the unscaled map.  Every product is symmetric in exact
+  // arithmetic (all are polynomials in T): the lower triangle is formed on the
+  // tensor cores and mirrored.  ||W_k - I|| is checked before each update; the
+  // iteration stops at the tolerance or when it stops contracting.
+  auto fmap = [](double x) { return x * (3.0 - x) * (3.0 - x) / 4.0; };
+  double lo = std::max(a / cscale, 1e-300), up = 1.0;
   double prev = INFINITY;
   for (int k = 0; k < 100; ++k) {
+    double sigma = 1.0;
+    if (up - lo > 1e-3 * up) {  // bisection for f(sigma lo) = f(sigma up), sigma up in [1, 3)
+      double s0 = 1.0 / up, s1 = 2.5 / up;  // sigma * u <= 2.5: safe if u underestimates by 10%
+      for (int b = 0; b < 200; ++b) {
+        const double sm = 0.5 * (s0 + s1);
+        if (fmap(sm * lo) < fmap(sm * up)) s0 = sm; else s1 = sm;
+      }
+      sigma = s0;
+    }
+    const double sk = std::sqrt(sigma);
     GemmArgs g{};
-    g.M = nrp; g.N = nrp; g.K = nrp; g.lda = g.ldb = g.ldc = nrp;
-    g.A = Zm; g.B = Y; g.C = W; g.alpha = -0.5; g.diag = 1.5;
+    g.M = nrp; g.N = nrp; g.K = nrp; g.lda = g.ldb = g.ldc = nrp; g.tri = 1;
+    g.A = Zm; g.B = Y; g.C = W; g.alpha = -0.5 * sigma; g.diag = 1.5;
     launch_dgemm(g, true, s);
+    launch_mirror_lower(W, nrp, nrp, s);
     LAKER_CUDA(ctx, cudaMemsetAsync(scal + 1, 0, sizeof(double), s));
     frob_minus_identity_kernel<<<4 * ctx->num_sms, 256, 0, s>>>(W, nrp, nrp, scal + 1);
-    L += 2;
+    L += 3;
     double fn = 0.0;
     LAKER_CUDA(ctx, cudaMemcpyAsync(&fn, scal + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
     LAKER_CUDA(ctx, cudaStreamSynchronize(s));
     fn = std::sqrt(fn);
-    if (debug) std::fprintf(stderr, "[fit] NS %d ||W-I||_F = %.3e\n", k, fn);
-    if (fn < 1e-14 * std::sqrt((double)nrp) || (prev < 1e-6 && fn > 0.5 * prev)) break;
-    prev = fn;
-    g.diag = 0.0; g.alpha = 1.0;
+    if (debug) std::fprintf(stderr, "[fit] NS %d sigma %.4f [%.3e, %.3e] ||W-I||_F = %.3e\n", k, sigma, lo, up, fn);
+    if (sigma == 1.0 && (fn < 1e-14 * std::sqrt((double)nrp) || (prev < 1e-6 && fn > 0.5 * prev))) {
+      if (fn > prev) std::swap(Zm, Zsave);  // rounding floor reached: keep the better previous iterate
+      break;
+    }
+    prev = sigma == 1.0 ? fn : INFINITY;
+    if (sigma == 1.0) LAKER_CUDA(ctx, cudaMemcpyAsync(Zsave, Zm, sq * 8, cudaMemcpyDeviceToDevice, s));
+    g.diag = 0.0; g.alpha = sk;
     g.A = Y; g.B = W; g.C = Tmp;
     launch_dgemm(g, true, s);
+    launch_mirror_lower(Tmp, nrp, nrp, s);
     std::swap(Y, Tmp);
     g.A = W; g.B = Zm; g.C = Tmp;
     launch_dgemm(g, true, s);
+    launch_mirror_lower(Tmp, nrp, nrp, s);
     std::swap(Zm, Tmp);
-    symmetrize_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(Y, nrp, nrp);
-    symmetrize_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(Zm, nrp, nrp);
     L += 4;
+    const double nl = fmap(sigma * lo), nu = (sigma * up >= 1.0 && sigma * lo <= 1.0) ? 1.0 : fmap(sigma * up);
+    lo = std::min(nl, nu);
+    up = std::max(nl, nu);
   }
+  tick("newton_schulz");
   // M = T^{-1/2} - a^{-1/2} I = Z / sqrt(c) - a^{-1/2} I   (into Zm)
   scale_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(Zm, nrp, nrp, nrp, 1.0 / std::sqrt(cscale));
   add_diag_kernel<<<cdiv(nrp, 256), 256, 0, s>>>(Zm, nrp, 0, nrp, -1.0 / std::sqrt(a));
@@ -643,15 +704,17 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       LAKER_CUDA(ctx, cudaMalloc(&ctx->P, (size_t)(ctx->r1 - ctx->r0) * ld * 8));
     }
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->P, 0, (size_t)(ctx->r1 - ctx->r0) * ld * 8, s));
-    // P_loc = (W_loc Q^T + Q_loc W^T) / 2 + a^{-1/2} I: entry (i, j) and entry (j, i) are
-    // formed from the same two dot products, so P is symmetric (the DMMA product is
-    // commutative in its operands) and each row is independent of the sharding.
+    // P_ij = W_i . Q_j for i >= j and P_ij = Q_i . W_j for i < j (+ a^{-1/2} on the
+    // diagonal): the upper entry (i, j) is the same DMMA dot product as the lower
+    // entry (j, i) (the product is commutative in its operands), so P is bitwise
+    // symmetric, every row is independent of the row sharding (each rank holds
+    // W and Q in full), and the work is one n_loc x n x N_r GEMM split in two.
     GemmArgs p{};
     p.M = ctx->r1 - ctx->r0; p.N = n; p.K = nrp;
     p.A = Wr + ctx->r0 * nrp; p.lda = nrp; p.B = Qr; p.ldb = nrp; p.C = ctx->P; p.ldc = ld;
-    p.alpha = 0.5; p.diag = 1.0 / std::sqrt(a); p.diag_offset = -ctx->r0;
+    p.alpha = 1.0; p.diag = 1.0 / std::sqrt(a); p.diag_offset = -ctx->r0; p.tri = 1; p.tri_off = ctx->r0;
     launch_dgemm(p, false, s);
-    p.A = Qr + ctx->r0 * nrp; p.B = Wr; p.beta = 1.0; p.Cin = ctx->P; p.ldcin = ld; p.diag = 0.0;
+    p.A = Qr + ctx->r0 * nrp; p.B = Wr; p.diag = 0.0; p.tri = 2;
     launch_dgemm(p, false, s);
     L += 2;
     if (n % 2 == 1) {  // the last double2 store of each row spilled one past n: restore zero padding
@@ -660,6 +723,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     dbg("Wt", Wt, nrp, ld, ld);
     dbg("P0", ctx->P, ctx->r1 - ctx->r0, n, ld);
   }
+  tick("P_form");
   // trace of Sigma* = n a + sum_k b_k C_kk
   double htr = 0.0;
   {

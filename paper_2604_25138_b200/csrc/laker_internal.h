@@ -171,7 +171,11 @@ struct GemmArgs {
   double diag;
   int64_t diag_offset;
   bool lower_only;        // skip CTA tiles strictly above the block diagonal
+  int tri;                // 0 all; 1 only entries with row + tri_off >= col; 2 only row + tri_off < col
+  int64_t tri_off;        // (tiles with no kept entry are skipped; masked entries are not written)
 };
+// copy the strict lower triangle of the n x n matrix A onto its upper triangle
+void launch_mirror_lower(double *A, int64_t lda, int64_t n, cudaStream_t s);
 void dgemm_init();
 void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s);
 
