@@ -18,13 +18,24 @@
 namespace laker {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, ST = 3;
-constexpr int AS = BK + 4;       // As[m][k] row stride (doubles)
+constexpr int BK = 16, ST = 3;
+constexpr int AS = BK + 4;       // As[m][k] row stride (doubles): 8 words mod 32
 constexpr int BS_NK = BK + 4;    // Bs[n][k]
-constexpr int BS_KN = BN + 4;    // Bs[k][n]
-constexpr int A_ELEMS = BM * AS;
-constexpr int B_ELEMS_NK = BN * BS_NK;
-constexpr int B_ELEMS_KN = BK * BS_KN;
+
+// CTA tile BM x BN, WM x WN warps, warp tile (BM/WM) x (BN/WN) of 8 x 8 DMMA fragments.
+template <int BM_, int BN_, int WM_, int WN_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int THREADS = 32 * WM * WN;
+  static constexpr int MI = BM / WM / 8, NJ = BN / WN / 8;
+  static constexpr int BS_KN = BN + 4;  // Bs[k][n] stride: BN + 4 = 4 mod 16 doubles
+  static constexpr int A_ELEMS = BM * AS;
+  static constexpr int B_ELEMS_NK = BN * BS_NK;
+  static constexpr int B_ELEMS_KN = BK * BS_KN;
+  static constexpr size_t smem(bool kn) { return (size_t)ST * (A_ELEMS + (kn ? B_ELEMS_KN : B_ELEMS_NK)) * 8; }
+};
+using TileL = Tile<128, 128, 2, 4>;  // 256 threads, 64 x 32 per warp
+using TileS = Tile<64, 64, 2, 2>;    // 128 threads, 32 x 32 per warp (skinny / small problems)
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -44,40 +55,41 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <bool B_KN>
-__global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
+template <class TL, bool B_KN>
+__global__ void __launch_bounds__(TL::THREADS) dgemm_kernel(const GemmArgs g) {
+  constexpr int BM = TL::BM, BN = TL::BN, MI = TL::MI, NJ = TL::NJ, NT = TL::THREADS;
   const int bm = blockIdx.y, bn = blockIdx.x;
-  if (g.lower_only && bn > bm) return;
+  if (g.lower_only && (int64_t)bn * BN > (int64_t)bm * BM + BM - 1) return;
   if (g.tri == 1 && (int64_t)bm * BM + BM - 1 + g.tri_off < (int64_t)bn * BN) return;
   if (g.tri == 2 && (int64_t)bm * BM + g.tri_off >= (int64_t)bn * BN + BN - 1) return;
   extern __shared__ __align__(16) double sm[];
   double *As = sm;
-  double *Bs = sm + ST * A_ELEMS;
-  constexpr int BSZ = B_KN ? B_ELEMS_KN : B_ELEMS_NK;
+  double *Bs = sm + ST * TL::A_ELEMS;
+  constexpr int BSZ = B_KN ? TL::B_ELEMS_KN : TL::B_ELEMS_NK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+  const int wm = (warp / TL::WN) * (BM / TL::WM), wn = (warp % TL::WN) * (BN / TL::WN);
   const int fr = lane >> 2, fk = lane & 3;
   const int64_t row0 = (int64_t)bm * BM, col0 = (int64_t)bn * BN;
 
   auto load_stage = [&](int st, int k0) {
-    double *as = As + st * A_ELEMS;
+    double *as = As + st * TL::A_ELEMS;
     double *bs = Bs + st * BSZ;
 #pragma unroll
-    for (int c = tid; c < BM * BK / 2; c += 256) {
+    for (int c = tid; c < BM * BK / 2; c += NT) {
       const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
       const bool ok = row0 + r < g.M;
       cp_async16(as + r * AS + cc, g.A + (ok ? (row0 + r) : 0) * g.lda + k0 + cc, ok);
     }
     if (B_KN) {
 #pragma unroll
-      for (int c = tid; c < BK * BN / 2; c += 256) {
+      for (int c = tid; c < BK * BN / 2; c += NT) {
         const int r = c / (BN / 2), cc = (c % (BN / 2)) * 2;
         const bool ok = col0 + cc < g.N;
-        cp_async16(bs + r * BS_KN + cc, g.B + (int64_t)(k0 + r) * g.ldb + (ok ? col0 + cc : 0), ok);
+        cp_async16(bs + r * TL::BS_KN + cc, g.B + (int64_t)(k0 + r) * g.ldb + (ok ? col0 + cc : 0), ok);
       }
     } else {
 #pragma unroll
-      for (int c = tid; c < BN * BK / 2; c += 256) {
+      for (int c = tid; c < BN * BK / 2; c += NT) {
         const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
         const bool ok = col0 + r < g.N;
         cp_async16(bs + r * BS_NK + cc, g.B + (ok ? (col0 + r) : 0) * g.ldb + k0 + cc, ok);
@@ -85,11 +97,11 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
     }
   };
 
-  double acc[8][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int KT = g.K / BK;
 #pragma unroll
@@ -103,31 +115,31 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
     const int nk = kt + ST - 1;
     if (nk < KT) load_stage(nk % ST, nk * BK);
     cp_commit();
-    const double *as = As + (kt % ST) * A_ELEMS;
+    const double *as = As + (kt % ST) * TL::A_ELEMS;
     const double *bs = Bs + (kt % ST) * BSZ;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double a[8], b[4];
+      double a[MI], b[NJ];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = as[(wm + 8 * i + fr) * AS + kk + fk];
+      for (int i = 0; i < MI; ++i) a[i] = as[(wm + 8 * i + fr) * AS + kk + fk];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        b[j] = B_KN ? bs[(kk + fk) * BS_KN + wn + 8 * j + fr] : bs[(wn + 8 * j + fr) * BS_NK + kk + fk];
+      for (int j = 0; j < NJ; ++j)
+        b[j] = B_KN ? bs[(kk + fk) * TL::BS_KN + wn + 8 * j + fr] : bs[(wn + 8 * j + fr) * BS_NK + kk + fk];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[i], b[j]);
     }
   }
   cp_wait<0>();
 
   // epilogue
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < MI; ++i) {
     const int64_t r = row0 + wm + 8 * i + fr;
     if (r >= g.M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int64_t c = col0 + wn + 8 * j + 2 * fk;
       if (c >= g.N) continue;
       double v0 = g.alpha * acc[i][j][0], v1 = g.alpha * acc[i][j][1];
@@ -153,8 +165,6 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(const GemmArgs g) {
   }
 }
 
-constexpr size_t smem_bytes(bool kn) { return (size_t)ST * (A_ELEMS + (kn ? B_ELEMS_KN : B_ELEMS_NK)) * 8; }
-
 __global__ void mirror_lower_kernel(double *A, int64_t lda, int64_t n) {
   __shared__ double t[32][33];
   const int64_t bi = blockIdx.y, bj = blockIdx.x;  // tile (bi, bj) with bj > bi: upper tile <- lower tile (bj, bi)
@@ -179,17 +189,30 @@ void launch_mirror_lower(double *A, int64_t lda, int64_t n, cudaStream_t s) {
 }
 
 void dgemm_init() {
-  cudaFuncSetAttribute(dgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(false));
-  cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(true));
+  cudaFuncSetAttribute(dgemm_kernel<TileL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileL::smem(false));
+  cudaFuncSetAttribute(dgemm_kernel<TileL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileL::smem(true));
+  cudaFuncSetAttribute(dgemm_kernel<TileS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileS::smem(false));
+  cudaFuncSetAttribute(dgemm_kernel<TileS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileS::smem(true));
 }
 
 void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return;
-  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
-  if (b_kn)
-    dgemm_kernel<true><<<grid, 256, smem_bytes(true), s>>>(g);
-  else
-    dgemm_kernel<false><<<grid, 256, smem_bytes(false), s>>>(g);
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t tiles_l = ((g.N + 127) / 128) * ((g.M + 127) / 128);
+  if (tiles_l >= 2 * sms || g.lower_only) {
+    dim3 grid((unsigned)((g.N + 127) / 128), (unsigned)((g.M + 127) / 128));
+    if (b_kn)
+      dgemm_kernel<TileL, true><<<grid, TileL::THREADS, TileL::smem(true), s>>>(g);
+    else
+      dgemm_kernel<TileL, false><<<grid, TileL::THREADS, TileL::smem(false), s>>>(g);
+  } else {  // skinny or small: 64 x 64 tiles, 4 warps (more CTAs in flight)
+    dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
+    if (b_kn)
+      dgemm_kernel<TileS, true><<<grid, TileS::THREADS, TileS::smem(true), s>>>(g);
+    else
+      dgemm_kernel<TileS, false><<<grid, TileS::THREADS, TileS::smem(false), s>>>(g);
+  }
 }
 
 }  // namespace laker
