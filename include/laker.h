@@ -71,10 +71,13 @@ enum { LAKER_TERM_RESIDUAL_TOL = 0, LAKER_TERM_MAX_ITERS = 1, LAKER_TERM_ZERO_RH
 laker_status laker_get_unique_id(unsigned char id[128]);
 
 /* Create a context on CUDA device `device`.  world >= 1, 0 <= rank < world.
-   nccl_id: the 128-byte id from rank 0; required when world > 1.  With
-   world == 1 it may be NULL (single-GPU path) or an id from
+   nccl_id: the 128-byte id from rank 0 (ncclCommInitRank over `world` ranks).
+   With world == 1 it may be NULL (single-GPU path) or an id from
    laker_get_unique_id, which creates a 1-rank communicator and runs the
-   row-sharded collective code path (used to test it on one GPU).
+   row-sharded collective code path (used to test it on one GPU).  With
+   world > 1 and NULL the context is a detached shard: row-sharded assembly,
+   predict and the row hooks work, calls that need collectives (LEARNED fit,
+   solve, apply) return NOT_READY (used to test the sharded layouts).
    cuda_stream: a cudaStream_t to order all work on, or NULL for a
    context-owned non-blocking stream.  *out is NULL on failure. */
 laker_status laker_create(laker_ctx *out, int device, int rank, int world,

@@ -141,7 +141,9 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
                           void *cuda_stream) {
   if (!out) return LAKER_ERR_INVALID_ARGUMENT;
   *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_id)) return LAKER_ERR_INVALID_ARGUMENT;
+  // world > 1 without an id: a detached shard (row-sharded assembly / predict / hooks
+  // only, no collectives) -- used to test the sharded layouts on one GPU.
+  if (world < 1 || rank < 0 || rank >= world) return LAKER_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -297,6 +299,8 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
     case LAKER_PRECOND_LEARNED:
       if (ctx->storage != LAKER_STORE_MATERIALIZED)
         return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: LEARNED needs MATERIALIZED storage");
+      if (ctx->world > 1 && !ctx->comm)
+        return set_err(ctx, LAKER_ERR_NOT_READY, "fit: detached shard (no NCCL communicator)");
       {
         laker_status st = laker::fit_learned(ctx, *opts, report);
         if (st != LAKER_OK) return st;
@@ -312,6 +316,7 @@ laker_status laker_pcg_solve(laker_ctx ctx, int32_t nrhs, const double *Y, doubl
                              const laker_solve_opts *opts, laker_solve_report *reports, double *history) {
   CHECK_CTX(ctx);
   if (!ctx->assembled) return set_err(ctx, LAKER_ERR_NOT_READY, "solve: assemble the kernel first");
+  if (ctx->world > 1 && !ctx->comm) return set_err(ctx, LAKER_ERR_NOT_READY, "solve: detached shard (no NCCL communicator)");
   if (nrhs < 1 || !Y || !alpha || !opts || !(opts->tol > 0.0 && opts->tol < 1.0) || opts->max_iters < 0)
     return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "solve: need nrhs >= 1, Y, alpha, 0 < tol < 1");
   cudaSetDevice(ctx->device);
@@ -473,6 +478,7 @@ laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows) {
 laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y) {
   CHECK_CTX(ctx);
   if (!ctx->assembled) return set_err(ctx, LAKER_ERR_NOT_READY, "apply: assemble first");
+  if (ctx->world > 1 && !ctx->comm) return set_err(ctx, LAKER_ERR_NOT_READY, "apply: detached shard (no NCCL communicator)");
   if (!x || !y) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "apply: NULL");
   cudaSetDevice(ctx->device);
   DevView xv, yv;

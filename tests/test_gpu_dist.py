@@ -65,3 +65,39 @@ def test_fused_iteration_equals_unfused(L):
         del os.environ["LAKER_FUSED"]
     c.close()
     assert r0[0]["iters"] == r1[0]["iters"] and (h0 == h1).all() and (a0 == a1).all()
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_row_sharded_assembly_and_predict_layouts(L, W):
+    """Detached shards (world = W, no communicator) on one GPU: each rank's K rows
+    are the rows [r n/W, (r+1) n/W) of the full kernel, bitwise (EXACT and FAST);
+    each rank's predict rows match the full map; the dense P loaded per rank
+    round-trips.  (The collectives themselves need W GPUs.)"""
+    P = make_problem(3, n=2048)
+    full = L.Context(0)
+    for mode in (L.MODE_EXACT, L.MODE_FAST):
+        full.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, mode)
+        Kf = full.get_kernel_rows()
+        alpha = np.random.default_rng(1).standard_normal(P.n)
+        Eq = np.ascontiguousarray(P.Eq[:1000])
+        mf = full.predict(Eq, alpha, mode=mode)
+        for r in range(W):
+            c = L.Context(0, r, W, None)
+            c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, mode)
+            Kr = c.get_kernel_rows()
+            rows = slice(r * P.n // W, (r + 1) * P.n // W)
+            if mode == L.MODE_EXACT:
+                assert (Kr == Kf[rows]).all()
+            else:
+                assert np.abs(Kr / Kf[rows] - 1).max() <= 1e-13
+            out = np.full(Eq.shape[0], np.nan)
+            c.predict(Eq, alpha, mode=mode, out=out)
+            per = -(-Eq.shape[0] // W)
+            sl = slice(r * per, min(Eq.shape[0], (r + 1) * per))
+            assert (out[sl] == mf[sl]).all() and np.isnan(np.delete(out, np.r_[sl])).all()
+            c.set_preconditioner(L.PRECOND_EXTERNAL_DENSE, np.ascontiguousarray(Kf[rows]))
+            assert (c.get_preconditioner_rows() == Kf[rows]).all()
+            with pytest.raises(L.LakerError):
+                c.pcg_solve(P.y, 1e-8)
+            c.close()
+    full.close()
