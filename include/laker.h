@@ -197,6 +197,8 @@ typedef struct {
   int64_t op_launches, prec_launches;
   double assemble_ms, fit_ms, solve_ms, predict_ms; /* last call of each (events) */
   int64_t kernel_launches;       /* kernels this context launched since creation */
+  int32_t symmetric_k, symmetric_p; /* 1: K / dense P found bitwise symmetric on one rank, so the
+                                       PCG applies stream only their block upper triangle (symv) */
 } laker_stats;
 laker_status laker_get_stats(laker_ctx ctx, laker_stats *out);
 

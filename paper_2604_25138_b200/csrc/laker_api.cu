@@ -2,6 +2,7 @@
 // staging, context lifecycle, and dispatch to the kernels.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -19,6 +20,28 @@ laker_status set_err(laker_ctx ctx, laker_status s, const std::string &msg) {
 laker_status cuda_err(laker_ctx ctx, cudaError_t e, const char *what) {
   std::string m = std::string(what) + ": " + cudaGetErrorString(e);
   return set_err(ctx, e == cudaErrorMemoryAllocation ? LAKER_ERR_OUT_OF_MEMORY : LAKER_ERR_CUDA, m);
+}
+
+// The symmetric GEMV (symv.cu) is selected for K (which = 0) or P (which = 1)
+// only on a single rank, for a materialized matrix that a device check finds
+// bitwise symmetric.  LAKER_SYMV=0 disables it (A/B measurements).
+laker_status refresh_symmetry(laker_ctx ctx, int which) {
+  bool &flag = which == 0 ? ctx->k_sym : ctx->p_sym;
+  flag = false;
+  const double *A = which == 0 ? ctx->K : ctx->P;
+  if (!A || ctx->world != 1 || ctx->storage != LAKER_STORE_MATERIALIZED) return LAKER_OK;
+  const char *env = std::getenv("LAKER_SYMV");
+  if (env && env[0] == '0') return LAKER_OK;
+  LAKER_CUDA(ctx, symv_plan(ctx->symv, ctx->n, ctx->ld, ctx->num_sms));
+  int *dflag = reinterpret_cast<int *>(ctx->flags + 2);
+  LAKER_CUDA(ctx, cudaMemsetAsync(dflag, 0, sizeof(int), ctx->stream));
+  launch_symv_check(A, ctx->n, ctx->ld, dflag, ctx->stream);
+  ctx->stats.kernel_launches++;
+  int h = 1;
+  LAKER_CUDA(ctx, cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (h == 0) flag = symv_bind(ctx->symv, which, A);
+  return LAKER_OK;
 }
 
 }  // namespace laker
@@ -168,6 +191,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   c->gemv_grid = laker::gemv_max_grid(c->num_sms);
   laker::gemv_init();
+  laker::symv_init();
   laker::dgemm_init();
   laker::otf_fast_init();
   const size_t npart = 4096;
@@ -208,6 +232,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   cudaFree(ctx->counters);
   cudaFree(ctx->partials);
   cudaFree(ctx->flags);
+  laker::symv_free(ctx->symv);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -227,6 +252,7 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   free_dev(ctx, ctx->P);
   free_dev(ctx, ctx->Pdiag);
   ctx->assembled = false;
+  ctx->k_sym = ctx->p_sym = false;
   ctx->precond_kind = LAKER_PRECOND_NONE;
   ctx->n = n;
   ctx->d = d;
@@ -277,6 +303,7 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   ctx->stats.exp_overflow += hf[1];
   ctx->assembled = true;
   if (hf[1] > 0) return set_err(ctx, LAKER_ERR_OVERFLOW, "scale*<e_i,e_j> exceeded ln(DBL_MAX)");
+  LAKER_TRY(laker::refresh_symmetry(ctx, 0));
   return LAKER_OK;
 }
 
@@ -289,6 +316,7 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
   switch (opts->kind) {
     case LAKER_PRECOND_NONE:
       free_dev(ctx, ctx->P);
+      ctx->p_sym = false;
       ctx->precond_kind = LAKER_PRECOND_NONE;
       return LAKER_OK;
     case LAKER_PRECOND_JACOBI:
@@ -302,10 +330,11 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
       if (ctx->world > 1 && !ctx->comm)
         return set_err(ctx, LAKER_ERR_NOT_READY, "fit: detached shard (no NCCL communicator)");
       {
+        ctx->p_sym = false;
         laker_status st = laker::fit_learned(ctx, *opts, report);
         if (st != LAKER_OK) return st;
         LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        return LAKER_OK;
+        return laker::refresh_symmetry(ctx, 1);
       }
     default:
       return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: unknown kind");
@@ -410,7 +439,7 @@ laker_status laker_load_kernel_rows(laker_ctx ctx, const double *K_rows) {
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   free_dev(ctx, ctx->Pdiag);  // Jacobi diagonal derived from E no longer matches
   if (ctx->precond_kind == LAKER_PRECOND_JACOBI) ctx->precond_kind = LAKER_PRECOND_NONE;
-  return LAKER_OK;
+  return laker::refresh_symmetry(ctx, 0);
 }
 
 laker_status laker_get_kernel_rows(laker_ctx ctx, double *K_rows) {
@@ -458,7 +487,7 @@ laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *dat
                                       ctx->n * sizeof(double), rows, cudaMemcpyDefault, ctx->stream));
     LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->precond_kind = kind;
-    return LAKER_OK;
+    return laker::refresh_symmetry(ctx, 1);
   }
   return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "set_preconditioner: kind must be NONE, JACOBI or EXTERNAL_DENSE");
 }
@@ -504,6 +533,8 @@ laker_status laker_get_stats(laker_ctx ctx, laker_stats *out) {
   ctx->stats.precond_kind = ctx->precond_kind;
   ctx->stats.storage = ctx->storage;
   ctx->stats.mode = ctx->mode;
+  ctx->stats.symmetric_k = ctx->k_sym ? 1 : 0;
+  ctx->stats.symmetric_p = ctx->p_sym ? 1 : 0;
   *out = ctx->stats;
   return LAKER_OK;
 }

@@ -42,6 +42,8 @@ struct Buf {
   size_t bytes = 0;
 };
 
+struct SymvPlan;  // symv.cu
+
 }  // namespace laker
 
 struct laker_ctx_s {
@@ -70,6 +72,11 @@ struct laker_ctx_s {
   laker::dd_pair *partials = nullptr;      // per-CTA pairs (>= 2 x grid)
   unsigned long long *flags = nullptr;     // [0] exp inconclusive, [1] exp overflow
   int gemv_grid = 0, num_sms = 0;
+
+  // symmetric (upper-triangle) GEMV, single rank: used for K / P only after a
+  // device check found them bitwise symmetric (symv.cu)
+  laker::SymvPlan *symv = nullptr;
+  bool k_sym = false, p_sym = false;
 
   laker_stats stats{};
 };
@@ -120,6 +127,19 @@ void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
 void gemv_init();
 int gemv_max_grid(int num_sms);
 size_t gemv_smem_bytes();
+
+// ----------------------------------------------------------------- symv.cu
+// Symmetric Dot2 GEMV over the block upper triangle (half the bytes of gemv.cu),
+// same outputs and epilogues, bitwise equal rows.  which = 0 (K) / 1 (P).
+cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms);
+void symv_free(SymvPlan *&p);
+bool symv_bind(SymvPlan *p, int which, const double *A);
+void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s);
+void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s);
+void symv_init();
+size_t symv_smem_bytes();
+// set ctx->k_sym / p_sym: bitwise-symmetry check of the (whole, single-rank) matrix
+laker_status refresh_symmetry(laker_ctx ctx, int which);
 
 // -------------------------------------------------------------- assemble.cu
 void launch_assemble_exact_sym(const double *E, int64_t n, int32_t d, double scale, double *K,

@@ -36,7 +36,12 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
     a.dot_out = dot_out;
     a.epi = epi;
     a.evict_first = true;
-    launch_gemv(a, ctx->gemv_grid, ctx->stream);
+    if (ctx->k_sym) {
+      launch_symv(ctx->symv, 0, a, ctx->stream);
+      ctx->stats.kernel_launches++;
+    } else {
+      launch_gemv(a, ctx->gemv_grid, ctx->stream);
+    }
   } else {
     launch_kernel_matvec(ctx->mode, ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, ctx->E, ctx->n, ctx->d,
                                ctx->scale, p, ctx->lambda, p + ctx->r0, q, ctx->flags,
@@ -67,7 +72,12 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
   a.dot_out = dot_out;
   a.epi = epi;
   a.evict_first = true;
-  launch_gemv(a, ctx->gemv_grid, ctx->stream);
+  if (ctx->p_sym) {
+    launch_symv(ctx->symv, 1, a, ctx->stream);
+    ctx->stats.kernel_launches++;
+  } else {
+    launch_gemv(a, ctx->gemv_grid, ctx->stream);
+  }
   ctx->stats.kernel_launches++;
 }
 

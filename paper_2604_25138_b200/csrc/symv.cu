@@ -1,0 +1,541 @@
+// Symmetric streaming Dot2 GEMV: the per-iteration
+// K.p and P.r products of the PCG (Alg. 1 l.16-21; rows a4/a7/a9)
+// reading only the block upper triangle of a bitwise-symmetric matrix, i.e.
+// half the HBM bytes of gemv.cu.  K is symmetric by construction (P:141-147,
+// K_ij = exp(scale <e_i, e_j>) with q = k, reading R2) and so is
+// P = Sigma*^{-1/2} (formed bitwise symmetric, B4); the
+// host verifies bitwise symmetry on the device before selecting this path
+// (symv_check_kernel) and otherwise uses gemv.cu.
+//
+// Blocking: block-rows of 128 rows, tiles of 128 rows x 32 columns (32 KiB),
+// block-row I streams the tiles with column index jt >= 4I.  The four tiles
+// over the diagonal block contribute to rows only; every other tile (I, jt)
+// contributes K_IJ x_J to its rows and K_IJ^T x_I to the rows of column
+// block jt (K_ji = K_ij).  With tiles linearised row-major over the upper
+// triangle, persistent CTA b owns the contiguous range [T b/G, T (b+1)/G).
+//
+// Roles (one CTA per SM): a producer warp loads each tile with one 2-D TMA
+// (cp.async.bulk.tensor, OOB rows/columns zero-filled -> ragged n) plus the
+// 32-entry slice of x with a 1-D bulk copy into a 6-stage mbarrier ring;
+// 16 consumer warps (warp w: rows 8w .. 8w+7, column c = lane) keep one Dot2
+// pair per row for the whole block-row segment and one Dot2 pair for their
+// column per tile; a reducer warp sums the 16 warps' column pairs of each tile
+// in a fixed order and stores one pair per column to `colpart[I][j]`.  At the
+// end of a block-row segment each consumer warp reduces its 8 row pairs over
+// its 32 lanes and stores them to `rowpart`.
+//
+// symv_finalize_kernel then forms, for every row i of block-row J,
+//   y_i = RN( sum_{I<J} colpart[I][i] + sum_{segments} rowpart + lambda x_i )
+// in a fixed order, plus the Dot2 pair x_i y_i per CTA, and the last CTA runs
+// the PCG scalar epilogue (delta / beta / store), exactly as gemv.cu.  Every
+// partial is an unrounded Dot2 pair combined by TwoSum, so y_i is the
+// correctly rounded row sum in practice and bitwise equal to gemv.cu and to
+// the oracle's sequential Dot2 (tests/test_gpu_symv.py).
+#include <cuda.h>
+
+#include <vector>
+
+#include "laker_internal.h"
+#include "tma.cuh"
+
+namespace laker {
+namespace {
+
+constexpr int kSR = 128;                 // rows per block-row
+constexpr int kSC = 32;                  // columns per tile
+constexpr int kTPD = kSR / kSC;          // tiles per diagonal block
+constexpr int kRPT = 8;                  // rows per consumer thread
+constexpr int kCons = 512;               // consumer threads
+constexpr int kConsWarps = kCons / 32;   // 16
+constexpr int kRedWarps = 4;             // warps 16..19: column reducers (one per SM sub-partition)
+constexpr int kRedWarp0 = kConsWarps;
+constexpr int kProdWarp = kConsWarps + kRedWarps;  // warp 20: TMA producer
+constexpr int kSymThreads = (kConsWarps + kRedWarps + 1) * 32;
+constexpr int kSStages = 6;
+constexpr uint32_t kTileBytes = kSR * kSC * 8;   // 32768
+constexpr uint32_t kXBytes = kSC * 8;            // 256
+constexpr size_t kStageBytes = kTileBytes + 512;  // tile + x slice (keeps 512 B alignment)
+constexpr int kRedBufs = 3;
+constexpr size_t kRedBytes = kRedBufs * kConsWarps * kSC * sizeof(dd_pair);  // [3][16 warps][32 cols]
+constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 64 * sizeof(uint64_t);
+constexpr int kFinThreads = 256;
+constexpr int kFinSub = 8;               // threads per row in the finalize kernel
+
+struct SymvArgs {
+  int64_t n;
+  int32_t nb, nct, maxseg;
+  int64_t T;
+  const int64_t *toff;   // [nb + 1] first tile of each block-row
+  const int32_t *segfirst;  // [nb] first CTA covering block-row I
+  const int32_t *nseg;   // [nb]
+  const double *x;       // padded to >= nct * 64 (zeros past n)
+  double *y;
+  double lambda;
+  PcgState *state;
+  int epi;
+  double *dot_out;
+  dd_pair *pair_out;
+  dd_pair *colpart;      // [nb][ldcp]
+  int64_t ldcp;
+  dd_pair *rowpart;      // [nb][maxseg][128]
+  dd_pair *partials;     // finalize: per-CTA pairs
+  unsigned int *counter;
+  int evict_first;
+};
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int32_t c0, int32_t c1,
+                                            uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+
+__device__ __forceinline__ int find_block_row(const int64_t *toff, int nb, int64_t t) {
+  int lo = 0, hi = nb - 1;  // largest I with toff[I] <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (toff[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kSymThreads, 1)
+    symv_dot2_kernel(const __grid_constant__ CUtensorMap tm, const SymvArgs a) {
+  if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
+  extern __shared__ __align__(128) unsigned char smem[];  // 128 B suffices for unswizzled TMA
+  dd_pair *red = reinterpret_cast<dd_pair *>(smem + kSStages * kStageBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSStages * kStageBytes + kRedBytes);
+  uint64_t *empty = full + kSStages;
+  uint64_t *rfull = empty + kSStages;  // [kRedBufs]
+  uint64_t *rempty = rfull + kRedBufs;  // [kRedBufs]
+  __shared__ int s_I0;
+  __shared__ double s_xr[kConsWarps][kRPT];  // x at the consumer warp's 16 rows (warp-private)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t t0 = a.T * blockIdx.x / gridDim.x;
+  const int64_t t1 = a.T * (blockIdx.x + 1) / gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < kSStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsWarps);
+    }
+    for (int b = 0; b < kRedBufs; ++b) {
+      mbar_init(&rfull[b], kConsWarps);
+      mbar_init(&rempty[b], kRedWarps);
+    }
+    fence_mbar_init();
+    s_I0 = find_block_row(a.toff, a.nb, t0);
+  }
+  if (warp == kProdWarp && lane == 0) prefetch_tmap(&tm);
+  __syncthreads();
+  if (t0 >= t1) return;
+  const int I0 = s_I0;
+
+  if (warp == kProdWarp) {
+    // ------------------------------------------------ TMA producer (one lane)
+    if (lane == 0) {
+      const uint64_t pol_a = a.evict_first ? l2_policy_evict_first() : l2_policy_evict_last();
+      const uint64_t pol_x = l2_policy_evict_last();
+      int I = I0;
+      int64_t rbeg = a.toff[I], rend = a.toff[I + 1];
+      int slot = 0;
+      uint32_t ph = 0;
+      bool first = true;
+      for (int64_t t = t0; t < t1; ++t) {
+        while (t >= rend) {
+          rbeg = rend;
+          rend = a.toff[++I + 1];
+        }
+        const int jt = kTPD * I + (int)(t - rbeg);
+        if (!first) mbar_wait(&empty[slot], ph ^ 1u);
+        unsigned char *st = smem + slot * kStageBytes;
+        mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
+        tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
+        bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
+        if (++slot == kSStages) {
+          slot = 0;
+          ph ^= 1u;
+          first = false;
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp >= kRedWarp0) {
+    // ------------------------------------------------ column reducers: warp r owns columns
+    // 8r .. 8r+7; lane l sums the pairs of warps 4q .. 4q+3 (q = l / 8) of column 8r + l % 8,
+    // then the four q-partials are combined by shuffles -- a fixed-shape tree.
+    const int r = warp - kRedWarp0, q = lane >> 3, col = 8 * r + (lane & 7);
+    int I = I0;
+    int64_t rbeg = a.toff[I], rend = a.toff[I + 1];
+    int b = 0;
+    uint32_t rph = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      while (t >= rend) {
+        rbeg = rend;
+        rend = a.toff[++I + 1];
+      }
+      const int jt = kTPD * I + (int)(t - rbeg);
+      if (jt / kTPD == I) continue;  // diagonal-block tile: rows only
+      mbar_wait(&rfull[b], rph);
+      const dd_pair *rb = red + b * kConsWarps * kSC + 4 * q * kSC + col;
+      dd_pair v0 = rb[0], v1 = rb[kSC], v2 = rb[2 * kSC], v3 = rb[3 * kSC];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rempty[b]);
+      pair_add(v0, v1);
+      pair_add(v2, v3);
+      pair_add(v0, v2);
+#pragma unroll
+      for (int off = 8; off < 32; off <<= 1) {
+        dd_pair o;
+        o.s = __shfl_down_sync(0xffffffffu, v0.s, off);
+        o.c = __shfl_down_sync(0xffffffffu, v0.c, off);
+        if ((q & ((2 * off >> 3) - 1)) == 0) pair_add(v0, o);
+      }
+      if (q == 0) a.colpart[(int64_t)I * a.ldcp + (int64_t)jt * kSC + col] = v0;
+      if (++b == kRedBufs) {
+        b = 0;
+        rph ^= 1u;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  const int c = lane;  // column within the tile; rows 8 warp .. 8 warp + 7
+  dd_pair acc[kRPT];
+  double *xr = s_xr[warp];
+  int curI = -1;
+  int64_t rbeg = 0, rend = 0;
+  int slot = 0, b = 0;
+  uint32_t ph = 0, rph = 0;
+  bool rfirst = true;
+
+  auto flush_rows = [&](int I) {
+    // reduce the 8 row pairs over the warp's 32 columns; lane k stores row k
+    const int s = blockIdx.x - a.segfirst[I];
+    dd_pair *dst = a.rowpart + ((int64_t)I * a.maxseg + s) * kSR + warp * kRPT;
+#pragma unroll
+    for (int k = 0; k < kRPT; ++k) {
+      dd_pair v = warp_reduce_pair(acc[k]);
+      v.s = __shfl_sync(0xffffffffu, v.s, 0);
+      v.c = __shfl_sync(0xffffffffu, v.c, 0);
+      if (lane == k) dst[k] = v;
+    }
+  };
+
+  for (int64_t t = t0; t < t1; ++t) {
+    if (t >= rend) {
+      if (curI >= 0) flush_rows(curI);
+      curI = (curI < 0) ? I0 : curI + 1;
+      while (t >= a.toff[curI + 1]) ++curI;
+      rbeg = a.toff[curI];
+      rend = a.toff[curI + 1];
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{0.0, 0.0};
+      __syncwarp();
+      if (lane < kRPT) xr[lane] = a.x[(int64_t)curI * kSR + warp * kRPT + lane];
+      __syncwarp();
+    }
+    const int I = curI;
+    const int jt = kTPD * I + (int)(t - rbeg);
+    const bool diag = jt / kTPD == I;
+    mbar_wait(&full[slot], ph);
+    const double *tile = reinterpret_cast<const double *>(smem + slot * kStageBytes);
+    const double xc = tile[kSR * kSC + c];
+    const double *tp = tile + warp * kRPT * kSC + c;
+    dd_pair cacc = {0.0, 0.0};
+    if (diag) {
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) dot2_step(acc[k], tp[k * kSC], xc);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) {
+        const double v = tp[k * kSC];
+        dot2_step(acc[k], v, xc);
+        dot2_step(cacc, v, xr[k]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == kSStages) {
+      slot = 0;
+      ph ^= 1u;
+    }
+    if (!diag) {
+      if (!rfirst) mbar_wait(&rempty[b], rph ^ 1u);
+      red[b * kConsWarps * kSC + warp * kSC + c] = cacc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rfull[b]);
+      if (++b == kRedBufs) {
+        b = 0;
+        rph ^= 1u;
+        rfirst = false;
+      }
+    }
+  }
+  if (curI >= 0) flush_rows(curI);
+}
+
+// y_i = RN(sum of the partial pairs of row i in a fixed order + lambda x_i); Dot2 x.y
+// per CTA; the last CTA reduces the CTA pairs in CTA order and runs the epilogue.
+__global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
+  if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
+  __shared__ dd_pair sred[kFinThreads / 32];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int sub = lane & (kFinSub - 1);
+  const int64_t i = ((int64_t)blockIdx.x * kFinThreads + tid) / kFinSub;
+  dd_pair dotp = {0.0, 0.0};
+  dd_pair v = {0.0, 0.0};
+  const bool valid = i < a.n;
+  const int J = valid ? (int)(i / kSR) : 0, r = valid ? (int)(i % kSR) : 0;
+  if (valid) {
+    // column partials of the tiles (I, .) above this row's diagonal block, I = sub (mod 8)
+    for (int I = sub; I < J; I += kFinSub) {
+      dd_pair o;
+      o.s = __ldcg(&a.colpart[(int64_t)I * a.ldcp + i].s);
+      o.c = __ldcg(&a.colpart[(int64_t)I * a.ldcp + i].c);
+      pair_add(v, o);
+    }
+    // row partials of this block-row's segments
+    const int ns = a.nseg[J];
+    for (int q = sub; q < ns; q += kFinSub) {
+      const dd_pair *p = a.rowpart + ((int64_t)J * a.maxseg + q) * kSR + r;
+      dd_pair o;
+      o.s = __ldcg(&p->s);
+      o.c = __ldcg(&p->c);
+      pair_add(v, o);
+    }
+  }
+  // combine the 8 sub-sums in sub order (lanes sub = 0..7 of this row); all lanes shuffle
+#pragma unroll
+  for (int off = 1; off < kFinSub; off <<= 1) {
+    dd_pair o;
+    o.s = __shfl_down_sync(0xffffffffu, v.s, off, kFinSub);
+    o.c = __shfl_down_sync(0xffffffffu, v.c, off, kFinSub);
+    if ((sub & (2 * off - 1)) == 0) pair_add(v, o);
+  }
+  if (valid && sub == 0) {
+    const double xi = a.x[i];
+    if (a.lambda != 0.0) dot2_step(v, a.lambda, xi);
+    const double yv = pair_value(v);
+    a.y[i] = yv;
+    dot2_step(dotp, xi, yv);
+  }
+  dotp = warp_reduce_pair(dotp);
+  if (lane == 0) sred[warp] = dotp;
+  __syncthreads();
+  if (tid == 0) {
+    dd_pair t = sred[0];
+    for (int w = 1; w < kFinThreads / 32; ++w) pair_add(t, sred[w]);
+    a.partials[blockIdx.x] = t;
+    __threadfence();
+    s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || warp != 0) return;
+  __threadfence();
+  v = dd_pair{0.0, 0.0};
+  for (int b = lane; b < (int)gridDim.x; b += 32) {
+    dd_pair o = {__ldcg(&a.partials[b].s), __ldcg(&a.partials[b].c)};
+    pair_add(v, o);
+  }
+  v = warp_reduce_pair(v);
+  if (lane != 0) return;
+  *a.counter = 0u;
+  PcgState *st = a.state;
+  const double dv = pair_value(v);
+  switch (a.epi) {
+    case kEpiDelta:
+      if (!(dv > 0.0)) {
+        st->term = LAKER_TERM_BREAKDOWN;
+        st->done = 1;
+      } else {
+        st->delta = __ddiv_rn(st->rho, dv);
+      }
+      break;
+    case kEpiBeta:
+      if (!(dv > 0.0)) {
+        st->term = LAKER_TERM_INDEFINITE;
+        st->done = 1;
+      } else {
+        st->beta = __ddiv_rn(dv, st->rho);
+        st->rho = dv;
+      }
+      break;
+    case kEpiStoreDot:
+      if (a.dot_out) *a.dot_out = dv;
+      break;
+    case kEpiStorePair:
+      if (a.pair_out) *a.pair_out = v;
+      break;
+    default:
+      break;
+  }
+}
+
+// flag[0] = 1 if A (n x n, row stride ld) is not bitwise symmetric
+__global__ void symv_check_kernel(const double *__restrict__ A, int64_t n, int64_t ld, int *flag) {
+  __shared__ double tI[32][33];
+  __shared__ double tJ[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = (int64_t)bi * 32 + r, j = (int64_t)bj * 32 + tx;
+    tI[r][tx] = (i < n && j < n) ? A[i * ld + j] : 0.0;
+    const int64_t i2 = (int64_t)bj * 32 + r, j2 = (int64_t)bi * 32 + tx;
+    tJ[r][tx] = (i2 < n && j2 < n) ? A[i2 * ld + j2] : 0.0;
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int r = ty; r < 32; r += 8)
+    bad |= __double_as_longlong(tI[r][tx]) != __double_as_longlong(tJ[tx][r]);
+  if (__syncthreads_or(bad) && tx == 0 && ty == 0) atomicExch(flag, 1);
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                     const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+struct SymvPlan {
+  int64_t n = 0, ld = 0, T = 0, ldcp = 0;
+  int nb = 0, nct = 0, maxseg = 0, grid = 0, fin_grid = 0;
+  int64_t *toff = nullptr;
+  int32_t *segfirst = nullptr, *nseg = nullptr;
+  dd_pair *colpart = nullptr, *rowpart = nullptr;
+  CUtensorMap tm[2];
+  const void *tm_base[2] = {nullptr, nullptr};
+};
+
+size_t symv_smem_bytes() { return kSymSmem; }
+
+void symv_init() {
+  cudaFuncSetAttribute(symv_dot2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
+}
+
+void symv_free(SymvPlan *&p) {
+  if (!p) return;
+  cudaFree(p->toff);
+  cudaFree(p->segfirst);
+  cudaFree(p->nseg);
+  cudaFree(p->colpart);
+  cudaFree(p->rowpart);
+  delete p;
+  p = nullptr;
+}
+
+cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
+  if (p && p->n == n && p->ld == ld) return cudaSuccess;
+  symv_free(p);
+  p = new SymvPlan();
+  p->n = n;
+  p->ld = ld;
+  p->nb = (int)((n + kSR - 1) / kSR);
+  p->nct = (int)((n + kSC - 1) / kSC);
+  std::vector<int64_t> toff(p->nb + 1, 0);
+  for (int I = 0; I < p->nb; ++I) toff[I + 1] = toff[I] + (p->nct - kTPD * I);
+  p->T = toff[p->nb];
+  p->grid = (int)std::min<int64_t>(num_sms, p->T);
+  std::vector<int32_t> segfirst(p->nb), nseg(p->nb);
+  auto cta_of = [&](int64_t t) {  // CTA b with floor(T b / G) <= t < floor(T (b+1) / G)
+    int64_t b = (t * p->grid) / p->T;
+    while (b + 1 < p->grid && p->T * (b + 1) / p->grid <= t) ++b;
+    while (b > 0 && p->T * b / p->grid > t) --b;
+    return (int)b;
+  };
+  p->maxseg = 1;
+  for (int I = 0; I < p->nb; ++I) {
+    segfirst[I] = cta_of(toff[I]);
+    nseg[I] = cta_of(toff[I + 1] - 1) - segfirst[I] + 1;
+    p->maxseg = std::max(p->maxseg, (int)nseg[I]);
+  }
+  p->ldcp = (int64_t)p->nct * kSC;
+  const int64_t rows_fin = (int64_t)n * kFinSub;
+  p->fin_grid = (int)((rows_fin + kFinThreads - 1) / kFinThreads);
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->segfirst, segfirst.size() * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->nseg, nseg.size() * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->colpart, (size_t)p->nb * p->ldcp * sizeof(dd_pair))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->rowpart, (size_t)p->nb * p->maxseg * kSR * sizeof(dd_pair))) != cudaSuccess) return e;
+  cudaMemcpy(p->toff, toff.data(), toff.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->segfirst, segfirst.data(), segfirst.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->nseg, nseg.data(), nseg.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  return cudaSuccess;
+}
+
+int symv_finalize_grid(const SymvPlan *p) { return p->fin_grid; }
+
+// which = 0 (K) or 1 (P); (re)encodes the tensor map when the base pointer changed
+bool symv_bind(SymvPlan *p, int which, const double *A) {
+  if (p->tm_base[which] == A) return true;
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)p->n, (cuuint64_t)p->n};
+  cuuint64_t strides[1] = {(cuuint64_t)p->ld * sizeof(double)};
+  cuuint32_t box[2] = {kSC, kSR};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&p->tm[which], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(A), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  p->tm_base[which] = A;
+  return true;
+}
+
+void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s) {
+  SymvArgs a{};
+  a.n = p->n;
+  a.nb = p->nb;
+  a.nct = p->nct;
+  a.maxseg = p->maxseg;
+  a.T = p->T;
+  a.toff = p->toff;
+  a.segfirst = p->segfirst;
+  a.nseg = p->nseg;
+  a.x = g.x;
+  a.y = g.y;
+  a.lambda = g.lambda;
+  a.state = g.state;
+  a.epi = g.epi;
+  a.dot_out = g.dot_out;
+  a.pair_out = g.pair_out;
+  a.colpart = p->colpart;
+  a.ldcp = p->ldcp;
+  a.rowpart = p->rowpart;
+  a.partials = g.partials;
+  a.counter = g.counter;
+  a.evict_first = g.evict_first ? 1 : 0;
+  symv_dot2_kernel<<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
+  symv_finalize_kernel<<<p->fin_grid, kFinThreads, 0, s>>>(a);
+}
+
+void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s) {
+  const int nt = (int)((n + 31) / 32);
+  symv_check_kernel<<<dim3(nt, nt), dim3(32, 8), 0, s>>>(A, n, ld, flag);
+}
+
+}  // namespace laker

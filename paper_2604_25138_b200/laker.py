@@ -74,7 +74,8 @@ class Stats(ctypes.Structure):
                 ("op_launches", ctypes.c_int64), ("prec_launches", ctypes.c_int64),
                 ("assemble_ms", ctypes.c_double), ("fit_ms", ctypes.c_double),
                 ("solve_ms", ctypes.c_double), ("predict_ms", ctypes.c_double),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64),
+                ("symmetric_k", ctypes.c_int32), ("symmetric_p", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
