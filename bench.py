@@ -105,11 +105,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def _traffic_per_launch():
-    """dram bytes per GEMV launch from the committed `ncu --set full` summary, if any."""
+def _traffic_per_launch(kind: str):
+    """dram bytes per operator-apply launch (kind 'symv' or 'gemv') from the committed
+    `ncu --set full` summary (profiles/roofline_traffic.json), if any."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     try:
-        return json.load(open(p)).get("gemv_bytes_per_launch")
+        return json.load(open(p)).get(f"{kind}_bytes_per_launch")
     except Exception:
         return None
 
@@ -266,15 +267,34 @@ def run_ours(args, rank, world, local_rank):
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     rows = n // world
-    bytes_per_launch = 8.0 * rows * n + 16.0 * n
+    sym, fac, nr = s1["symmetric_k"], s1["p_factored"], s1["n_dirs"]
+    # algorithmic bytes per operator apply: the stored
+    # triangle of the symmetric K (symv) or the local rows (gemv), plus x read and y written
+    if sym:
+        bytes_per_launch = 8.0 * n * (n + 1) / 2 + 16.0 * n
+        kname = "symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, Dot2)"
+    else:
+        bytes_per_launch = 8.0 * rows * n + 16.0 * n
+        kname = "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)"
+    if fac:
+        prec_bytes = 8.0 * (2 * n * nr + nr * nr) + 8.0 * (3 * n + 4 * nr)
+        pname = "3 x gemv_dot2_kernel: z = Q^T r, w = M z, theta = a^-1/2 r + Q w (factored P)"
+    elif args.precond == "learned":
+        prec_bytes = (8.0 * n * (n + 1) / 2 if s1["symmetric_p"] else 8.0 * rows * n) + 16.0 * n
+        pname = "symv (dense P)" if s1["symmetric_p"] else "gemv (dense P)"
+    else:
+        prec_bytes, pname = None, None
     dom_ms = op_ms if op_launches else float("nan")
     achieved = bytes_per_launch / (dom_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)",
+    roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback",
-            "traffic": _traffic_per_launch(), "bytes_per_launch": bytes_per_launch,
-            "mean_launch_ms": dom_ms, "launches": op_launches,
-            "precond_gemv_mean_launch_ms": prec_ms if prec_launches else None}
+            "traffic": _traffic_per_launch("symv" if sym else "gemv"), "bytes_per_launch": bytes_per_launch,
+            "mean_launch_ms": dom_ms, "launches": op_launches}
+    if prec_bytes and prec_launches:
+        roof["precond"] = {"kernel": pname, "bytes_per_apply": prec_bytes, "mean_apply_ms": prec_ms,
+                           "achieved": prec_bytes / (prec_ms * 1e-3) / 1e9, "applies": prec_launches,
+                           "frac": prec_bytes / (prec_ms * 1e-3) / 1e9 / hbm_peak}
     clocks = clk.summary()
     ctx.close()
     if rank != 0:
@@ -285,6 +305,9 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": "C3 (BASELINE.json configs[2]): n=16384 clustered sensors, d=64, "
                                    "lambda=1e-4, PCG to rel resid 1e-8, K materialized 2 GiB, grid 256x256",
                        "precond": args.precond, "mode": args.mode, "parallelism": f"rowshard{world}",
+                       "k_apply": "symmetric (upper triangle)" if sym else "full rows",
+                       "p_layout": ("factored, N_r=%d" % nr) if fac else ("dense" if args.precond == "learned"
+                                                                           else args.precond),
                        "l2": "inputs larger than L2 (K = 2 GiB per solve pass >> 126 MB)"},
             "time_to_solution_s": pcg_total / args.steps, "pcg_iters_per_solve": its[0],
             "stage_ms": {k: v / args.steps for k, v in stage.items()},

@@ -114,7 +114,18 @@ typedef struct {
   const double *Z;   /* n x N_r column-major N(0,1) draws z_k (Eq. random_directions,
                         P:239), host or device; NULL -> device Philox stream `seed` */
   uint64_t seed;
+  int32_t p_layout;  /* how P = Sigma*^{-1/2} is stored and applied (LAKER_P_*):
+                        AUTO (0): FACTORED on one rank, DENSE rows when sharded */
 } laker_fit_opts;
+
+/* P = a^{-1/2} I + Q M Q^T with Q (n x N_r, orthonormal columns, the thin QR of
+   Ubar) and M = T^{-1/2} - a^{-1/2} I (N_r x N_r) is exact (O4').
+   DENSE: the n x n rows are formed (bitwise symmetric, B4) and each apply
+   streams them (8 n^2 bytes, or 4 n^2 through the symmetric GEMV).
+   FACTORED: Q^T, Q and M are kept and each apply is theta = a^{-1/2} r +
+   Q (M (Q^T r)) -- three Dot2 GEMV passes, 16 n N_r + 8 N_r^2 bytes (SURVEY
+   §8(f) NEXT-1); no n x n matrix is formed. */
+enum { LAKER_P_AUTO = 0, LAKER_P_DENSE = 1, LAKER_P_FACTORED = 2 };
 
 typedef struct {
   int32_t iters, n_dirs, converged;
@@ -184,6 +195,10 @@ laker_status laker_get_kernel_rows(laker_ctx ctx, double *K_rows);
    or NULL to derive it from the assembled K; NONE: data ignored. */
 laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *data);
 laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows);
+/* LEARNED P in factored form: Q (n x n_dirs row-major), M (n_dirs x n_dirs
+   row-major) and the scalar a^{-1/2} (host), so that P = a^{-1/2} I + Q M Q^T;
+   any pointer may be NULL.  NOT_READY if the context holds no factored P. */
+laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *M, double *a_inv_sqrt);
 /* y = (lambda I + K) x, x and y length n (y complete on every rank). */
 laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y);
 
@@ -199,6 +214,7 @@ typedef struct {
   int64_t kernel_launches;       /* kernels this context launched since creation */
   int32_t symmetric_k, symmetric_p; /* 1: K / dense P found bitwise symmetric on one rank, so the
                                        PCG applies stream only their block upper triangle (symv) */
+  int32_t p_factored, n_dirs;    /* 1: LEARNED P held as Q, M, a (LAKER_P_FACTORED); its N_r */
 } laker_stats;
 laker_status laker_get_stats(laker_ctx ctx, laker_stats *out);
 

@@ -13,6 +13,11 @@
  *   orc_apply        q = (lambda I + K) p                 P:517-519 (matvec remark)
  *   orc_jacobi_diag  d_i = 1 / (lambda + K_ii)            P:727, P:757-758 (Jacobi PCG baseline)
  *   orc_pcg          Alg. 1 "Preconditioned Conjugate Gradient", P:306-321 (and P:589-626), verbatim
+ *   orc_factored_apply / orc_pcg_factored
+ *                    theta = P r with P = Sigma*^{-1/2} held as a^{-1/2} I + Q M Q^T
+ *                    (Eq. preconditioner-Sigmma P:273-278 in the structured form
+ *                    of DESIGN.md O4': Sigma* = a I + Q (T - a I) Q^T, Q^T Q = I,
+ *                    so Sigma*^{-1/2} = a^{-1/2} I + Q (T^{-1/2} - a^{-1/2} I) Q^T)
  *
  * Rounding policy (readings R17/R18): every inner product is Dot2
  * (Ogita, Rump & Oishi, "Accurate sum and dot product", SIAM J. Sci. Comput.
@@ -179,8 +184,40 @@ ORC_API int64_t orc_jacobi_diag(int64_t n, int32_t d, const double *E, double sc
   return n_overflow;
 }
 
+/* ------------------------------------------------------- factored P apply */
+/* P = ainv I + Q M Q^T: Q n x m row-major, M m x m row-major (O4').
+   z_k = RN(sum_i Q_ik r_i), w_k = RN(sum_j M_kj z_j),
+   theta_i = RN(ainv r_i + sum_k Q_ik w_k), each a Dot2 in index order. */
+typedef struct { int64_t m; const double *Q, *M; double ainv; } orc_factored;
+
+static void factored_apply(int64_t n, const orc_factored *F, const double *r, double *theta) {
+  const int64_t m = F->m;
+  double *z = malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  double *w = malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < m; ++k) z[k] = dot2(n, F->Q + k, m, r, 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < m; ++k) w[k] = dot2(m, F->M + k * m, 1, z, 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    dot2_t A = {0.0, 0.0};
+    dot2_add(&A, F->ainv, r[i]);
+    const double *q = F->Q + i * m;
+    for (int64_t k = 0; k < m; ++k) dot2_add(&A, q[k], w[k]);
+    theta[i] = dot2_result(A);
+  }
+  free(z);
+  free(w);
+}
+
+ORC_API void orc_factored_apply(int64_t n, int64_t m, const double *Q, const double *M, double ainv,
+                                const double *r, double *theta) {
+  orc_factored F = {m, Q, M, ainv};
+  factored_apply(n, &F, r, theta);
+}
+
 /* ----------------------------------------------------------------------- PCG */
-enum { ORC_P_NONE = 0, ORC_P_JACOBI = 1, ORC_P_DENSE = 2 };
+enum { ORC_P_NONE = 0, ORC_P_JACOBI = 1, ORC_P_DENSE = 2, ORC_P_FACTORED = 3 };
 enum { ORC_TERM_RESIDUAL_TOL = 0, ORC_TERM_MAX_ITERS = 1, ORC_TERM_ZERO_RHS = 2,
        ORC_TERM_BREAKDOWN = 3, ORC_TERM_INDEFINITE = 4 };
 
@@ -191,11 +228,14 @@ typedef struct {
   double true_rel_residual; /* ||y - (lambda I + K) alpha|| / ||y|| recomputed at exit */
 } orc_pcg_report;
 
-static void precond_apply(int pkind, int64_t n, const double *P, const double *r, double *theta) {
+static void precond_apply(int pkind, int64_t n, const double *P, const orc_factored *F, const double *r,
+                          double *theta) {
   if (pkind == ORC_P_NONE) {
     memcpy(theta, r, (size_t)n * sizeof(double));
   } else if (pkind == ORC_P_JACOBI) {
     for (int64_t i = 0; i < n; ++i) theta[i] = P[i] * r[i];
+  } else if (pkind == ORC_P_FACTORED) {
+    factored_apply(n, F, r, theta);
   } else {
     dense_apply(n, P, r, theta);
   }
@@ -210,8 +250,8 @@ static void precond_apply(int pkind, int64_t n, const double *P, const double *r
  * P: NULL for NONE, diag (n) for JACOBI, dense n x n row-major for DENSE.
  * history (optional, >= max_iters): ||r^{k+1}|| / ||y|| per iteration.
  */
-ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, int pkind,
-                    const double *P, double tol, int32_t max_iters, double *alpha,
+static int pcg_impl(int64_t n, const double *K, double lambda, const double *y, int pkind,
+                    const double *P, const orc_factored *F, double tol, int32_t max_iters, double *alpha,
                     orc_pcg_report *rep, double *history) {
   double *r = malloc(sizeof(double) * n), *th = malloc(sizeof(double) * n);
   double *p = malloc(sizeof(double) * n), *q = malloc(sizeof(double) * n);
@@ -223,7 +263,7 @@ ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, 
     rep->termination = ORC_TERM_ZERO_RHS;
     goto done;
   }
-  precond_apply(pkind, n, P, r, th);
+  precond_apply(pkind, n, P, F, r, th);
   memcpy(p, th, sizeof(double) * n);
   double rho = dot2(n, r, 1, th, 1);
   if (!(rho > 0.0)) { rep->termination = ORC_TERM_INDEFINITE; status = 1; goto done; }
@@ -242,7 +282,7 @@ ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, 
     rep->rel_residual = rel;
     if (history) history[k] = rel;
     if (rel <= tol) { rep->termination = ORC_TERM_RESIDUAL_TOL; break; }
-    precond_apply(pkind, n, P, r, th);
+    precond_apply(pkind, n, P, F, r, th);
     double rho_new = dot2(n, r, 1, th, 1);
     if (!(rho_new > 0.0)) { rep->termination = ORC_TERM_INDEFINITE; status = 1; break; }
     double beta = rho_new / rho;
@@ -262,6 +302,21 @@ ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, 
 done:
   free(r); free(th); free(p); free(q);
   return status;
+}
+
+ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, int pkind,
+                    const double *P, double tol, int32_t max_iters, double *alpha,
+                    orc_pcg_report *rep, double *history) {
+  if (pkind == ORC_P_FACTORED) return -1; /* use orc_pcg_factored */
+  return pcg_impl(n, K, lambda, y, pkind, P, NULL, tol, max_iters, alpha, rep, history);
+}
+
+/* PCG with the factored P = ainv I + Q M Q^T (Q n x m, M m x m, row-major). */
+ORC_API int orc_pcg_factored(int64_t n, const double *K, double lambda, const double *y, int64_t m,
+                             const double *Q, const double *M, double ainv, double tol, int32_t max_iters,
+                             double *alpha, orc_pcg_report *rep, double *history) {
+  orc_factored F = {m, Q, M, ainv};
+  return pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
 }
 
 /* Thread count actually used by the parallel loops (for cpu_baseline.cores). */

@@ -35,8 +35,8 @@ import scipy.linalg as sla
 
 __all__ = [
     "lib", "exp_cr", "dot2", "assemble", "assemble_rows", "cross_kernel", "predict",
-    "apply", "dense_apply", "jacobi_diag", "pcg", "PcgReport", "P_NONE", "P_JACOBI",
-    "P_DENSE", "TERM_RESIDUAL_TOL", "TERM_MAX_ITERS", "TERM_ZERO_RHS", "TERM_BREAKDOWN",
+    "apply", "dense_apply", "factored_apply", "jacobi_diag", "pcg", "pcg_factored", "PcgReport",
+    "P_NONE", "P_JACOBI", "P_DENSE", "factors", "TERM_RESIDUAL_TOL", "TERM_MAX_ITERS", "TERM_ZERO_RHS", "TERM_BREAKDOWN",
     "TERM_INDEFINITE", "rho_schedule", "nr_schedule", "directions", "cccp_step_literal",
     "cccp_fit_literal",
     "cccp_fit_structured", "FitReport", "reference_solve", "cond_spd", "cond_precond",
@@ -65,6 +65,9 @@ def _load():
     L.orc_jacobi_diag.argtypes = [i64, i32, D, dbl, dbl, D]; L.orc_jacobi_diag.restype = i64
     L.orc_pcg.argtypes = [i64, D, dbl, D, ctypes.c_int, D, dbl, i32, D, ctypes.c_void_p, D]
     L.orc_pcg.restype = ctypes.c_int
+    L.orc_factored_apply.argtypes = [i64, i64, D, D, dbl, D, D]; L.orc_factored_apply.restype = None
+    L.orc_pcg_factored.argtypes = [i64, D, dbl, D, i64, D, D, dbl, dbl, i32, D, ctypes.c_void_p, D]
+    L.orc_pcg_factored.restype = ctypes.c_int
     L.orc_num_threads.argtypes = []; L.orc_num_threads.restype = ctypes.c_int
     return L
 
@@ -154,6 +157,16 @@ def dense_apply(P, r) -> np.ndarray:
     return th
 
 
+def factored_apply(Q, M, ainv: float, r) -> np.ndarray:
+    """theta = P r with P = ainv I + Q M Q^T held in factored form (P:273-278 via
+    O4'): z = Q^T r, w = M z, theta_i = ainv r_i + Q_i. w, each entry one Dot2."""
+    Q, M, r = _c(Q), _c(M), _c(r)
+    n, m = Q.shape
+    th = np.empty(n)
+    lib.orc_factored_apply(n, m, _p(Q), _p(M), float(ainv), _p(r), _p(th))
+    return th
+
+
 def jacobi_diag(E, scale: float, lam: float) -> np.ndarray:
     """P_J = diag(lambda I + G)^{-1} (P:727, P:757-758)."""
     E = _c(E)
@@ -199,6 +212,21 @@ def pcg(K, lam: float, y, pkind: int = P_NONE, P=None, tol: float = 1e-10,
 
 
 # --------------------------------------------------------------- CCCP fit
+def pcg_factored(K, lam: float, y, Q, M, ainv: float, tol: float = 1e-10,
+                 max_iters: Optional[int] = None):
+    """`pcg` with the factored preconditioner of `factored_apply`."""
+    K, y, Q, M = _c(K), _c(y), _c(Q), _c(M)
+    n = K.shape[0]
+    max_iters = 10 * n if max_iters is None else int(max_iters)
+    alpha = np.empty(n)
+    hist = np.zeros(max(max_iters, 1))
+    rep = _CReport()
+    lib.orc_pcg_factored(n, _p(K), float(lam), _p(y), Q.shape[1], _p(Q), _p(M), float(ainv), float(tol),
+                         max_iters, _p(alpha), ctypes.byref(rep), _p(hist))
+    return alpha, PcgReport(rep.iters, rep.termination, rep.rel_residual, rep.true_rel_residual,
+                            hist[: rep.iters].copy())
+
+
 def nr_schedule(n: int) -> int:
     """N_r = min(n, max(ceil(8 sqrt n), ceil(n/4))) (P:743 shape)."""
     return int(min(n, max(math.ceil(8.0 * math.sqrt(n)), math.ceil(n / 4.0))))
@@ -379,6 +407,14 @@ def cccp_fit_structured(K, lam: float, Z, gamma: float = 0.1, eps: float = 1e-12
     M = Ti - Im / math.sqrt(a)
     P = np.eye(n) / math.sqrt(a) + Q @ M @ Q.T
     return 0.5 * (P + P.T), rep, state
+
+
+def factors(state) -> tuple:
+    """(Q, M, a^{-1/2}) of P = Sigma*^{-1/2} = a^{-1/2} I + Q (T^{-1/2} - a^{-1/2} I) Q^T
+    from a `cccp_fit_structured` state (O4')."""
+    a = state.a
+    M = _inv_sqrt_spd(state.T) - np.eye(state.T.shape[0]) / math.sqrt(a)
+    return state.Q, 0.5 * (M + M.T), 1.0 / math.sqrt(a)
 
 
 # ------------------------------------------------------- reference + metrics

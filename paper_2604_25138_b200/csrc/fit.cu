@@ -357,6 +357,63 @@ double host_rho(int64_t nr, int64_t n, double gamma, double lmin, double rho_flo
 
 }  // namespace
 
+void free_factors(laker_ctx ctx) {
+  cudaFree(ctx->Qt);
+  cudaFree(ctx->Qr);
+  cudaFree(ctx->Mf);
+  cudaFree(ctx->fz);
+  ctx->Qt = ctx->Qr = ctx->Mf = ctx->fz = ctx->fw = nullptr;
+  ctx->p_factored = false;
+  ctx->f_nr = ctx->f_nrp = ctx->f_ldq = 0;
+}
+
+// P = a^{-1/2} I + Q M Q^T, rows [r0, r1) into ctx->P.  P_ij = W_i . Q_j for i >= j
+// and Q_i . W_j for i < j (+ a^{-1/2} on the diagonal) with W = Q M: the upper
+// entry (i, j) is the same DMMA dot product as the lower entry (j, i) (the product
+// is commutative in its operands), so P is bitwise symmetric, every row is
+// independent of the row sharding (each rank holds W and Q in full), and the work
+// is one n_loc x n x N_r GEMM split in two (B4).
+laker_status form_dense_p(laker_ctx ctx, const double *Ut, const double *Mm, int64_t ldm, int64_t nrp,
+                          double ainv) {
+  const int64_t n = ctx->n, ld = ctx->ld;
+  cudaStream_t s = ctx->stream;
+  int64_t &L = ctx->stats.kernel_launches;
+  DevMem mem{{}, s};
+  double *Wt, *Qr, *Wr;  // Wt = M Q^T (nrp x ld); Qr, Wr row-major ld x nrp (k contiguous)
+  LAKER_CUDA(ctx, mem.alloc(&Wt, (size_t)nrp * ld));
+  LAKER_CUDA(ctx, mem.alloc(&Qr, (size_t)ld * nrp));
+  LAKER_CUDA(ctx, mem.alloc(&Wr, (size_t)ld * nrp));
+  GemmArgs g{};
+  g.M = nrp; g.N = ld; g.K = nrp; g.A = Mm; g.lda = ldm; g.B = Ut; g.ldb = ld; g.C = Wt; g.ldc = ld;
+  g.alpha = 1.0;
+  launch_dgemm(g, true, s);
+  launch_transpose(Ut, nrp, ld, ld, Qr, nrp, s);
+  launch_transpose(Wt, nrp, ld, ld, Wr, nrp, s);
+  L += 3;
+  if (!ctx->P) LAKER_CUDA(ctx, cudaMalloc(&ctx->P, (size_t)(ctx->r1 - ctx->r0) * ld * 8));
+  LAKER_CUDA(ctx, cudaMemsetAsync(ctx->P, 0, (size_t)(ctx->r1 - ctx->r0) * ld * 8, s));
+  GemmArgs p{};
+  p.M = ctx->r1 - ctx->r0; p.N = n; p.K = nrp;
+  p.A = Wr + ctx->r0 * nrp; p.lda = nrp; p.B = Qr; p.ldb = nrp; p.C = ctx->P; p.ldc = ld;
+  p.alpha = 1.0; p.diag = ainv; p.diag_offset = -ctx->r0; p.tri = 1; p.tri_off = ctx->r0;
+  launch_dgemm(p, false, s);
+  p.A = Qr + ctx->r0 * nrp; p.B = Wr; p.diag = 0.0; p.tri = 2;
+  launch_dgemm(p, false, s);
+  L += 2;
+  if (n % 2 == 1) {  // the last double2 store of each row spilled one past n: restore zero padding
+    LAKER_CUDA(ctx, cudaMemset2DAsync(ctx->P + n, ld * 8, 0, 8, ctx->r1 - ctx->r0, s));
+  }
+  LAKER_CUDA(ctx, cudaGetLastError());
+  return LAKER_OK;
+}
+
+laker_status ensure_dense_p(laker_ctx ctx) {
+  if (ctx->P || !ctx->p_factored) return LAKER_OK;
+  LAKER_TRY(form_dense_p(ctx, ctx->Qt, ctx->Mf, ctx->f_ldq, ctx->f_nrp, ctx->f_ainv));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return LAKER_OK;
+}
+
 laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_report *rep) {
   const int64_t n = ctx->n, ld = ctx->ld;
   int64_t nr = o.n_dirs;
@@ -686,41 +743,37 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   L += 2;
 
   dbg("M", Zm, nrp, nrp, nrp);
-  // ---- 5. P = a^{-1/2} I + Q M Q^T with Q^T = Ut (nrp x ld)
-  {
-    double *Wt = Zt;  // reuse: Wt = M Q^T (nrp x ld)
-    GemmArgs g{};
-    g.M = nrp; g.N = ld; g.K = nrp; g.A = Zm; g.lda = nrp; g.B = Ut; g.ldb = ld; g.C = Wt; g.ldc = ld;
-    g.alpha = 1.0;
-    launch_dgemm(g, true, s);
+  // ---- 5. P = a^{-1/2} I + Q M Q^T with Q^T = Ut (nrp x ld), M = Zm
+  const double ainv = 1.0 / std::sqrt(a);
+  const bool factored = o.p_layout == LAKER_P_FACTORED ||
+                        (o.p_layout == LAKER_P_AUTO && ctx->world == 1 && !ctx->comm);
+  free_factors(ctx);
+  if (factored) {
+    // keep the factors: Q^T for z = Q^T r, Q for Q w, and M
+    if (ctx->P) {
+      cudaFree(ctx->P);
+      ctx->P = nullptr;
+    }
+    const int64_t ldq = (nrp + 255) / 256 * 256;  // gemv streams whole 256-column chunks
+    LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ld * 8));
+    LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)n * ldq * 8));
+    LAKER_CUDA(ctx, cudaMalloc(&ctx->Mf, (size_t)nrp * ldq * 8));
+    LAKER_CUDA(ctx, cudaMalloc(&ctx->fz, (size_t)2 * ldq * 8));
+    ctx->fw = ctx->fz + ldq;
+    LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Qr, 0, (size_t)n * ldq * 8, s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Mf, 0, (size_t)nrp * ldq * 8, s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(ctx->fz, 0, (size_t)2 * ldq * 8, s));
+    LAKER_CUDA(ctx, cudaMemcpyAsync(ctx->Qt, Ut, (size_t)nrp * ld * 8, cudaMemcpyDeviceToDevice, s));
+    launch_transpose(Ut, nrp, n, ld, ctx->Qr, ldq, s);
+    LAKER_CUDA(ctx, cudaMemcpy2DAsync(ctx->Mf, ldq * 8, Zm, nrp * 8, nrp * 8, nrp, cudaMemcpyDeviceToDevice, s));
     ++L;
-    double *Qr, *Wr;  // row-major n x nrp (k contiguous)
-    LAKER_CUDA(ctx, mem.alloc(&Qr, (size_t)ld * nrp));
-    LAKER_CUDA(ctx, mem.alloc(&Wr, (size_t)ld * nrp));
-    launch_transpose(Ut, nrp, ld, ld, Qr, nrp, s);
-    launch_transpose(Wt, nrp, ld, ld, Wr, nrp, s);
-    L += 2;
-    if (!ctx->P) {
-      LAKER_CUDA(ctx, cudaMalloc(&ctx->P, (size_t)(ctx->r1 - ctx->r0) * ld * 8));
-    }
-    LAKER_CUDA(ctx, cudaMemsetAsync(ctx->P, 0, (size_t)(ctx->r1 - ctx->r0) * ld * 8, s));
-    // P_ij = W_i . Q_j for i >= j and P_ij = Q_i . W_j for i < j (+ a^{-1/2} on the
-    // diagonal): the upper entry (i, j) is the same DMMA dot product as the lower
-    // entry (j, i) (the product is commutative in its operands), so P is bitwise
-    // symmetric, every row is independent of the row sharding (each rank holds
-    // W and Q in full), and the work is one n_loc x n x N_r GEMM split in two.
-    GemmArgs p{};
-    p.M = ctx->r1 - ctx->r0; p.N = n; p.K = nrp;
-    p.A = Wr + ctx->r0 * nrp; p.lda = nrp; p.B = Qr; p.ldb = nrp; p.C = ctx->P; p.ldc = ld;
-    p.alpha = 1.0; p.diag = 1.0 / std::sqrt(a); p.diag_offset = -ctx->r0; p.tri = 1; p.tri_off = ctx->r0;
-    launch_dgemm(p, false, s);
-    p.A = Qr + ctx->r0 * nrp; p.B = Wr; p.diag = 0.0; p.tri = 2;
-    launch_dgemm(p, false, s);
-    L += 2;
-    if (n % 2 == 1) {  // the last double2 store of each row spilled one past n: restore zero padding
-      LAKER_CUDA(ctx, cudaMemset2DAsync(ctx->P + n, ld * 8, 0, 8, ctx->r1 - ctx->r0, s));
-    }
-    dbg("Wt", Wt, nrp, ld, ld);
+    ctx->f_nr = nr;
+    ctx->f_nrp = nrp;
+    ctx->f_ldq = ldq;
+    ctx->f_ainv = ainv;
+    ctx->p_factored = true;
+  } else {
+    LAKER_TRY(form_dense_p(ctx, Ut, Zm, nrp, nrp, ainv));
     dbg("P0", ctx->P, ctx->r1 - ctx->r0, n, ld);
   }
   tick("P_form");

@@ -44,7 +44,7 @@ struct Cfg {
   static constexpr int CPT = 2;                            // columns per consumer thread
   static constexpr int CHUNK = kConsumers * CPT;           // 1024 / 512 columns per unit
   static constexpr size_t STAGE = (size_t)(ROWS + NX) * CHUNK;
-  static constexpr size_t SMEM = kStages * STAGE * sizeof(double) + kWarps * ROWS * sizeof(dd_pair) +
+  static constexpr size_t SMEM = kStages * STAGE * sizeof(double) + 2 * kWarps * ROWS * sizeof(dd_pair) +
                                  2 * kStages * sizeof(uint64_t) + 16;
 };
 
@@ -112,14 +112,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   extern __shared__ __align__(128) unsigned char smem[];
   double *ring = reinterpret_cast<double *>(smem);
   dd_pair *red = reinterpret_cast<dd_pair *>(smem + kStages * C::STAGE * sizeof(double));
-  uint64_t *full = reinterpret_cast<uint64_t *>(red + kWarps * ROWS);
+  uint64_t *full = reinterpret_cast<uint64_t *>(red + 2 * kWarps * ROWS);
   uint64_t *empty = full + kStages;
   __shared__ int s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t groups = (a.rows + ROWS - 1) / ROWS;
-  const int64_t g0 = groups * blockIdx.x / gridDim.x;
-  const int64_t g1 = groups * (blockIdx.x + 1) / gridDim.x;
+  // rows split evenly over the CTAs (time ~ rows streamed), groups of ROWS from each start
+  const int64_t rbeg = a.rows * blockIdx.x / gridDim.x;
+  const int64_t rend = a.rows * (blockIdx.x + 1) / gridDim.x;
   const int64_t ncp = (a.ncols + 255) / 256 * 256;  // padded columns actually streamed
   const int64_t nchunks = (ncp + kChunk - 1) / kChunk;
   // fused: x = fma(xs, xa, xb) with xs = beta (K) or -delta (P)
@@ -145,13 +145,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
     if (lane == 0) {
       const uint64_t pol_a = a.evict_first ? l2_policy_evict_first() : l2_policy_evict_last();
       const uint64_t pol_x = l2_policy_evict_last();
-      int64_t it = 0;
-      for (int64_t g = g0; g < g1; ++g) {
-        const int64_t rb = g * ROWS;
-        const int nr = (int)imin64(ROWS, a.rows - rb);
-        for (int64_t c = 0; c < nchunks; ++c, ++it) {
-          const int slot = (int)(it % kStages);
-          if (it >= kStages) mbar_wait(&empty[slot], (uint32_t)(((it / kStages) - 1) & 1));
+      int slot = 0;
+      uint32_t ph = 0;
+      bool first = true;
+      for (int64_t rb = rbeg; rb < rend; rb += ROWS) {
+        const int nr = (int)imin64(ROWS, rend - rb);
+        for (int64_t c = 0; c < nchunks; ++c) {
+          if (!first) mbar_wait(&empty[slot], ph ^ 1u);
           const int64_t col0 = c * kChunk;
           const int width = (int)imin64(kChunk, ncp - col0);
           const uint32_t bytes = (uint32_t)width * 8u;
@@ -161,6 +161,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
           if (C::NX == 2) bulk_g2s(dst + (ROWS + 1) * kChunk, a.xb + col0, bytes, &full[slot], pol_x);
           for (int r = 0; r < nr; ++r)
             bulk_g2s(dst + r * kChunk, a.A + (rb + r) * a.ld + col0, bytes, &full[slot], pol_a);
+          if (++slot == kStages) {
+            slot = 0;
+            ph ^= 1u;
+            first = false;
+          }
         }
       }
     }
@@ -168,13 +173,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   }
 
   // ---------------- consumer warps
-  __shared__ double xrow[ROWS];  // x at the group's own row indices, captured from the ring
+  __shared__ double xrow_buf[2][ROWS];  // x at the group's own row indices, captured from the ring
+  __shared__ dd_pair spart[kWarps][2];
   dd_pair part = {0.0, 0.0}, part2 = {0.0, 0.0};
   const int cb = tid * kCPT;
-  int64_t it = 0;
-  for (int64_t g = g0; g < g1; ++g) {
-    const int64_t rb = g * ROWS;
-    const int nr = (int)imin64(ROWS, a.rows - rb);
+  int slot = 0, gpar = 0;
+  uint32_t ph = 0;
+  for (int64_t rb = rbeg; rb < rend; rb += ROWS, gpar ^= 1) {
+    const int nr = (int)imin64(ROWS, rend - rb);
+    double *xrow = xrow_buf[FUSE == FUSE_NONE ? gpar : 0];
     const int64_t own0 = a.row0 + rb;  // global index of the group's first row
     dd_pair acc[ROWS];
 #pragma unroll
@@ -184,9 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       pcur_i = a.pcur[own0 + lane];
       alpha_i = a.alpha[own0 + lane];
     }
-    for (int64_t c = 0; c < nchunks; ++c, ++it) {
-      const int slot = (int)(it % kStages);
-      mbar_wait(&full[slot], (uint32_t)((it / kStages) & 1));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      mbar_wait(&full[slot], ph);
       const int64_t col0 = c * kChunk;
       const int width = (int)imin64(kChunk, ncp - col0);
       if (cb < width) {
@@ -223,8 +229,77 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == kStages) {
+        slot = 0;
+        ph ^= 1u;
+      }
     }
-    // rows: warp butterfly, then the warp pairs in warp order
+    if constexpr (FUSE == FUSE_NONE) {
+      // rows: reduce-scatter inside the warp (row R ends in lane 4R: 9 pair adds per
+      // lane instead of 40), then warp R combines the 16 warps' pairs of row R by a
+      // fixed-shape shuffle tree; red / xrow double-buffered by group parity, so one
+      // CTA barrier per group
+      static_assert(ROWS == 8, "reduce-scatter layout assumes 8 rows");
+      dd_pair v4[4], v2[2], v1;
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const dd_pair snd = b4 ? acc[j] : acc[4 + j];
+        dd_pair rcv;
+        rcv.s = __shfl_xor_sync(0xffffffffu, snd.s, 16);
+        rcv.c = __shfl_xor_sync(0xffffffffu, snd.c, 16);
+        v4[j] = b4 ? acc[4 + j] : acc[j];
+        pair_add(v4[j], rcv);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const dd_pair snd = b3 ? v4[j] : v4[2 + j];
+        dd_pair rcv;
+        rcv.s = __shfl_xor_sync(0xffffffffu, snd.s, 8);
+        rcv.c = __shfl_xor_sync(0xffffffffu, snd.c, 8);
+        v2[j] = b3 ? v4[2 + j] : v4[j];
+        pair_add(v2[j], rcv);
+      }
+      {
+        const dd_pair snd = b2 ? v2[0] : v2[1];
+        dd_pair rcv;
+        rcv.s = __shfl_xor_sync(0xffffffffu, snd.s, 4);
+        rcv.c = __shfl_xor_sync(0xffffffffu, snd.c, 4);
+        v1 = b2 ? v2[1] : v2[0];
+        pair_add(v1, rcv);
+      }
+#pragma unroll
+      for (int off = 2; off > 0; off >>= 1) {
+        dd_pair rcv;
+        rcv.s = __shfl_xor_sync(0xffffffffu, v1.s, off);
+        rcv.c = __shfl_xor_sync(0xffffffffu, v1.c, off);
+        pair_add(v1, rcv);
+      }
+      dd_pair *rb_red = red + gpar * kWarps * ROWS;
+      if ((lane & 3) == 0) rb_red[warp * ROWS + (lane >> 2)] = v1;
+      named_bar_sync(1, kConsumers);
+      if (warp < nr) {
+        const int R = warp;
+        dd_pair t = lane < kWarps ? rb_red[lane * ROWS + R] : dd_pair{0.0, 0.0};
+#pragma unroll
+        for (int off = 1; off < kWarps; off <<= 1) {
+          dd_pair o;
+          o.s = __shfl_down_sync(0xffffffffu, t.s, off);
+          o.c = __shfl_down_sync(0xffffffffu, t.c, off);
+          if ((lane & (2 * off - 1)) == 0) pair_add(t, o);
+        }
+        if (lane == 0) {
+          const int64_t gi = a.row0 + rb + R;
+          const double xi = a.xd != nullptr ? a.xd[gi] : xrow[R];
+          if (a.lambda != 0.0) dot2_step(t, a.lambda, xi);  // the lambda x_i term of the row
+          const double yv = pair_value(t);
+          a.y[rb + R] = yv;
+          dot2_step(part, xi, yv);
+        }
+      }
+      continue;
+    }
+    // fused variants: warp butterfly, then the warp pairs in warp order
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       const dd_pair v = warp_reduce_pair(acc[r]);
@@ -253,8 +328,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   }
 
   // ---------------- CTA partials, then the last CTA reduces in CTA order
+  if (FUSE == FUSE_NONE) {  // row partials live in lane 0 of warps 0..7: gather them in warp order
+    if (lane == 0) spart[warp][0] = part;
+    named_bar_sync(1, kConsumers);
+    if (warp == 0) {
+      part = lane < kWarps ? spart[lane][0] : dd_pair{0.0, 0.0};
+#pragma unroll
+      for (int off = 1; off < kWarps; off <<= 1) {
+        dd_pair o;
+        o.s = __shfl_down_sync(0xffffffffu, part.s, off);
+        o.c = __shfl_down_sync(0xffffffffu, part.c, off);
+        if ((lane & (2 * off - 1)) == 0) pair_add(part, o);
+      }
+    }
+  }
   if (warp == 0) {
-    const dd_pair v = warp_reduce_pair(part);
+    const dd_pair v = FUSE == FUSE_NONE ? part : warp_reduce_pair(part);
     const dd_pair v2 = warp_reduce_pair(part2);
     if (lane == 0) {
       a.partials[2 * blockIdx.x] = v;

@@ -123,11 +123,6 @@ laker_status ensure_jacobi(laker_ctx ctx) {
 
 #define CHECK_CTX(ctx) \
   if (!(ctx)) return LAKER_ERR_INVALID_ARGUMENT
-#define LAKER_TRY(expr)                  \
-  do {                                   \
-    laker_status _s = (expr);            \
-    if (_s != LAKER_OK) return _s;       \
-  } while (0)
 
 }  // namespace
 
@@ -229,6 +224,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   free_dev(ctx, ctx->K);
   free_dev(ctx, ctx->P);
   free_dev(ctx, ctx->Pdiag);
+  laker::free_factors(ctx);
   cudaFree(ctx->counters);
   cudaFree(ctx->partials);
   cudaFree(ctx->flags);
@@ -251,6 +247,7 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   free_dev(ctx, ctx->K);
   free_dev(ctx, ctx->P);
   free_dev(ctx, ctx->Pdiag);
+  laker::free_factors(ctx);
   ctx->assembled = false;
   ctx->k_sym = ctx->p_sym = false;
   ctx->precond_kind = LAKER_PRECOND_NONE;
@@ -316,10 +313,12 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
   switch (opts->kind) {
     case LAKER_PRECOND_NONE:
       free_dev(ctx, ctx->P);
+      laker::free_factors(ctx);
       ctx->p_sym = false;
       ctx->precond_kind = LAKER_PRECOND_NONE;
       return LAKER_OK;
     case LAKER_PRECOND_JACOBI:
+      laker::free_factors(ctx);
       LAKER_TRY(ensure_jacobi(ctx));
       ctx->precond_kind = LAKER_PRECOND_JACOBI;
       LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -331,10 +330,12 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
         return set_err(ctx, LAKER_ERR_NOT_READY, "fit: detached shard (no NCCL communicator)");
       {
         ctx->p_sym = false;
+        if (opts->p_layout < LAKER_P_AUTO || opts->p_layout > LAKER_P_FACTORED)
+          return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: bad p_layout");
         laker_status st = laker::fit_learned(ctx, *opts, report);
         if (st != LAKER_OK) return st;
         LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        return laker::refresh_symmetry(ctx, 1);
+        return ctx->p_factored ? LAKER_OK : laker::refresh_symmetry(ctx, 1);
       }
     default:
       return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: unknown kind");
@@ -460,6 +461,9 @@ laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *dat
   if (!ctx->assembled) return set_err(ctx, LAKER_ERR_NOT_READY, "set_preconditioner: assemble first");
   cudaSetDevice(ctx->device);
   const int64_t rows = ctx->r1 - ctx->r0;
+  if (kind != LAKER_PRECOND_NONE && kind != LAKER_PRECOND_JACOBI && kind != LAKER_PRECOND_EXTERNAL_DENSE)
+    return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "set_preconditioner: kind must be NONE, JACOBI or EXTERNAL_DENSE");
+  laker::free_factors(ctx);
   if (kind == LAKER_PRECOND_NONE) {
     ctx->precond_kind = kind;
     return LAKER_OK;
@@ -494,12 +498,29 @@ laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *dat
 
 laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows) {
   CHECK_CTX(ctx);
-  if (!ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "no dense preconditioner");
+  if (!ctx->P && !ctx->p_factored) return set_err(ctx, LAKER_ERR_NOT_READY, "no dense preconditioner");
   if (!P_rows) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "NULL");
   cudaSetDevice(ctx->device);
+  LAKER_TRY(laker::ensure_dense_p(ctx));  // factored P: the rows are formed from the factors
   const int64_t rows = ctx->r1 - ctx->r0;
   LAKER_CUDA(ctx, cudaMemcpy2DAsync(P_rows, ctx->n * sizeof(double), ctx->P, ctx->ld * sizeof(double),
                                     ctx->n * sizeof(double), rows, cudaMemcpyDefault, ctx->stream));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return LAKER_OK;
+}
+
+laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *M, double *a_inv_sqrt) {
+  CHECK_CTX(ctx);
+  if (!ctx->p_factored) return set_err(ctx, LAKER_ERR_NOT_READY, "no factored preconditioner");
+  cudaSetDevice(ctx->device);
+  const int64_t n = ctx->n, nr = ctx->f_nr;
+  if (Q)
+    LAKER_CUDA(ctx, cudaMemcpy2DAsync(Q, nr * sizeof(double), ctx->Qr, ctx->f_ldq * sizeof(double),
+                                      nr * sizeof(double), n, cudaMemcpyDefault, ctx->stream));
+  if (M)
+    LAKER_CUDA(ctx, cudaMemcpy2DAsync(M, nr * sizeof(double), ctx->Mf, ctx->f_ldq * sizeof(double),
+                                      nr * sizeof(double), nr, cudaMemcpyDefault, ctx->stream));
+  if (a_inv_sqrt) *a_inv_sqrt = ctx->f_ainv;
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return LAKER_OK;
 }
@@ -535,6 +556,8 @@ laker_status laker_get_stats(laker_ctx ctx, laker_stats *out) {
   ctx->stats.mode = ctx->mode;
   ctx->stats.symmetric_k = ctx->k_sym ? 1 : 0;
   ctx->stats.symmetric_p = ctx->p_sym ? 1 : 0;
+  ctx->stats.p_factored = ctx->p_factored ? 1 : 0;
+  ctx->stats.n_dirs = (int32_t)ctx->f_nr;
   *out = ctx->stats;
   return LAKER_OK;
 }

@@ -78,6 +78,15 @@ struct laker_ctx_s {
   laker::SymvPlan *symv = nullptr;
   bool k_sym = false, p_sym = false;
 
+  // factored LEARNED P = f_ainv I + Q M Q^T (fit.cu; applied in pcg.cu)
+  bool p_factored = false;
+  double *Qt = nullptr;             // nrp x ld   (row k = q_k, zero padded)
+  double *Qr = nullptr;             // n x f_ldq  (row i = Q_i., zero padded)
+  double *Mf = nullptr;             // nrp x f_ldq
+  double *fz = nullptr, *fw = nullptr;  // f_ldq workspaces (z = Q^T r, w = M z), zero padded
+  int64_t f_nr = 0, f_nrp = 0, f_ldq = 0;
+  double f_ainv = 0.0;
+
   laker_stats stats{};
 };
 
@@ -86,6 +95,12 @@ namespace laker {
 // error helpers (api.cu)
 laker_status set_err(laker_ctx ctx, laker_status s, const std::string &msg);
 laker_status cuda_err(laker_ctx ctx, cudaError_t e, const char *what);
+
+#define LAKER_TRY(expr)            \
+  do {                             \
+    laker_status _s = (expr);      \
+    if (_s != LAKER_OK) return _s; \
+  } while (0)
 
 #define LAKER_CUDA(ctx, call)                                      \
   do {                                                             \
@@ -122,6 +137,9 @@ struct GemvArgs {
   double *alpha;          // P mode: alpha = fma(delta, pcur, alpha) on own rows
   const double *pcur;
   double *hist;           // P mode: residual history
+  // non-square applies (factored P): when set, the diagonal term lambda xd_i and the
+  // epilogue dot use xd (global row index row0 + i) instead of the streamed x
+  const double *xd;
 };
 void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
 void gemv_init();
@@ -211,6 +229,12 @@ void launch_transpose(const double *A, int64_t rows, int64_t cols, int64_t lda, 
 
 // ------------------------------------------------------------------- fit.cu
 laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_report *rep);
+// dense P rows [r0, r1) into ctx->P from the factors (nrp x ld Q^T, M with row stride ldm)
+laker_status form_dense_p(laker_ctx ctx, const double *Ut, const double *Mm, int64_t ldm, int64_t nrp,
+                          double ainv);
+// form (once) and cache the dense rows of a factored P (block / sharded solvers, hooks)
+laker_status ensure_dense_p(laker_ctx ctx);
+void free_factors(laker_ctx ctx);
 
 // ------------------------------------------------------------------- pcg.cu
 laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,

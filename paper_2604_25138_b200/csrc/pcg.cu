@@ -57,6 +57,26 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
 }
 
 static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgState *st, int epi, double *dot_out) {
+  if (ctx->p_factored) {
+    // theta = a^{-1/2} r + Q (M (Q^T r)): three Dot2 GEMV passes (NEXT-1); the last
+    // one carries the a^{-1/2} r_i term and the r.theta epilogue
+    const int64_t nrp = ctx->f_nrp, ldq = ctx->f_ldq;
+    GemvArgs z{};
+    z.A = ctx->Qt; z.ld = ctx->ld; z.rows = nrp; z.ncols = ctx->n; z.x = r; z.row0 = 0; z.y = ctx->fz;
+    z.state = st; z.partials = ctx->partials; z.counter = ctx->counters + kCtrGemv; z.epi = kEpiNone;
+    z.evict_first = true;
+    launch_gemv(z, ctx->gemv_grid, ctx->stream);
+    GemvArgs w = z;
+    w.A = ctx->Mf; w.ld = ldq; w.rows = nrp; w.ncols = nrp; w.x = ctx->fz; w.y = ctx->fw;
+    w.evict_first = false;  // 128 MiB at C3: may stay in L2 across iterations
+    launch_gemv(w, ctx->gemv_grid, ctx->stream);
+    GemvArgs t = z;
+    t.A = ctx->Qr; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fw; t.row0 = ctx->r0;
+    t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
+    launch_gemv(t, ctx->gemv_grid, ctx->stream);
+    ctx->stats.kernel_launches += 3;
+    return;
+  }
   GemvArgs a{};
   a.A = ctx->P;
   a.ld = ctx->ld;
@@ -99,7 +119,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   const int64_t n = ctx->n, ld = ctx->ld;
   const int pk = ctx->precond_kind;
   const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
-  if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  if (dense && !ctx->P && !ctx->p_factored) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
   if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
   const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
   cudaStream_t s = ctx->stream;
@@ -151,7 +171,8 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   // Measured on B200 (profiles/r01_*): the fused pair runs 0.367 + 0.371 ms vs 2 x 0.353 ms
   // unfused (the second staged vector chunk costs more than the removed small kernels),
   // so the unfused iteration stays the default; LAKER_FUSED=1 selects the fused one.
-  const bool fused = dense && ctx->storage == LAKER_STORE_MATERIALIZED && std::getenv("LAKER_FUSED") != nullptr;
+  const bool fused = dense && !ctx->p_factored && ctx->storage == LAKER_STORE_MATERIALIZED &&
+                     std::getenv("LAKER_FUSED") != nullptr;
   auto record_fused = [&](int j) {
     double *p_old = (j % 2 == 0) ? w.p : p2, *p_new = (j % 2 == 0) ? p2 : w.p;
     double *r_old = (j % 2 == 0) ? w.r : r2, *r_new = (j % 2 == 0) ? r2 : w.r;

@@ -22,12 +22,14 @@ constexpr int kBR = 32;   // rows of A per CTA
 constexpr int kBK = 32;   // k chunk
 constexpr int kBM = 64;   // RHS per CTA (columns)
 
-// Q[i][c] = RN(lambda X[row0+i][c] + sum_j A[i][j] X[j][c]), Dot2 per entry.
+// Q[i][c] = RN(lambda Xd[row0+i][c] + sum_j A[i][j] X[j][c]), Dot2 per entry (Xd = X
+// for the operator; Xd = R for the last pass of the factored P, Q (M (Q^T R)) + a^-1/2 R).
 __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict__ A, int64_t lda, int64_t rows,
                                                         int64_t kdim, const double *__restrict__ X, int64_t ldx,
                                                         int64_t m, double *__restrict__ Q, int64_t ldq,
                                                         double lambda, int64_t row0,
-                                                        const int32_t *__restrict__ all_done) {
+                                                        const int32_t *__restrict__ all_done,
+                                                        const double *__restrict__ Xd) {
   if (all_done && *(volatile const int32_t *)all_done) return;
   __shared__ double As[kBR][kBK + 1];
   __shared__ __align__(16) double Xs[kBK][kBM];
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         if (R0 + tr + a < rows && C0 + tc + b < m)
-          dot2_step(acc[a][b], lambda, X[(row0 + R0 + tr + a) * ldx + C0 + tc + b]);
+          dot2_step(acc[a][b], lambda, Xd[(row0 + R0 + tr + a) * ldx + C0 + tc + b]);
   }
   for (int64_t k0 = 0; k0 < kdim; k0 += kBK) {
     __syncthreads();
@@ -302,7 +304,8 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   const int64_t n = ctx->n, ld = ctx->ld;
   const int pk = ctx->precond_kind;
   const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
-  if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  const bool fac = dense && ctx->p_factored;
+  if (dense && !ctx->P && !fac) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
   if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
   const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
   const int64_t mp = (m + 1) / 2 * 2;  // even row stride for the DMMA epilogue
@@ -312,6 +315,12 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   LAKER_CUDA(ctx, cudaMallocAsync(&base, 5 * blk * sizeof(double), s));
   LAKER_CUDA(ctx, cudaMemsetAsync(base, 0, 5 * blk * sizeof(double), s));
   double *al = base, *rr = al + blk, *th = rr + blk, *pp = th + blk, *qq = pp + blk;
+  double *zb = nullptr, *wb = nullptr;  // factored P: Q^T R and M Q^T R (nrp x mp)
+  if (fac) {
+    LAKER_CUDA(ctx, cudaMallocAsync(&zb, 2 * (size_t)ctx->f_nrp * mp * sizeof(double), s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(zb, 0, 2 * (size_t)ctx->f_nrp * mp * sizeof(double), s));
+    wb = zb + (size_t)ctx->f_nrp * mp;
+  }
   PcgState *st = nullptr;
   double *hist = nullptr, *trel = nullptr;
   int32_t *all_done = nullptr;
@@ -342,17 +351,34 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     ctx->stats.kernel_launches++;
   };
   const bool exact = ctx->mode == LAKER_MODE_EXACT;
-  auto apply = [&](const double *Amat, double lam, const double *X, double *Out, bool gated = true) {
+  // Out (rows x m) = A (rows x kdim, lda) X + lam Xd
+  auto gemm = [&](const double *Amat, int64_t lda, int64_t rows, int64_t kdim, double lam, const double *X,
+                  const double *Xd, double *Out, bool gated) {
     if (exact) {
-      dim3 grid((unsigned)((n + kBR - 1) / kBR), (unsigned)((m + kBM - 1) / kBM));
-      gemm_dot2_kernel<<<grid, 256, 0, s>>>(Amat, ld, n, ld, X, mp, m, Out, mp, lam, 0, gated ? all_done : nullptr);
+      dim3 grid((unsigned)((rows + kBR - 1) / kBR), (unsigned)((m + kBM - 1) / kBM));
+      gemm_dot2_kernel<<<grid, 256, 0, s>>>(Amat, lda, rows, kdim, X, mp, m, Out, mp, lam, 0,
+                                            gated ? all_done : nullptr, Xd);
     } else {
       GemmArgs g{};
-      g.M = n; g.N = mp; g.K = ld; g.A = Amat; g.lda = ld; g.B = X; g.ldb = mp; g.C = Out; g.ldc = mp;
-      g.alpha = 1.0; g.beta = lam; g.Cin = X; g.ldcin = mp;
+      g.M = rows; g.N = mp; g.K = kdim; g.A = Amat; g.lda = lda; g.B = X; g.ldb = mp; g.C = Out; g.ldc = mp;
+      g.alpha = 1.0; g.beta = lam; g.Cin = Xd; g.ldcin = mp;
       launch_dgemm(g, true, s);
     }
     ctx->stats.kernel_launches++;
+  };
+  auto apply = [&](const double *Amat, double lam, const double *X, double *Out, bool gated = true) {
+    gemm(Amat, ld, n, ld, lam, X, X, Out, gated);
+  };
+  // theta = P R: dense rows, or the factored passes Z = Q^T R, W = M Z, Theta = Q W + a^-1/2 R
+  auto apply_p = [&](const double *R, double *Th) {
+    if (!fac) {
+      apply(ctx->P, 0.0, R, Th);
+      return;
+    }
+    const int64_t nrp = ctx->f_nrp, ldq = ctx->f_ldq;
+    gemm(ctx->Qt, ld, nrp, ld, 0.0, R, R, zb, true);
+    gemm(ctx->Mf, ldq, nrp, nrp, 0.0, zb, zb, wb, true);
+    gemm(ctx->Qr, ldq, n, nrp, ctx->f_ainv, wb, R, Th, true);
   };
   const int vg = 2 * ctx->num_sms;
   cudaEvent_t ev0, ev1;
@@ -361,7 +387,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   cudaEventRecord(ev0, s);
   col(kColInit);
   if (dense) {
-    apply(ctx->P, 0.0, rr, th);
+    apply_p(rr, th);
     col(kColBeta);  // initial rho = r.theta
     block_pupdate_kernel<<<vg, 256, 0, s>>>(n, m, mp, th, pp, st, 1, all_done);
     ctx->stats.kernel_launches++;
@@ -377,7 +403,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     col(kColDelta);
     col(kColUpdate);
     if (dense) {
-      apply(ctx->P, 0.0, rr, th);
+      apply_p(rr, th);
       col(kColBeta);
     }
     block_pupdate_kernel<<<vg, 256, 0, s>>>(n, m, mp, theta_src, pp, st, 0, all_done);
@@ -434,6 +460,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   cudaGraphExecDestroy(gexec);
   cudaGraphDestroy(graph);
   cudaFreeAsync(base, s);
+  if (zb) cudaFreeAsync(zb, s);
   cudaFreeAsync(st, s);
   cudaFreeAsync(hist, s);
   cudaFreeAsync(trel, s);

@@ -275,6 +275,7 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
   const int W = ctx->world;
   const int pk = ctx->precond_kind;
   const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
+  if (dense) LAKER_TRY(ensure_dense_p(ctx));  // a factored P is expanded once to its rows
   if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
   if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
   const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);

@@ -58,8 +58,8 @@ constexpr size_t kStageBytes = kTileBytes + 512;  // tile + x slice (keeps 512 B
 constexpr int kRedBufs = 3;
 constexpr size_t kRedBytes = kRedBufs * kConsWarps * kSC * sizeof(dd_pair);  // [3][16 warps][32 cols]
 constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 64 * sizeof(uint64_t);
-constexpr int kFinThreads = 256;
-constexpr int kFinSub = 8;               // threads per row in the finalize kernel
+constexpr int kFinThreads = 512;
+constexpr int kFinSub = 16;              // threads per row in the finalize kernel
 
 struct SymvArgs {
   int64_t n;
@@ -286,49 +286,57 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 
 // y_i = RN(sum of the partial pairs of row i in a fixed order + lambda x_i); Dot2 x.y
 // per CTA; the last CTA reduces the CTA pairs in CTA order and runs the epilogue.
+// kFinSub threads per row, each summing the partials I = sub (mod kFinSub) with all
+// its loads issued before the adds; rows grid-strided over a persistent grid.
+__device__ __forceinline__ dd_pair ldcg_pair(const dd_pair *p) {
+  return dd_pair{__ldcg(&p->s), __ldcg(&p->c)};
+}
+
 __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
+  constexpr int kRowsPerPass = kFinThreads / kFinSub;
+  constexpr int kMaxLd = 8;  // colpart loads batched per thread (nb <= kFinSub * kMaxLd handled per batch)
   __shared__ dd_pair sred[kFinThreads / 32];
   __shared__ int s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int sub = lane & (kFinSub - 1);
-  const int64_t i = ((int64_t)blockIdx.x * kFinThreads + tid) / kFinSub;
+  const int sub = tid & (kFinSub - 1);
   dd_pair dotp = {0.0, 0.0};
-  dd_pair v = {0.0, 0.0};
-  const bool valid = i < a.n;
-  const int J = valid ? (int)(i / kSR) : 0, r = valid ? (int)(i % kSR) : 0;
-  if (valid) {
-    // column partials of the tiles (I, .) above this row's diagonal block, I = sub (mod 8)
-    for (int I = sub; I < J; I += kFinSub) {
-      dd_pair o;
-      o.s = __ldcg(&a.colpart[(int64_t)I * a.ldcp + i].s);
-      o.c = __ldcg(&a.colpart[(int64_t)I * a.ldcp + i].c);
-      pair_add(v, o);
+  for (int64_t base = (int64_t)blockIdx.x * kRowsPerPass; base < a.n; base += (int64_t)gridDim.x * kRowsPerPass) {
+    const int64_t i = base + tid / kFinSub;
+    const bool valid = i < a.n;
+    const int J = valid ? (int)(i / kSR) : 0, r = valid ? (int)(i % kSR) : 0;
+    dd_pair v = {0.0, 0.0};
+    // column partials of the tiles (I, .) above this row's diagonal block, I = sub (mod kFinSub)
+    for (int I0 = sub; I0 < J; I0 += kFinSub * kMaxLd) {
+      dd_pair o[kMaxLd];
+#pragma unroll
+      for (int q = 0; q < kMaxLd; ++q) {
+        const int I = I0 + q * kFinSub;
+        o[q] = I < J ? ldcg_pair(&a.colpart[(int64_t)I * a.ldcp + i]) : dd_pair{0.0, 0.0};
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxLd; ++q) pair_add(v, o[q]);
     }
     // row partials of this block-row's segments
-    const int ns = a.nseg[J];
-    for (int q = sub; q < ns; q += kFinSub) {
-      const dd_pair *p = a.rowpart + ((int64_t)J * a.maxseg + q) * kSR + r;
-      dd_pair o;
-      o.s = __ldcg(&p->s);
-      o.c = __ldcg(&p->c);
-      pair_add(v, o);
+    if (valid) {
+      const int ns = a.nseg[J];
+      for (int q = sub; q < ns; q += kFinSub) pair_add(v, ldcg_pair(a.rowpart + ((int64_t)J * a.maxseg + q) * kSR + r));
     }
-  }
-  // combine the 8 sub-sums in sub order (lanes sub = 0..7 of this row); all lanes shuffle
+    // combine the kFinSub sub-sums in sub order; all lanes shuffle
 #pragma unroll
-  for (int off = 1; off < kFinSub; off <<= 1) {
-    dd_pair o;
-    o.s = __shfl_down_sync(0xffffffffu, v.s, off, kFinSub);
-    o.c = __shfl_down_sync(0xffffffffu, v.c, off, kFinSub);
-    if ((sub & (2 * off - 1)) == 0) pair_add(v, o);
-  }
-  if (valid && sub == 0) {
-    const double xi = a.x[i];
-    if (a.lambda != 0.0) dot2_step(v, a.lambda, xi);
-    const double yv = pair_value(v);
-    a.y[i] = yv;
-    dot2_step(dotp, xi, yv);
+    for (int off = 1; off < kFinSub; off <<= 1) {
+      dd_pair o;
+      o.s = __shfl_down_sync(0xffffffffu, v.s, off, kFinSub);
+      o.c = __shfl_down_sync(0xffffffffu, v.c, off, kFinSub);
+      if ((sub & (2 * off - 1)) == 0) pair_add(v, o);
+    }
+    if (valid && sub == 0) {
+      const double xi = a.x[i];
+      if (a.lambda != 0.0) dot2_step(v, a.lambda, xi);
+      const double yv = pair_value(v);
+      a.y[i] = yv;
+      dot2_step(dotp, xi, yv);
+    }
   }
   dotp = warp_reduce_pair(dotp);
   if (lane == 0) sred[warp] = dotp;
@@ -341,15 +349,24 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
     s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last || warp != 0) return;
+  if (!s_last) return;
+  // last CTA: one CTA pair per thread, then a fixed-shape block reduction
   __threadfence();
-  v = dd_pair{0.0, 0.0};
-  for (int b = lane; b < (int)gridDim.x; b += 32) {
-    dd_pair o = {__ldcg(&a.partials[b].s), __ldcg(&a.partials[b].c)};
-    pair_add(v, o);
+  dd_pair v = tid < (int)gridDim.x ? ldcg_pair(&a.partials[tid]) : dd_pair{0.0, 0.0};
+  for (int b = tid + kFinThreads; b < (int)gridDim.x; b += kFinThreads) pair_add(v, ldcg_pair(&a.partials[b]));
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    dd_pair o;
+    o.s = __shfl_down_sync(0xffffffffu, v.s, off);
+    o.c = __shfl_down_sync(0xffffffffu, v.c, off);
+    if ((lane & (2 * off - 1)) == 0) pair_add(v, o);
   }
-  v = warp_reduce_pair(v);
-  if (lane != 0) return;
+  __syncthreads();
+  if (lane == 0) sred[warp] = v;
+  __syncthreads();
+  if (tid != 0) return;
+  v = sred[0];
+  for (int w = 1; w < kFinThreads / 32; ++w) pair_add(v, sred[w]);
   *a.counter = 0u;
   PcgState *st = a.state;
   const double dv = pair_value(v);
@@ -473,8 +490,8 @@ cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
     p->maxseg = std::max(p->maxseg, (int)nseg[I]);
   }
   p->ldcp = (int64_t)p->nct * kSC;
-  const int64_t rows_fin = (int64_t)n * kFinSub;
-  p->fin_grid = (int)((rows_fin + kFinThreads - 1) / kFinThreads);
+  const int64_t passes = (n + kFinThreads / kFinSub - 1) / (kFinThreads / kFinSub);
+  p->fin_grid = (int)std::min<int64_t>(2 * num_sms, passes);
   cudaError_t e;
   if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&p->segfirst, segfirst.size() * sizeof(int32_t))) != cudaSuccess) return e;

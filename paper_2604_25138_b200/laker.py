@@ -29,12 +29,14 @@ STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "DIMENSION_MISMATCH", 3: "NOT_READY
 STORE_MATERIALIZED, STORE_ON_THE_FLY = 0, 1
 MODE_FAST, MODE_EXACT = 0, 1
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_LEARNED, PRECOND_EXTERNAL_DENSE = 0, 1, 2, 3
+P_AUTO, P_DENSE, P_FACTORED = 0, 1, 2
 TERM_RESIDUAL_TOL, TERM_MAX_ITERS, TERM_ZERO_RHS, TERM_BREAKDOWN, TERM_INDEFINITE = 0, 1, 2, 3, 4
 
 EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_status_string",
             "laker_last_error", "laker_assemble_kernel", "laker_fit_preconditioner", "laker_pcg_solve",
             "laker_predict", "laker_load_kernel_rows", "laker_get_kernel_rows", "laker_set_preconditioner",
-            "laker_get_preconditioner_rows", "laker_apply_operator", "laker_get_stats"]
+            "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_apply_operator",
+            "laker_get_stats"]
 
 
 class LakerError(RuntimeError):
@@ -47,7 +49,7 @@ class FitOpts(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("n_dirs", ctypes.c_int32), ("gamma", ctypes.c_double),
                 ("eps", ctypes.c_double), ("rho", ctypes.c_double), ("rho_floor", ctypes.c_double),
                 ("max_iters", ctypes.c_int32), ("fp_tol", ctypes.c_double), ("Z", ctypes.c_void_p),
-                ("seed", ctypes.c_uint64)]
+                ("seed", ctypes.c_uint64), ("p_layout", ctypes.c_int32)]
 
 
 class FitReport(ctypes.Structure):
@@ -75,7 +77,8 @@ class Stats(ctypes.Structure):
                 ("assemble_ms", ctypes.c_double), ("fit_ms", ctypes.c_double),
                 ("solve_ms", ctypes.c_double), ("predict_ms", ctypes.c_double),
                 ("kernel_launches", ctypes.c_int64),
-                ("symmetric_k", ctypes.c_int32), ("symmetric_p", ctypes.c_int32)]
+                ("symmetric_k", ctypes.c_int32), ("symmetric_p", ctypes.c_int32),
+                ("p_factored", ctypes.c_int32), ("n_dirs", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -96,6 +99,7 @@ def _load() -> ctypes.CDLL:
         "laker_get_kernel_rows": [vp, vp],
         "laker_set_preconditioner": [vp, st, vp],
         "laker_get_preconditioner_rows": [vp, vp],
+        "laker_get_preconditioner_factors": [vp, vp, vp, vp],
         "laker_apply_operator": [vp, vp, vp],
         "laker_get_stats": [vp, ctypes.POINTER(Stats)],
     }
@@ -177,8 +181,8 @@ def laker_assemble_kernel(ctx, E, scale: float, lam: float, storage: int = STORE
 
 def laker_fit_preconditioner(ctx, kind: int, n_dirs: int = 0, gamma: float = 0.1, eps: float = 1e-12,
                              rho: float = -1.0, rho_floor: float = 1e-3, max_iters: int = 200,
-                             fp_tol: float = 1e-8, Z=None, seed: int = 0) -> dict:
-    o = FitOpts(kind, n_dirs, gamma, eps, rho, rho_floor, max_iters, fp_tol, _ptr(Z), seed)
+                             fp_tol: float = 1e-8, Z=None, seed: int = 0, p_layout: int = P_AUTO) -> dict:
+    o = FitOpts(kind, n_dirs, gamma, eps, rho, rho_floor, max_iters, fp_tol, _ptr(Z), seed, p_layout)
     r = FitReport()
     _check(ctx, lib.laker_fit_preconditioner(ctx, ctypes.byref(o), ctypes.byref(r)))
     return {f: getattr(r, f) for f, _ in FitReport._fields_}
@@ -214,6 +218,10 @@ def laker_set_preconditioner(ctx, kind: int, data=None):
 
 def laker_get_preconditioner_rows(ctx, P_rows):
     _check(ctx, lib.laker_get_preconditioner_rows(ctx, _ptr(P_rows)))
+
+
+def laker_get_preconditioner_factors(ctx, Q, M, a_inv_sqrt) -> None:
+    _check(ctx, lib.laker_get_preconditioner_factors(ctx, _ptr(Q), _ptr(M), _ptr(a_inv_sqrt)))
 
 
 def laker_apply_operator(ctx, x, y):
@@ -306,6 +314,13 @@ class Context:
         P = np.empty((self.local_rows, self.n))
         laker_get_preconditioner_rows(self.h, P)
         return P
+
+    def get_preconditioner_factors(self):
+        """(Q n x N_r, M N_r x N_r, a^{-1/2}) of a factored LEARNED P."""
+        nr = self.stats()["n_dirs"]
+        Q, M, ai = np.empty((self.n, nr)), np.empty((nr, nr)), np.zeros(1)
+        laker_get_preconditioner_factors(self.h, Q, M, ai)
+        return Q, M, float(ai[0])
 
     def apply_operator(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64) if isinstance(x, np.ndarray) else x

@@ -32,7 +32,8 @@ def test_collective_path_equals_single(L, cid, n, kind):
             c.set_preconditioner(L.PRECOND_JACOBI)
         elif kind == "learned":
             Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
-            c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+            # dense rows on both sides (AUTO picks the factored P on the single-GPU path)
+            c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_DENSE)
         a, reps, hist = c.pcg_solve(P.y, P.tol, want_history=True)
         q = c.apply_operator(a)
         res.append((a, reps[0], hist, q))
@@ -56,7 +57,7 @@ def test_fused_iteration_equals_unfused(L):
     c = L.Context(0)
     c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(2, P.n, P.n_dirs))
-    c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_DENSE)  # fused needs dense P
     a0, r0, h0 = c.pcg_solve(P.y, P.tol, want_history=True)
     os.environ["LAKER_FUSED"] = "1"
     try:

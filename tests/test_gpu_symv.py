@@ -104,14 +104,14 @@ def test_symv_not_used_for_nonsymmetric(ctx, L):
 
 
 def test_symv_pcg_learned_gpu_fit(ctx, L):
-    """GPU-fitted P is bitwise symmetric -> both applies use symv; the staged
+    """GPU-fitted dense P is bitwise symmetric -> both applies use symv; the staged
     PCG (same K, the GPU's own P) equals the oracle's PCG bitwise."""
     P = make_problem(2)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(2, P.n, P.n_dirs))
-    ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_DENSE)
     st = ctx.stats()
-    assert st["symmetric_k"] == 1 and st["symmetric_p"] == 1
+    assert st["symmetric_k"] == 1 and st["symmetric_p"] == 1 and st["p_factored"] == 0
     Pm = ctx.get_preconditioner_rows()
     K, _ = O.assemble(P.E, P.scale)
     ag, reps, hist = ctx.pcg_solve(P.y, P.tol, want_history=True)
