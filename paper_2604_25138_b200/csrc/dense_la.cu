@@ -12,35 +12,45 @@ namespace {
 constexpr int NB = 64;
 
 // Factor the 64 x 64 diagonal block at (j0, j0); zero its strict upper part.
+// Right-looking in shared memory, 256 threads as a 16 x 16 grid: step j divides
+// column j by the pivot sqrt(A_jj) (taken by every thread itself), then thread
+// (ty, tx) applies A_ik -= L_ij L_kj to rows i = j+1+ty+16a, columns
+// k = j+1+tx+16b with k <= i -- the textbook operations, two barriers per step.
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double *A, int64_t lda, int64_t j0, int *flag) {
   __shared__ double S[NB][NB + 1];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+#pragma unroll 4
   for (int e = tid; e < NB * NB; e += 256) {
     const int r = e / NB, c = e % NB;
     S[r][c] = A[(j0 + r) * lda + j0 + c];
   }
   __syncthreads();
   for (int j = 0; j < NB; ++j) {
-    if (tid == 0) {
-      const double d = S[j][j];
-      if (!(d > 0.0)) {
-        atomicExch(flag, 1);
-        S[j][j] = 1.0;
-      } else {
-        S[j][j] = __dsqrt_rn(d);
+    double d = S[j][j];
+    if (!(d > 0.0)) {
+      if (tid == 0) atomicExch(flag, 1);
+      d = 1.0;
+    }
+    const double piv = __dsqrt_rn(d);
+    // column j below the diagonal (rows j+1+tid), the pivot itself by thread 63
+    if (tid < NB - 1 - j) S[j + 1 + tid][j] = __ddiv_rn(S[j + 1 + tid][j], piv);
+    __syncthreads();
+    if (tid == NB - 1) S[j][j] = piv;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = j + 1 + ty + 16 * a;
+      if (i < NB) {
+        const double lij = S[i][j];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int k = j + 1 + tx + 16 * b;
+          if (k <= i) S[i][k] = __fma_rn(-lij, S[k][j], S[i][k]);
+        }
       }
     }
     __syncthreads();
-    const double piv = S[j][j];
-    for (int i = j + 1 + tid; i < NB; i += 256) S[i][j] = __ddiv_rn(S[i][j], piv);
-    __syncthreads();
-    const int m = NB - j - 1;
-    for (int e = tid; e < m * m; e += 256) {
-      const int i = j + 1 + e / m, k = j + 1 + e % m;
-      if (k <= i) S[i][k] = __fma_rn(-S[i][j], S[k][j], S[i][k]);
-    }
-    __syncthreads();
   }
+#pragma unroll 4
   for (int e = tid; e < NB * NB; e += 256) {
     const int r = e / NB, c = e % NB;
     A[(j0 + r) * lda + j0 + c] = c <= r ? S[r][c] : 0.0;
@@ -48,26 +58,31 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *A, int64_t lda,
 }
 
 // Rows [r0, r0 + nrows) of column block j0: X = A L^{-T}, L = A[j0.., j0..] (factored).
-// One CTA = 64 rows, one thread per row (the row held in registers).
-__global__ void __launch_bounds__(64) potrf_panel_kernel(double *A, int64_t lda, int64_t j0, int64_t r0,
-                                                         int64_t nrows) {
+// One thread per row (the row held in registers), right-looking substitution:
+// x_c = a_c / L_cc, then a_k -= x_c L_kc for k > c -- per entry the same fma
+// sequence as the dot-product form, with 64 independent chains of ILP.
+constexpr int kPanelThreads = 32;
+__global__ void __launch_bounds__(kPanelThreads) potrf_panel_kernel(double *A, int64_t lda, int64_t j0, int64_t r0,
+                                                                    int64_t nrows) {
   __shared__ double Ls[NB][NB + 1];
   const int tid = threadIdx.x;
-  for (int e = tid; e < NB * NB; e += 64) {
+#pragma unroll 16
+  for (int e = tid; e < NB * NB; e += kPanelThreads) {
     const int r = e / NB, c = e % NB;
     Ls[r][c] = A[(j0 + r) * lda + j0 + c];
   }
   __syncthreads();
-  const int64_t row = r0 + (int64_t)blockIdx.x * NB + tid;
+  const int64_t row = r0 + (int64_t)blockIdx.x * kPanelThreads + tid;
   if (row >= r0 + nrows) return;
   double *a = A + row * lda + j0;
   double x[NB];
 #pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    double s = a[c];
+  for (int c = 0; c < NB; ++c) x[c] = a[c];
 #pragma unroll
-    for (int k = 0; k < c; ++k) s = __fma_rn(-x[k], Ls[c][k], s);
-    x[c] = __ddiv_rn(s, Ls[c][c]);
+  for (int c = 0; c < NB; ++c) {
+    x[c] = __ddiv_rn(x[c], Ls[c][c]);
+#pragma unroll
+    for (int k = c + 1; k < NB; ++k) x[k] = __fma_rn(-x[c], Ls[k][c], x[k]);
   }
 #pragma unroll
   for (int c = 0; c < NB; ++c) a[c] = x[c];
@@ -79,11 +94,15 @@ __global__ void zero_upper_kernel(double *A, int64_t lda, int64_t n) {
     A[r * lda + c] = 0.0;
 }
 
-// X[b] = L[b,b]^{-1} B[b] for one 64-row block; one thread per column, solution in registers.
-__global__ void __launch_bounds__(128) trsm_diag_kernel(const double *L, int64_t ldl, int64_t b0, double *B,
-                                                        int64_t ldb, int64_t ncols) {
+// X[b] = L[b,b]^{-1} B[b] for one 64-row block; one thread per column, solution
+// in registers, right-looking (x_r = b_r / L_rr, then b_k -= L_kr x_r for k > r):
+// per entry the same fma sequence as the dot-product form, 64 chains of ILP.
+constexpr int kTrsmThreads = 32;
+__global__ void __launch_bounds__(kTrsmThreads) trsm_diag_kernel(const double *L, int64_t ldl, int64_t b0, double *B,
+                                                                 int64_t ldb, int64_t ncols) {
   __shared__ double Ls[NB][NB + 1];
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+#pragma unroll 16
+  for (int e = threadIdx.x; e < NB * NB; e += kTrsmThreads) {
     const int r = e / NB, c = e % NB;
     Ls[r][c] = L[(b0 + r) * ldl + b0 + c];
   }
@@ -92,11 +111,12 @@ __global__ void __launch_bounds__(128) trsm_diag_kernel(const double *L, int64_t
   if (j >= ncols) return;
   double x[NB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) {
-    double s = B[(b0 + r) * ldb + j];
+  for (int r = 0; r < NB; ++r) x[r] = B[(b0 + r) * ldb + j];
 #pragma unroll
-    for (int k = 0; k < r; ++k) s = __fma_rn(-Ls[r][k], x[k], s);
-    x[r] = __ddiv_rn(s, Ls[r][r]);
+  for (int r = 0; r < NB; ++r) {
+    x[r] = __ddiv_rn(x[r], Ls[r][r]);
+#pragma unroll
+    for (int k = r + 1; k < NB; ++k) x[k] = __fma_rn(-Ls[k][r], x[r], x[k]);
   }
 #pragma unroll
   for (int r = 0; r < NB; ++r) B[(b0 + r) * ldb + j] = x[r];
@@ -125,7 +145,8 @@ void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s
     ++*launches;
     const int64_t rest = n - j0 - NB;
     if (rest <= 0) break;
-    potrf_panel_kernel<<<(unsigned)((rest + NB - 1) / NB), 64, 0, s>>>(A, lda, j0, j0 + NB, rest);
+    potrf_panel_kernel<<<(unsigned)((rest + kPanelThreads - 1) / kPanelThreads), kPanelThreads, 0, s>>>(A, lda, j0,
+                                                                                                      j0 + NB, rest);
     ++*launches;
     GemmArgs g{};
     g.M = rest;
@@ -152,7 +173,8 @@ void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s
 void trsm_lower_left(const double *L, int64_t ldl, int64_t n, double *B, int64_t ldb, int64_t ncols,
                      cudaStream_t s, int64_t *launches) {
   for (int64_t b0 = 0; b0 < n; b0 += NB) {
-    trsm_diag_kernel<<<(unsigned)((ncols + 127) / 128), 128, 0, s>>>(L, ldl, b0, B, ldb, ncols);
+    trsm_diag_kernel<<<(unsigned)((ncols + kTrsmThreads - 1) / kTrsmThreads), kTrsmThreads, 0, s>>>(L, ldl, b0, B, ldb,
+                                                                                                    ncols);
     ++*launches;
     const int64_t rest = n - b0 - NB;
     if (rest <= 0) break;

@@ -365,6 +365,7 @@ void free_factors(laker_ctx ctx) {
   ctx->Qt = ctx->Qr = ctx->Mf = ctx->fz = ctx->fw = nullptr;
   ctx->p_factored = false;
   ctx->f_nr = ctx->f_nrp = ctx->f_ldq = 0;
+  ctx->f_alloc_nrp = ctx->f_alloc_n = 0;
 }
 
 // P = a^{-1/2} I + Q M Q^T, rows [r0, r1) into ctx->P.  P_ij = W_i . Q_j for i >= j
@@ -747,18 +748,25 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   const double ainv = 1.0 / std::sqrt(a);
   const bool factored = o.p_layout == LAKER_P_FACTORED ||
                         (o.p_layout == LAKER_P_AUTO && ctx->world == 1 && !ctx->comm);
-  free_factors(ctx);
+  ctx->p_factored = false;
   if (factored) {
-    // keep the factors: Q^T for z = Q^T r, Q for Q w, and M
+    // keep the factors: Q^T for z = Q^T r, Q for Q w, and M;
+    // buffers of the same size are reused across fits (cudaFree/cudaMalloc of ~1 GiB
+    // cost ~0.1 s per refit)
     if (ctx->P) {
       cudaFree(ctx->P);
       ctx->P = nullptr;
     }
     const int64_t ldq = (nrp + 255) / 256 * 256;  // gemv streams whole 256-column chunks
-    LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ld * 8));
-    LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)n * ldq * 8));
-    LAKER_CUDA(ctx, cudaMalloc(&ctx->Mf, (size_t)nrp * ldq * 8));
-    LAKER_CUDA(ctx, cudaMalloc(&ctx->fz, (size_t)2 * ldq * 8));
+    if (!(ctx->Qt && ctx->f_alloc_nrp == nrp && ctx->f_alloc_n == n)) {
+      free_factors(ctx);
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ld * 8));
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)n * ldq * 8));
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->Mf, (size_t)nrp * ldq * 8));
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->fz, (size_t)2 * ldq * 8));
+      ctx->f_alloc_nrp = nrp;
+      ctx->f_alloc_n = n;
+    }
     ctx->fw = ctx->fz + ldq;
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Qr, 0, (size_t)n * ldq * 8, s));
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Mf, 0, (size_t)nrp * ldq * 8, s));
@@ -773,6 +781,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     ctx->f_ainv = ainv;
     ctx->p_factored = true;
   } else {
+    free_factors(ctx);
     LAKER_TRY(form_dense_p(ctx, Ut, Zm, nrp, nrp, ainv));
     dbg("P0", ctx->P, ctx->r1 - ctx->r0, n, ld);
   }

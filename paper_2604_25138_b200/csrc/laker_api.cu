@@ -243,11 +243,24 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
       (mode != LAKER_MODE_FAST && mode != LAKER_MODE_EXACT))
     return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "assemble: need n>=1, d>=1, lambda>0, n % world == 0, valid enums");
   cudaSetDevice(ctx->device);
-  free_dev(ctx, ctx->E);
-  free_dev(ctx, ctx->K);
+  // E and K buffers of the same size are kept (a refit/re-solve loop re-assembles
+  // every step; cudaFree + cudaMalloc of 2 GiB costs ~10 ms); the factored-P
+  // buffers are kept too (invalidated here, refilled by the next fit)
+  const int64_t rows_new = n / ctx->world;
+  const size_t e_bytes = (size_t)n * d * sizeof(double);
+  const size_t k_bytes = storage == LAKER_STORE_MATERIALIZED ? (size_t)rows_new * laker::padded_ld(n) * sizeof(double) : 0;
+  if (ctx->E_bytes != e_bytes) {
+    free_dev(ctx, ctx->E);
+    ctx->E_bytes = 0;
+  }
+  if (ctx->K_bytes != k_bytes) {
+    free_dev(ctx, ctx->K);
+    ctx->K_bytes = 0;
+  }
   free_dev(ctx, ctx->P);
   free_dev(ctx, ctx->Pdiag);
-  laker::free_factors(ctx);
+  if (ctx->f_alloc_n != n) laker::free_factors(ctx);
+  ctx->p_factored = false;
   ctx->assembled = false;
   ctx->k_sym = ctx->p_sym = false;
   ctx->precond_kind = LAKER_PRECOND_NONE;
@@ -262,7 +275,10 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   ctx->r1 = ctx->r0 + n / ctx->world;
   const int64_t rows = ctx->r1 - ctx->r0;
   cudaStream_t s = ctx->stream;
-  LAKER_CUDA(ctx, cudaMalloc(&ctx->E, (size_t)n * d * sizeof(double)));
+  if (!ctx->E) {
+    LAKER_CUDA(ctx, cudaMalloc(&ctx->E, e_bytes));
+    ctx->E_bytes = e_bytes;
+  }
   if (is_device_ptr(E))
     LAKER_CUDA(ctx, cudaMemcpyAsync(ctx->E, E, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToDevice, s));
   else
@@ -273,7 +289,10 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
   if (storage == LAKER_STORE_MATERIALIZED) {
-    LAKER_CUDA(ctx, cudaMalloc(&ctx->K, (size_t)rows * ctx->ld * sizeof(double)));
+    if (!ctx->K) {
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->K, k_bytes));
+      ctx->K_bytes = k_bytes;
+    }
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->K, 0, (size_t)rows * ctx->ld * sizeof(double), s));
     const bool whole = (rows == n);
     if (mode == LAKER_MODE_EXACT) {

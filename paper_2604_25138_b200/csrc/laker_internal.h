@@ -85,6 +85,8 @@ struct laker_ctx_s {
   double *Mf = nullptr;             // nrp x f_ldq
   double *fz = nullptr, *fw = nullptr;  // f_ldq workspaces (z = Q^T r, w = M z), zero padded
   int64_t f_nr = 0, f_nrp = 0, f_ldq = 0;
+  int64_t f_alloc_nrp = 0, f_alloc_n = 0;  // sizes the factor buffers were allocated for (reused)
+  size_t E_bytes = 0, K_bytes = 0;         // allocations kept across assemble calls of the same size
   double f_ainv = 0.0;
 
   laker_stats stats{};

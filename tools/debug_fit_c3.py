@@ -1,10 +1,14 @@
+"""C3 fit with per-phase device timings (LAKER_DEBUG_FIT=1 prints them)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["LAKER_DEBUG_FIT"] = "1"
+os.environ.setdefault("LAKER_DEBUG_FIT", "1")
 from paper_2604_25138_b200 import laker as L
 from synth import make_problem
-P = make_problem(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
+
+P = make_problem(3)
 c = L.Context(0)
-c.assemble_kernel(P.E, P.scale, P.lam)
+c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
 for _ in range(2):
-    print(c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7), file=sys.stderr)
+    rep = c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7)
+    print(rep, c.stats()["fit_ms"], flush=True)
+c.close()
