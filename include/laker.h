@@ -202,6 +202,11 @@ laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *
 /* y = (lambda I + K) x, x and y length n (y complete on every rank). */
 laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y);
 
+/* Diagnostic: C (M x N int32, row-major) = A (M x K int8) B (N x K int8)^T on the
+   tcgen05 int8 tensor cores (csrc/igemm.cu), all DEVICE pointers, K % 16 == 0,
+   synchronous.  The building block of the fp64 emulation (Ozaki scheme). */
+laker_status laker_debug_igemm_s8(const int8_t *A, const int8_t *B, int32_t *C, int64_t M, int64_t N, int64_t K);
+
 typedef struct {
   int64_t n, local_rows, ld;     /* problem size, rows held, padded row stride (doubles) */
   int32_t rank, world, precond_kind, storage, mode;

@@ -36,7 +36,7 @@ EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_statu
             "laker_last_error", "laker_assemble_kernel", "laker_fit_preconditioner", "laker_pcg_solve",
             "laker_predict", "laker_load_kernel_rows", "laker_get_kernel_rows", "laker_set_preconditioner",
             "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_apply_operator",
-            "laker_get_stats"]
+            "laker_get_stats", "laker_debug_igemm_s8"]
 
 
 class LakerError(RuntimeError):
@@ -102,6 +102,7 @@ def _load() -> ctypes.CDLL:
         "laker_get_preconditioner_factors": [vp, vp, vp, vp],
         "laker_apply_operator": [vp, vp, vp],
         "laker_get_stats": [vp, ctypes.POINTER(Stats)],
+        "laker_debug_igemm_s8": [vp, vp, vp, i64, i64, i64],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -232,6 +233,15 @@ def laker_get_stats(ctx) -> dict:
     s = Stats()
     _check(ctx, lib.laker_get_stats(ctx, ctypes.byref(s)))
     return {f: getattr(s, f) for f, _ in Stats._fields_}
+
+
+def laker_debug_igemm_s8(A, B, C) -> None:
+    """C = A B^T on the tcgen05 int8 tensor cores; torch int8 / int32 CUDA tensors."""
+    M, K = A.shape
+    N = B.shape[0]
+    s = lib.laker_debug_igemm_s8(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K)
+    if s != LAKER_OK:
+        raise LakerError(s, "laker_debug_igemm_s8")
 
 
 # ------------------------------------------------------------ convenience
