@@ -207,6 +207,12 @@ laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y);
    synchronous.  The building block of the fp64 emulation (Ozaki scheme). */
 laker_status laker_debug_igemm_s8(const int8_t *A, const int8_t *B, int32_t *C, int64_t M, int64_t N, int64_t K);
 
+/* Diagnostic: C (M x N) = A (M x K) B (N x K)^T in fp64 emulated on the int8
+   tensor cores (Ozaki scheme, csrc/ozaki.cu; `slices` int8 digit slices per
+   input, 0 = default 8), fp64 row-major DEVICE pointers, synchronous. */
+laker_status laker_debug_ozaki_gemm(const double *A, const double *B, double *C, int64_t M, int64_t N, int64_t K,
+                                    int32_t slices);
+
 typedef struct {
   int64_t n, local_rows, ld;     /* problem size, rows held, padded row stride (doubles) */
   int32_t rank, world, precond_kind, storage, mode;

@@ -26,8 +26,13 @@ constexpr size_t kIgemmSmem = 1024 + kIStages * (kABytes + kBBytes) + 256;
 constexpr int kIThreads = 6 * 32;
 
 __global__ void __launch_bounds__(kIThreads, 1)
-    igemm_s8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int32_t *C,
-                    int64_t ldc, int64_t M, int64_t N, int64_t K) {
+    igemm_s8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const IgemmEpi e, int64_t K) {
+  const int64_t M = e.M, N = e.N;
+  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
+  // tiles with no kept entry of a triangular product are skipped entirely
+  if (e.tri == 1 && m0 + kBM - 1 + e.tri_off < n0) return;
+  if (e.tri == 2 && m0 + e.tri_off >= n0 + kBN - 1) return;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms (TMA destination and UMMA descriptors)
   const uint32_t base_s = smem_u32(smem_raw);
@@ -40,7 +45,6 @@ __global__ void __launch_bounds__(kIThreads, 1)
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
   const int nk = (int)((K + kBK - 1) / kBK);
 
   if (warp == 0 && lane == 0) {
@@ -89,16 +93,43 @@ __global__ void __launch_bounds__(kIThreads, 1)
     const int64_t row = m0 + q * 32 + lane;
     mbar_wait(tfull, 0);
     tc::fence_after();
+    const int ea = (e.mode != kIgemmStoreS32 && row < M) ? e.ea[row] : 0;
 #pragma unroll 1
     for (int c = 0; c < kBN; c += 32) {
+      if (n0 + c >= N) break;
       uint32_t v[32];
       tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
       tc::tmem_ld_wait();
-      if (row < M) {
-        int32_t *dst = C + row * ldc + n0 + c;
+      if (row >= M) continue;
+      if (e.mode == kIgemmStoreS32) {
+        int32_t *dst = e.Ci + row * e.ldci + n0 + c;
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (n0 + c + j < N) dst[j] = (int32_t)v[j];
+        continue;
+      }
+      // x = v 2^(shift + ea_row + eb_col): exact (|v| < 2^31, power-of-two scale)
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const int64_t col = n0 + c + j;
+        if (col >= N) break;
+        const double x = scalbn((double)(int32_t)v[j], e.shift + ea + e.eb[col]);
+        double *w = e.W + row * e.ldw + col;
+        if (e.mode == kIgemmAccInit) {
+          *w = x;
+        } else if (e.mode == kIgemmAccAdd) {
+          *w = __dadd_rn(*w, x);
+        } else {  // final: C = alpha (W + x) + beta Cin + diag
+          if (e.tri != 0) {
+            const int64_t gr = row + e.tri_off;
+            if (e.tri == 1 ? gr < col : gr >= col) continue;
+          }
+          const double tot = e.has_w ? __dadd_rn(*w, x) : x;
+          double out = __dmul_rn(e.alpha, tot);
+          if (e.beta != 0.0) out = __dadd_rn(out, __dmul_rn(e.beta, e.Cin[row * e.ldcin + col]));
+          if (e.diag != 0.0 && row - col == e.diag_offset) out = __dadd_rn(out, e.diag);
+          e.C[row * e.ldc + col] = out;
+        }
       }
     }
   }
@@ -149,8 +180,23 @@ cudaError_t launch_igemm_s8(const int8_t *A, int64_t lda, const int8_t *B, int64
                             int64_t M, int64_t N, int64_t K, cudaStream_t s) {
   CUtensorMap ta, tb;
   if (!make_tmap_s8(&ta, A, M, K, lda, kBM) || !make_tmap_s8(&tb, B, N, K, ldb, kBN)) return cudaErrorInvalidValue;
+  IgemmEpi e{};
+  e.mode = kIgemmStoreS32;
+  e.Ci = C;
+  e.ldci = ldc;
+  e.M = M;
+  e.N = N;
   dim3 grid((unsigned)((N + kBN - 1) / kBN), (unsigned)((M + kBM - 1) / kBM));
-  igemm_s8_kernel<<<grid, kIThreads, kIgemmSmem, s>>>(ta, tb, C, ldc, M, N, K);
+  igemm_s8_kernel<<<grid, kIThreads, kIgemmSmem, s>>>(ta, tb, e, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_igemm_epi(const int8_t *A, int64_t lda, const int8_t *B, int64_t ldb, int64_t K,
+                             const IgemmEpi &e, cudaStream_t s) {
+  CUtensorMap ta, tb;
+  if (!make_tmap_s8(&ta, A, e.M, K, lda, kBM) || !make_tmap_s8(&tb, B, e.N, K, ldb, kBN)) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((e.N + kBN - 1) / kBN), (unsigned)((e.M + kBM - 1) / kBM));
+  igemm_s8_kernel<<<grid, kIThreads, kIgemmSmem, s>>>(ta, tb, e, K);
   return cudaGetLastError();
 }
 

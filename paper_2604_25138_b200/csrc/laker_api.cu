@@ -184,10 +184,20 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
     c->owns_stream = true;
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    // keep freed stream-ordered allocations in the pool (the fit and the Ozaki GEMMs
+    // allocate GiB-sized scratch per call; returning it to the OS at every sync is slow)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   c->gemv_grid = laker::gemv_max_grid(c->num_sms);
   laker::gemv_init();
   laker::symv_init();
   laker::dgemm_init();
+  laker::igemm_init();
   laker::otf_fast_init();
   const size_t npart = 4096;
   if (cudaMalloc(&c->counters, laker::kNumCtr * sizeof(unsigned int)) != cudaSuccess ||

@@ -219,6 +219,42 @@ void launch_mirror_lower(double *A, int64_t lda, int64_t n, cudaStream_t s);
 void dgemm_init();
 void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s);
 
+// ---------------------------------------------------------------- igemm.cu
+// int8 tensor-core GEMM (tcgen05 kind::i8) with an Ozaki epilogue:
+// x = v 2^(shift + ea[row] + eb[col]) then W = x | W += x | C = alpha (W + x) + beta Cin + diag
+enum { kIgemmStoreS32 = 0, kIgemmAccInit = 1, kIgemmAccAdd = 2, kIgemmFinal = 3 };
+struct IgemmEpi {
+  int mode;
+  int64_t M, N;
+  int32_t *Ci;
+  int64_t ldci;
+  double *W;
+  int64_t ldw;
+  bool has_w;
+  const int32_t *ea, *eb;
+  int shift;
+  double *C;
+  int64_t ldc;
+  const double *Cin;
+  int64_t ldcin;
+  double alpha, beta, diag;
+  int64_t diag_offset;
+  int tri;
+  int64_t tri_off;
+};
+void igemm_init();
+cudaError_t launch_igemm_epi(const int8_t *A, int64_t lda, const int8_t *B, int64_t ldb, int64_t K,
+                             const IgemmEpi &e, cudaStream_t s);
+
+// ---------------------------------------------------------------- ozaki.cu
+// C = alpha A op(B) + beta Cin + diag (GemmArgs semantics, tri honoured; lower_only not
+// supported) in fp64 emulated on the int8 tensor cores: rows scaled by powers of two,
+// split into S signed 7-bit digit slices, all slice products with s + t <= S - 1
+// (0-based) accumulated exactly in int32 per digit level, levels summed in fp64.
+cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s);
+// route a GemmArgs to the Ozaki path when it is large enough to pay (LAKER_OZAKI=0 disables)
+bool ozaki_eligible(const GemmArgs &g);
+
 // ------------------------------------------------------------- dense_la.cu
 // In-place lower Cholesky of the n x n SPD matrix A (row-major, lda; n % 64 == 0);
 // strict upper triangle zeroed.  *flag (device) set to 1 on a pivot <= 0.

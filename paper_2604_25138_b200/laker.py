@@ -36,7 +36,7 @@ EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_statu
             "laker_last_error", "laker_assemble_kernel", "laker_fit_preconditioner", "laker_pcg_solve",
             "laker_predict", "laker_load_kernel_rows", "laker_get_kernel_rows", "laker_set_preconditioner",
             "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_apply_operator",
-            "laker_get_stats", "laker_debug_igemm_s8"]
+            "laker_get_stats", "laker_debug_igemm_s8", "laker_debug_ozaki_gemm"]
 
 
 class LakerError(RuntimeError):
@@ -103,6 +103,7 @@ def _load() -> ctypes.CDLL:
         "laker_apply_operator": [vp, vp, vp],
         "laker_get_stats": [vp, ctypes.POINTER(Stats)],
         "laker_debug_igemm_s8": [vp, vp, vp, i64, i64, i64],
+        "laker_debug_ozaki_gemm": [vp, vp, vp, i64, i64, i64, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -242,6 +243,15 @@ def laker_debug_igemm_s8(A, B, C) -> None:
     s = lib.laker_debug_igemm_s8(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K)
     if s != LAKER_OK:
         raise LakerError(s, "laker_debug_igemm_s8")
+
+
+def laker_debug_ozaki_gemm(A, B, C, slices: int = 0) -> None:
+    """C = A B^T in fp64 emulated on the int8 tensor cores; torch float64 CUDA tensors."""
+    M, K = A.shape
+    N = B.shape[0]
+    s = lib.laker_debug_ozaki_gemm(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, slices)
+    if s != LAKER_OK:
+        raise LakerError(s, "laker_debug_ozaki_gemm")
 
 
 # ------------------------------------------------------------ convenience

@@ -22,3 +22,38 @@ def test_igemm_s8_exact(M, N, K):
     C = Cd.cpu().numpy()
     bad = np.flatnonzero(C.ravel() != ref.ravel())
     assert bad.size == 0, (bad.size, bad[:5], C.ravel()[bad[:3]], ref.ravel()[bad[:3]])
+
+
+def _exact_rowcol(A, B, i, j):
+    from fractions import Fraction
+    return sum(Fraction(float(a)) * Fraction(float(b)) for a, b in zip(A[i], B[j]))
+
+
+@pytest.mark.parametrize("M,N,K,S", [(256, 256, 512, 8), (300, 520, 1000, 8), (128, 256, 4096, 7),
+                                     (257, 129, 96, 8)])
+def test_ozaki_gemm_accuracy(M, N, K, S):
+    """fp64 GEMM emulated with S int8 digit slices per input: every input is kept to
+    2^-(7S-1) of its row (column) maximum and every level sum is exact, so each
+    entry is within (S+2) K 2^-(7S-1) max_k|a_ik| max_k|b_jk| (+ the final fp64
+    roundings) of the exact product -- the max-norm form of the fp64 GEMM bound
+    K u |a||b|.  Checked against longdouble everywhere and exact rationals on
+    sampled entries; rows/columns span 2^+-20 in scale, entries 2^-8 within a row."""
+    import torch
+    from paper_2604_25138_b200 import laker as L
+    r = np.random.default_rng(M + N + K + S)
+    A = r.standard_normal((M, K)) * np.exp2(r.integers(-20, 20, (M, 1))) * np.exp2(r.uniform(-8, 0, (M, K)))
+    B = r.standard_normal((N, K)) * np.exp2(r.integers(-20, 20, (N, 1)))
+    Cd = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    L.laker_debug_ozaki_gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), Cd, S)
+    C = Cd.cpu().numpy()
+    ref = (A.astype(np.longdouble) @ B.astype(np.longdouble).T).astype(np.float64)
+    mx = np.outer(np.abs(A).max(axis=1), np.abs(B).max(axis=1))
+    bound = (S + 2) * K * 2.0 ** -(7 * S - 1) * mx + 8 * np.finfo(float).eps * np.abs(ref)
+    err = np.abs(C - ref)
+    assert (err <= bound).all(), (err / mx).max()
+    # and in the usual relative sense: comparable to an fp64 GEMM
+    absdot = np.abs(A) @ np.abs(B).T
+    assert (err / absdot).max() <= (2e-13 if S >= 8 else 2e-11)
+    for (i, j) in [(0, 0), (M - 1, N - 1), (M // 2, N // 3)]:
+        ex = _exact_rowcol(A, B, i, j)
+        assert abs(float(ex - __import__("fractions").Fraction(float(C[i, j])))) <= bound[i, j]
