@@ -279,8 +279,11 @@ bool ozaki_eligible(const GemmArgs &g) {
     mode = (v && v[0] == '0') ? 0 : 1;
   }
   if (!mode || g.lower_only) return false;
-  // pays above ~2^32 multiply-adds with K long enough to amortize the slicing
-  return g.K >= 512 && (double)g.M * (double)g.N * (double)g.K >= 4.0e9;
+  // pays above ~2^32 multiply-adds, with K long enough to amortize the slicing and
+  // both output dimensions >= 512 (each input is re-sliced per call: a skinny product
+  // such as the block solve's K X with 64 right-hand sides would re-slice the large
+  // operand every iteration for little tensor work)
+  return g.K >= 512 && g.M >= 512 && g.N >= 512 && (double)g.M * (double)g.N * (double)g.K >= 4.0e9;
 }
 
 cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s) {

@@ -55,8 +55,11 @@ def run_std(cid, kinds=("learned", "jacobi", "none")):
              time_to_solution_s=reps[0]["seconds"], iters_per_s=reps[0]["iters"] / reps[0]["seconds"],
              assemble_ms=asm, fit_ms=st["fit_ms"] if kind == "learned" else 0.0,
              fit_cccp_steps=fit.get("iters"), predict_ms=pst["predict_ms"], grid=P.Eq.shape[0],
-             gemv_ms=st["op_ms"] / max(st["op_launches"], 1),
-             gemv_gbs=(8.0 * P.n * P.n + 16 * P.n) / (st["op_ms"] / max(st["op_launches"], 1)) / 1e6,
+             k_apply="symv" if st["symmetric_k"] else "gemv", p_factored=st["p_factored"],
+             k_apply_ms=st["op_ms"] / max(st["op_launches"], 1),
+             k_apply_gbs=((4.0 * P.n * (P.n + 1) if st["symmetric_k"] else 8.0 * P.n * P.n) + 16 * P.n)
+             / (st["op_ms"] / max(st["op_launches"], 1)) / 1e6,
+             p_apply_ms=st["prec_ms"] / max(st["prec_launches"], 1) if st["prec_launches"] else None,
              exp_inconclusive=pst["exp_inconclusive"])
     c.close()
 
