@@ -198,6 +198,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   laker::symv_init();
   laker::dgemm_init();
   laker::igemm_init();
+  laker::otf_tc_init();
   laker::otf_fast_init();
   const size_t npart = 4096;
   if (cudaMalloc(&c->counters, laker::kNumCtr * sizeof(unsigned int)) != cudaSuccess ||
@@ -235,6 +236,8 @@ laker_status laker_destroy(laker_ctx ctx) {
   free_dev(ctx, ctx->P);
   free_dev(ctx, ctx->Pdiag);
   laker::free_factors(ctx);
+  laker::oz_slices_free(ctx->ozE, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->counters);
   cudaFree(ctx->partials);
   cudaFree(ctx->flags);
@@ -328,6 +331,13 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   ctx->stats.exp_inconclusive += hf[0];
   ctx->stats.exp_overflow += hf[1];
   ctx->assembled = true;
+  // digit slices of E for the tcgen05 QK^T of the FAST on-the-fly operator / predict
+  ctx->ozE_valid = false;
+  if (d <= 128) {
+    if (laker::oz_slices_make(ctx->ozE, ctx->E, n, d, 7, s) == cudaSuccess) ctx->ozE_valid = true;
+    ctx->stats.kernel_launches += 2;
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  }
   if (hf[1] > 0) return set_err(ctx, LAKER_ERR_OVERFLOW, "scale*<e_i,e_j> exceeded ln(DBL_MAX)");
   LAKER_TRY(laker::refresh_symmetry(ctx, 0));
   return LAKER_OK;
@@ -437,8 +447,8 @@ laker_status laker_predict(laker_ctx ctx, int64_t m, const double *Eq, const dou
   cudaEventCreate(&e1);
   cudaEventRecord(e0, ctx->stream);
   if (a1 > a0)
-    laker::launch_kernel_matvec(mode, ev.dptr + a0 * ctx->d, a1 - a0, ctx->E, ctx->n, ctx->d, ctx->scale,
-                                      alv.dptr, 0.0, nullptr, ov.dptr + a0, ctx->flags, nullptr, ctx->stream);
+    LAKER_CUDA(ctx, laker::launch_kernel_matvec_ctx(ctx, mode, ev.dptr + a0 * ctx->d, a1 - a0, false, 0, alv.dptr,
+                                                    0.0, nullptr, ov.dptr + a0, nullptr, ctx->stream));
   ctx->stats.kernel_launches++;
   LAKER_CUDA(ctx, cudaGetLastError());
   cudaEventRecord(e1, ctx->stream);

@@ -44,6 +44,14 @@ struct Buf {
 
 struct SymvPlan;  // symv.cu
 
+// digit slices of a row-major fp64 matrix for the Ozaki products (otf_tc.cu)
+struct OzSlices {
+  int8_t *s = nullptr;   // rows x (S Kp), forward slice order
+  int32_t *e = nullptr;  // rows
+  int64_t rows = 0, Kp = 0;
+  int S = 0;
+};
+
 }  // namespace laker
 
 struct laker_ctx_s {
@@ -88,6 +96,10 @@ struct laker_ctx_s {
   int64_t f_alloc_nrp = 0, f_alloc_n = 0;  // sizes the factor buffers were allocated for (reused)
   size_t E_bytes = 0, K_bytes = 0;         // allocations kept across assemble calls of the same size
   double f_ainv = 0.0;
+
+  // FAST on-the-fly: digit slices of E for the tcgen05 QK^T (otf_tc.cu), built lazily
+  laker::OzSlices ozE;
+  bool ozE_valid = false;
 
   laker_stats stats{};
 };
@@ -186,6 +198,12 @@ void launch_kernel_matvec_fast(const double *Eq, int64_t m, const double *E, int
                                const double *w, double lambda, const double *xdiag, double *out,
                                const int32_t *done, cudaStream_t s);
 void otf_fast_init();
+// mode dispatch with the context: FAST and d <= 128 -> tcgen05 QK^T (otf_tc.cu) with the
+// E slices cached in ctx (rows of Eq = rows [eq_row0, eq_row0 + m) of E when Eq_is_E),
+// else otf_fast.cu (DMMA) / the EXACT kernel.  LAKER_OTF_TC=0 selects DMMA.
+cudaError_t launch_kernel_matvec_ctx(laker_ctx ctx, int mode, const double *Eq, int64_t m, bool Eq_is_E,
+                                     int64_t eq_row0, const double *w, double lambda, const double *xdiag,
+                                     double *out, const int32_t *done, cudaStream_t s);
 // mode dispatch for the on-the-fly matvec (EXACT: correctly rounded entries + Dot2)
 inline void launch_kernel_matvec(int mode, const double *Eq, int64_t m, const double *E, int64_t n, int32_t d,
                                  double scale, const double *w, double lambda, const double *xdiag, double *out,
@@ -254,6 +272,19 @@ cudaError_t launch_igemm_epi(const int8_t *A, int64_t lda, const int8_t *B, int6
 cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s);
 // route a GemmArgs to the Ozaki path when it is large enough to pay (LAKER_OZAKI=0 disables)
 bool ozaki_eligible(const GemmArgs &g);
+void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
+                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s);
+
+// --------------------------------------------------------------- otf_tc.cu
+// FAST on-the-fly kernel matvec on the tcgen05 int8 tensor cores: the QK^T dot
+// products of exp(scale <eq_a, e_i>) in Ozaki digit levels (S slices, d <= 128),
+// scale + exp + weight + row-sum epilogue fused (same contract as otf_fast.cu).
+cudaError_t oz_slices_make(OzSlices &o, const double *X, int64_t rows, int32_t d, int S, cudaStream_t s);
+void oz_slices_free(OzSlices &o, cudaStream_t s);
+cudaError_t launch_otf_tc(const OzSlices &A, int64_t a0, int64_t m, const OzSlices &B, int64_t n, double scale,
+                          const double *w, double lambda, const double *xdiag, double *out, const int32_t *done,
+                          cudaStream_t s);
+void otf_tc_init();
 
 // ------------------------------------------------------------- dense_la.cu
 // In-place lower Cholesky of the n x n SPD matrix A (row-major, lda; n % 64 == 0);

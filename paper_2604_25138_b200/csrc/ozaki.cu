@@ -272,6 +272,18 @@ inline int ozaki_S() {
 
 }  // namespace
 
+// scales + digit slices of a rows x K fp64 matrix (K-contiguous, or K x rows if trans):
+// out[r][slot(s) Kp + k], slot(s) = rev ? S-1-s : s; e[r] the row's power-of-two exponent
+void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
+                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s) {
+  if (trans)
+    ozaki_rowexp_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(X, ld, rows, K, 1, e);
+  else
+    ozaki_rowexp_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(X, ld, rows, K, 0, e);
+  ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32)), 256, 0, s>>>(
+      X, ld, rows, K, trans, e, S, rev, out, Kp);
+}
+
 bool ozaki_eligible(const GemmArgs &g) {
   static int mode = -1;
   if (mode < 0) {

@@ -43,9 +43,8 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
       launch_gemv(a, ctx->gemv_grid, ctx->stream);
     }
   } else {
-    launch_kernel_matvec(ctx->mode, ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, ctx->E, ctx->n, ctx->d,
-                               ctx->scale, p, ctx->lambda, p + ctx->r0, q, ctx->flags,
-                               st ? &st->done : nullptr, ctx->stream);
+    launch_kernel_matvec_ctx(ctx, ctx->mode, ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, true, ctx->r0, p,
+                             ctx->lambda, p + ctx->r0, q, st ? &st->done : nullptr, ctx->stream);
     if (epi == kEpiDelta) {
       const int g = (int)std::min<int64_t>(2 * ctx->num_sms, (ctx->n + kVecThreads - 1) / kVecThreads);
       dot_delta_kernel<<<g, kVecThreads, 0, ctx->stream>>>(ctx->n, p, q, st, ctx->partials,

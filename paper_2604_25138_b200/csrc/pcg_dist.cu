@@ -240,9 +240,8 @@ static void dist_operator(laker_ctx ctx, const double *p_full, double *q_loc, Pc
     a.pair_out = reinterpret_cast<dd_pair *>(pair_out); a.evict_first = true;
     launch_gemv(a, ctx->gemv_grid, ctx->stream);
   } else {
-    launch_kernel_matvec(ctx->mode, ctx->E + ctx->r0 * ctx->d, nloc, ctx->E, ctx->n, ctx->d, ctx->scale, p_full,
-                               ctx->lambda, p_full + ctx->r0, q_loc, ctx->flags, st ? &st->done : nullptr,
-                               ctx->stream);
+    launch_kernel_matvec_ctx(ctx, ctx->mode, ctx->E + ctx->r0 * ctx->d, nloc, true, ctx->r0, p_full, ctx->lambda,
+                             p_full + ctx->r0, q_loc, st ? &st->done : nullptr, ctx->stream);
     if (pair_out) {
       const int g = (int)std::min<int64_t>(2 * ctx->num_sms, (nloc + kVecThreads - 1) / kVecThreads);
       local_pair_kernel<<<g, kVecThreads, 0, ctx->stream>>>(nloc, p_full + ctx->r0, q_loc, pair_out, st,
