@@ -58,34 +58,45 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *A, int64_t lda,
 }
 
 // Rows [r0, r0 + nrows) of column block j0: X = A L^{-T}, L = A[j0.., j0..] (factored).
-// One thread per row (the row held in registers), right-looking substitution:
-// x_c = a_c / L_cc, then a_k -= x_c L_kc for k > c -- per entry the same fma
-// sequence as the dot-product form, with 64 independent chains of ILP.
-constexpr int kPanelThreads = 32;
+// Four threads per row (thread k holds entries c = k, k+4, ... in registers),
+// right-looking: x_c = a_c / L_cc from its owner by a shuffle, then
+// a_i -= x_c L_ic for i > c -- per entry the same fma sequence as the dot form.
+constexpr int kPanelThreads = 128;
+constexpr int kPanelRows = kPanelThreads / 4;
 __global__ void __launch_bounds__(kPanelThreads) potrf_panel_kernel(double *A, int64_t lda, int64_t j0, int64_t r0,
                                                                     int64_t nrows) {
   __shared__ double Ls[NB][NB + 1];
-  const int tid = threadIdx.x;
-#pragma unroll 16
-  for (int e = tid; e < NB * NB; e += kPanelThreads) {
+#pragma unroll 8
+  for (int e = threadIdx.x; e < NB * NB; e += kPanelThreads) {
     const int r = e / NB, c = e % NB;
     Ls[r][c] = A[(j0 + r) * lda + j0 + c];
   }
   __syncthreads();
-  const int64_t row = r0 + (int64_t)blockIdx.x * kPanelThreads + tid;
-  if (row >= r0 + nrows) return;
-  double *a = A + row * lda + j0;
-  double x[NB];
+  const int lane = threadIdx.x & 31, k = lane & 3;
+  const int64_t row = r0 + (int64_t)blockIdx.x * kPanelRows + (threadIdx.x >> 2);
+  const bool ok = row < r0 + nrows;
+  double *a = A + (ok ? row : r0) * lda + j0;
+  double x[NB / 4];
 #pragma unroll
-  for (int c = 0; c < NB; ++c) x[c] = a[c];
+  for (int t = 0; t < NB / 4; ++t) x[t] = ok ? a[4 * t + k] : 0.0;
 #pragma unroll
   for (int c = 0; c < NB; ++c) {
-    x[c] = __ddiv_rn(x[c], Ls[c][c]);
+    double xc = 0.0;
+    if (k == (c & 3)) {
+      xc = __ddiv_rn(x[c >> 2], Ls[c][c]);
+      x[c >> 2] = xc;
+    }
+    xc = __shfl_sync(0xffffffffu, xc, (lane & ~3) | (c & 3));
 #pragma unroll
-    for (int k = c + 1; k < NB; ++k) x[k] = __fma_rn(-x[c], Ls[k][c], x[k]);
+    for (int t = 0; t < NB / 4; ++t) {
+      const int i = 4 * t + k;
+      if (4 * t + 3 > c && i > c) x[t] = __fma_rn(-xc, Ls[i][c], x[t]);
+    }
   }
+  if (ok) {
 #pragma unroll
-  for (int c = 0; c < NB; ++c) a[c] = x[c];
+    for (int t = 0; t < NB / 4; ++t) a[4 * t + k] = x[t];
+  }
 }
 
 __global__ void zero_upper_kernel(double *A, int64_t lda, int64_t n) {
@@ -94,32 +105,48 @@ __global__ void zero_upper_kernel(double *A, int64_t lda, int64_t n) {
     A[r * lda + c] = 0.0;
 }
 
-// X[b] = L[b,b]^{-1} B[b] for one 64-row block; one thread per column, solution
-// in registers, right-looking (x_r = b_r / L_rr, then b_k -= L_kr x_r for k > r):
-// per entry the same fma sequence as the dot-product form, 64 chains of ILP.
-constexpr int kTrsmThreads = 32;
+// X[b] = L[b,b]^{-1} B[b] for one 64-row block.  Four threads per column (lanes
+// 4c .. 4c+3 of a warp), thread k holding rows k, k+4, ... of the column in
+// registers: step r takes x_r = b_r / L_rr from its owner by a shuffle and every
+// thread updates its rows i > r, b_i -= L_ir x_r -- per entry the same fma
+// sequence as the dot-product form.  8 columns per warp, 4 warps per CTA: 4x the
+// warps of a thread-per-column solve for the latency-bound 64-step chain.
+constexpr int kTrsmThreads = 128;
+constexpr int kTrsmCols = kTrsmThreads / 4;
 __global__ void __launch_bounds__(kTrsmThreads) trsm_diag_kernel(const double *L, int64_t ldl, int64_t b0, double *B,
                                                                  int64_t ldb, int64_t ncols) {
   __shared__ double Ls[NB][NB + 1];
-#pragma unroll 16
+#pragma unroll 8
   for (int e = threadIdx.x; e < NB * NB; e += kTrsmThreads) {
     const int r = e / NB, c = e % NB;
     Ls[r][c] = L[(b0 + r) * ldl + b0 + c];
   }
   __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncols) return;
-  double x[NB];
+  const int lane = threadIdx.x & 31, k = lane & 3;
+  const int64_t j = (int64_t)blockIdx.x * kTrsmCols + (threadIdx.x >> 2);
+  const bool ok = j < ncols;
+  double x[NB / 4];
 #pragma unroll
-  for (int r = 0; r < NB; ++r) x[r] = B[(b0 + r) * ldb + j];
+  for (int t = 0; t < NB / 4; ++t) x[t] = ok ? B[(b0 + 4 * t + k) * ldb + j] : 0.0;
 #pragma unroll
   for (int r = 0; r < NB; ++r) {
-    x[r] = __ddiv_rn(x[r], Ls[r][r]);
+    // owner k == r % 4 holds row r in x[r / 4]
+    double xr = 0.0;
+    if (k == (r & 3)) {
+      xr = __ddiv_rn(x[r >> 2], Ls[r][r]);
+      x[r >> 2] = xr;
+    }
+    xr = __shfl_sync(0xffffffffu, xr, (lane & ~3) | (r & 3));
 #pragma unroll
-    for (int k = r + 1; k < NB; ++k) x[k] = __fma_rn(-Ls[k][r], x[r], x[k]);
+    for (int t = 0; t < NB / 4; ++t) {
+      const int i = 4 * t + k;
+      if (4 * t + 3 > r && i > r) x[t] = __fma_rn(-Ls[i][r], xr, x[t]);
+    }
   }
+  if (ok) {
 #pragma unroll
-  for (int r = 0; r < NB; ++r) B[(b0 + r) * ldb + j] = x[r];
+    for (int t = 0; t < NB / 4; ++t) B[(b0 + 4 * t + k) * ldb + j] = x[t];
+  }
 }
 
 __global__ void transpose_kernel(const double *__restrict__ A, int64_t rows, int64_t cols, int64_t lda,
@@ -145,8 +172,8 @@ void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s
     ++*launches;
     const int64_t rest = n - j0 - NB;
     if (rest <= 0) break;
-    potrf_panel_kernel<<<(unsigned)((rest + kPanelThreads - 1) / kPanelThreads), kPanelThreads, 0, s>>>(A, lda, j0,
-                                                                                                      j0 + NB, rest);
+    potrf_panel_kernel<<<(unsigned)((rest + kPanelRows - 1) / kPanelRows), kPanelThreads, 0, s>>>(A, lda, j0,
+                                                                                                  j0 + NB, rest);
     ++*launches;
     GemmArgs g{};
     g.M = rest;
@@ -173,8 +200,8 @@ void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s
 void trsm_lower_left(const double *L, int64_t ldl, int64_t n, double *B, int64_t ldb, int64_t ncols,
                      cudaStream_t s, int64_t *launches) {
   for (int64_t b0 = 0; b0 < n; b0 += NB) {
-    trsm_diag_kernel<<<(unsigned)((ncols + kTrsmThreads - 1) / kTrsmThreads), kTrsmThreads, 0, s>>>(L, ldl, b0, B, ldb,
-                                                                                                    ncols);
+    trsm_diag_kernel<<<(unsigned)((ncols + kTrsmCols - 1) / kTrsmCols), kTrsmThreads, 0, s>>>(L, ldl, b0, B, ldb,
+                                                                                              ncols);
     ++*launches;
     const int64_t rest = n - b0 - NB;
     if (rest <= 0) break;
