@@ -4,6 +4,8 @@
 // update) and the lower-triangular solve with many right-hand sides
 // (64-row diagonal solves with the solution held in registers, GEMM updates
 // of the rows below).
+#include <algorithm>
+
 #include "laker_internal.h"
 
 namespace laker {
@@ -166,24 +168,53 @@ __global__ void transpose_kernel(const double *__restrict__ A, int64_t rows, int
 
 }  // namespace
 
+// Two-level blocking: 64-wide diagonal steps inside 256-wide block columns, so the
+// bulk of the flops is in K = 256 GEMM updates (a K = 64 DMMA GEMM runs at a
+// fraction of the rate: its 3-stage ring never fills) -- same operations per entry.
+constexpr int NB2 = 256;
+
 void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s, int64_t *launches) {
-  for (int64_t j0 = 0; j0 < n; j0 += NB) {
-    potrf_diag_kernel<<<1, 256, 0, s>>>(A, lda, j0, flag);
-    ++*launches;
-    const int64_t rest = n - j0 - NB;
+  for (int64_t J0 = 0; J0 < n; J0 += NB2) {
+    const int64_t Jend = std::min<int64_t>(n, J0 + NB2);
+    for (int64_t j0 = J0; j0 < Jend; j0 += NB) {
+      potrf_diag_kernel<<<1, 256, 0, s>>>(A, lda, j0, flag);
+      ++*launches;
+      const int64_t rest = n - j0 - NB;
+      if (rest <= 0) break;
+      potrf_panel_kernel<<<(unsigned)((rest + kPanelRows - 1) / kPanelRows), kPanelThreads, 0, s>>>(A, lda, j0,
+                                                                                                    j0 + NB, rest);
+      ++*launches;
+      const int64_t inblk = Jend - j0 - NB;  // remaining columns of this block column
+      if (inblk <= 0) continue;
+      GemmArgs g{};  // A[j0+64.., j0+64 .. Jend) -= P P[0:inblk]^T  (lower tiles)
+      g.M = rest;
+      g.N = inblk;
+      g.K = NB;
+      g.A = A + (j0 + NB) * lda + j0;
+      g.lda = lda;
+      g.B = g.A;
+      g.ldb = lda;
+      g.C = A + (j0 + NB) * lda + j0 + NB;
+      g.ldc = lda;
+      g.Cin = g.C;
+      g.ldcin = lda;
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      g.lower_only = true;
+      launch_dgemm(g, false, s);
+      ++*launches;
+    }
+    const int64_t rest = n - Jend;
     if (rest <= 0) break;
-    potrf_panel_kernel<<<(unsigned)((rest + kPanelRows - 1) / kPanelRows), kPanelThreads, 0, s>>>(A, lda, j0,
-                                                                                                  j0 + NB, rest);
-    ++*launches;
-    GemmArgs g{};
+    GemmArgs g{};  // trailing matrix: A[Jend.., Jend..] -= P P^T with P = A[Jend.., J0 .. Jend)
     g.M = rest;
     g.N = rest;
-    g.K = NB;
-    g.A = A + (j0 + NB) * lda + j0;
+    g.K = Jend - J0;
+    g.A = A + Jend * lda + J0;
     g.lda = lda;
     g.B = g.A;
     g.ldb = lda;
-    g.C = A + (j0 + NB) * lda + j0 + NB;
+    g.C = A + Jend * lda + Jend;
     g.ldc = lda;
     g.Cin = g.C;
     g.ldcin = lda;
@@ -199,21 +230,42 @@ void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s
 
 void trsm_lower_left(const double *L, int64_t ldl, int64_t n, double *B, int64_t ldb, int64_t ncols,
                      cudaStream_t s, int64_t *launches) {
-  for (int64_t b0 = 0; b0 < n; b0 += NB) {
-    trsm_diag_kernel<<<(unsigned)((ncols + kTrsmCols - 1) / kTrsmCols), kTrsmThreads, 0, s>>>(L, ldl, b0, B, ldb,
-                                                                                              ncols);
-    ++*launches;
-    const int64_t rest = n - b0 - NB;
+  for (int64_t B0 = 0; B0 < n; B0 += NB2) {
+    const int64_t Bend = std::min<int64_t>(n, B0 + NB2);
+    for (int64_t b0 = B0; b0 < Bend; b0 += NB) {
+      trsm_diag_kernel<<<(unsigned)((ncols + kTrsmCols - 1) / kTrsmCols), kTrsmThreads, 0, s>>>(L, ldl, b0, B, ldb,
+                                                                                                ncols);
+      ++*launches;
+      const int64_t inblk = Bend - b0 - NB;
+      if (inblk <= 0) continue;
+      GemmArgs g{};  // rows b0+64 .. Bend of the block: -= L[., b0:b0+64] X_b
+      g.M = inblk;
+      g.N = ncols;
+      g.K = NB;
+      g.A = L + (b0 + NB) * ldl + b0;
+      g.lda = ldl;
+      g.B = B + b0 * ldb;
+      g.ldb = ldb;
+      g.C = B + (b0 + NB) * ldb;
+      g.ldc = ldb;
+      g.Cin = g.C;
+      g.ldcin = ldb;
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      launch_dgemm(g, true, s);
+      ++*launches;
+    }
+    const int64_t rest = n - Bend;
     if (rest <= 0) break;
-    GemmArgs g{};
+    GemmArgs g{};  // rows below the block: -= L[Bend.., B0:Bend] X_[B0:Bend]  (K = 256)
     g.M = rest;
     g.N = ncols;
-    g.K = NB;
-    g.A = L + (b0 + NB) * ldl + b0;
+    g.K = Bend - B0;
+    g.A = L + Bend * ldl + B0;
     g.lda = ldl;
-    g.B = B + b0 * ldb;
+    g.B = B + B0 * ldb;
     g.ldb = ldb;
-    g.C = B + (b0 + NB) * ldb;
+    g.C = B + Bend * ldb;
     g.ldc = ldb;
     g.Cin = g.C;
     g.ldcin = ldb;
