@@ -171,7 +171,7 @@ __global__ void transpose_kernel(const double *__restrict__ A, int64_t rows, int
 // Two-level blocking: 64-wide diagonal steps inside 256-wide block columns, so the
 // bulk of the flops is in K = 256 GEMM updates (a K = 64 DMMA GEMM runs at a
 // fraction of the rate: its 3-stage ring never fills) -- same operations per entry.
-constexpr int NB2 = 256;
+constexpr int NB2 = 512;
 
 void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s, int64_t *launches) {
   for (int64_t J0 = 0; J0 < n; J0 += NB2) {
