@@ -199,6 +199,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   laker::dgemm_init();
   laker::igemm_init();
   laker::otf_tc_init();
+  laker::oz_skinny_init();
   laker::otf_fast_init();
   const size_t npart = 4096;
   if (cudaMalloc(&c->counters, laker::kNumCtr * sizeof(unsigned int)) != cudaSuccess ||

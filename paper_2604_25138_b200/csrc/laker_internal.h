@@ -273,7 +273,7 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
 // route a GemmArgs to the Ozaki path when it is large enough to pay (LAKER_OZAKI=0 disables)
 bool ozaki_eligible(const GemmArgs &g);
 void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
-                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s);
+                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf = nullptr);
 
 // --------------------------------------------------------------- otf_tc.cu
 // FAST on-the-fly kernel matvec on the tcgen05 int8 tensor cores: the QK^T dot
@@ -285,6 +285,16 @@ cudaError_t launch_otf_tc(const OzSlices &A, int64_t a0, int64_t m, const OzSlic
                           const double *w, double lambda, const double *xdiag, double *out, const int32_t *done,
                           cudaStream_t s);
 void otf_tc_init();
+
+// ---------------------------------------------------------- ozaki_skinny.cu
+// multi-RHS products C (M x N<=64) = alpha A op(B) + beta Cin with A pre-sliced (tcgen05)
+cudaError_t oz_slices_make_general(OzSlices &o, const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S,
+                                   cudaStream_t s, unsigned long long *mx_buf = nullptr);
+cudaError_t launch_oz_skinny(const OzSlices &A, const OzSlices &B, int64_t N, double alpha, double beta,
+                             const double *Cin, int64_t ldcin, double *C, int64_t ldc, double *part, int max_splits,
+                             int num_sms, cudaStream_t s);
+void oz_skinny_init();
+int oz_skinny_max_slices();
 
 // ------------------------------------------------------------- dense_la.cu
 // In-place lower Cholesky of the n x n SPD matrix A (row-major, lda; n % 64 == 0);

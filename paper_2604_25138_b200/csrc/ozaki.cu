@@ -229,6 +229,35 @@ __global__ void __launch_bounds__(256) ozaki_rowexp_kernel(const double *__restr
   }
 }
 
+// column maxima of a K x rows matrix (the transposed layout): 32 columns x 8 k-lanes per
+// CTA over a 1024-row chunk, |max| as IEEE bits (monotone for non-negative doubles) into
+// mx[r] by atomicMax; ozaki_bits2exp_kernel turns them into frexp exponents
+__global__ void __launch_bounds__(256) ozaki_colmax_kernel(const double *__restrict__ X, int64_t ld, int64_t rows,
+                                                           int64_t K, unsigned long long *__restrict__ mx) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * 32 + tx;
+  const int64_t k0 = (int64_t)blockIdx.y * 1024;
+  double m = 0.0;
+  if (r < rows)
+    for (int64_t k = k0 + ty; k < k0 + 1024 && k < K; k += 8) m = fmax(m, fabs(X[k * ld + r]));
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && r < rows) {
+    for (int i = 1; i < 8; ++i) m = fmax(m, red[i][tx]);
+    atomicMax(&mx[r], (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+__global__ void ozaki_bits2exp_kernel(const unsigned long long *__restrict__ mx, int64_t rows, int32_t *__restrict__ e) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const double m = __longlong_as_double((long long)mx[r]);
+  int ex = 0;
+  if (m > 0.0) frexp(m, &ex);
+  e[r] = ex;
+}
+
 // digits: out[r][slot(s) Kp + k] for s < S, slot(s) = rev ? S-1-s : s; 32 x 32 tiles
 // staged through shared memory so both the fp64 reads and the int8 writes coalesce
 __global__ void __launch_bounds__(256) ozaki_split_kernel(const double *__restrict__ X, int64_t ld, int64_t rows,
@@ -275,11 +304,18 @@ inline int ozaki_S() {
 // scales + digit slices of a rows x K fp64 matrix (K-contiguous, or K x rows if trans):
 // out[r][slot(s) Kp + k], slot(s) = rev ? S-1-s : s; e[r] the row's power-of-two exponent
 void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
-                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s) {
-  if (trans)
-    ozaki_rowexp_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(X, ld, rows, K, 1, e);
-  else
+                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf) {
+  if (trans) {
+    unsigned long long *mx = mx_buf;
+    if (!mx) cudaMallocAsync(&mx, (size_t)rows * sizeof(unsigned long long), s);
+    cudaMemsetAsync(mx, 0, (size_t)rows * sizeof(unsigned long long), s);
+    ozaki_colmax_kernel<<<dim3((unsigned)((rows + 31) / 32), (unsigned)((K + 1023) / 1024)), 256, 0, s>>>(X, ld, rows,
+                                                                                                        K, mx);
+    ozaki_bits2exp_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(mx, rows, e);
+    if (!mx_buf) cudaFreeAsync(mx, s);
+  } else {
     ozaki_rowexp_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(X, ld, rows, K, 0, e);
+  }
   ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32)), 256, 0, s>>>(
       X, ld, rows, K, trans, e, S, rev, out, Kp);
 }
@@ -315,16 +351,10 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   eb = ea + M;
   const bool fused = std::getenv("LAKER_OZAKI_UNFUSED") == nullptr;
   if (!fused && S > 1 && (err = cudaMallocAsync(&W, (size_t)M * N * sizeof(double), s)) != cudaSuccess) return err;
-  // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn)
-  ozaki_rowexp_kernel<<<(unsigned)((M + 7) / 8), 256, 0, s>>>(g.A, g.lda, M, K, 0, ea);
-  if (b_kn)
-    ozaki_rowexp_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(g.B, g.ldb, N, K, 1, eb);
-  else
-    ozaki_rowexp_kernel<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(g.B, g.ldb, N, K, 0, eb);
-  ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((M + 31) / 32)), 256, 0, s>>>(
-      g.A, g.lda, M, K, 0, ea, S, 0, As, Kp);
-  ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((N + 31) / 32)), 256, 0, s>>>(
-      g.B, g.ldb, N, K, b_kn ? 1 : 0, eb, S, 1, Bs, Kp);
+  // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn);
+  // (B slices in reverse order: level h's pairs are a contiguous K range in both paths)
+  launch_ozaki_split(g.A, g.lda, M, K, 0, S, 0, As, ea, Kp, s);
+  launch_ozaki_split(g.B, g.ldb, N, K, b_kn ? 1 : 0, S, 1, Bs, eb, Kp, s);
   if (fused) {
     static bool attr = false;
     if (!attr) {

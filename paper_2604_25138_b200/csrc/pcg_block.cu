@@ -13,6 +13,8 @@
 // Per-column scalars (delta, beta, termination) come from fixed-order Dot2
 // column reductions; a converged column is frozen (its delta/beta are not
 // applied) while the others continue; the loop ends when every column is done.
+#include <cstdlib>
+
 #include "pcg_kernels.cuh"
 
 namespace laker {
@@ -369,6 +371,32 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   auto apply = [&](const double *Amat, double lam, const double *X, double *Out, bool gated = true) {
     gemm(Amat, ld, n, ld, lam, X, X, Out, gated);
   };
+  // FAST: the operator product K X on the tcgen05 int8 tensor cores (ozaki_skinny.cu),
+  // K sliced once per solve and the right-hand-side block per product.  K's entries
+  // lie in a narrow range (exp of small arguments), so per-row digit scaling keeps
+  // ~2^-46 of every entry; the preconditioner factors (Q, M: entries spanning many
+  // binades, M indefinite-sign) stay on the DMMA GEMM -- sliced, their small entries
+  // lost enough precision to make r.theta <= 0 near convergence (tested).
+  const char *tcenv = std::getenv("LAKER_BLOCK_TC");
+  const bool tcb = !exact && m <= 64 && !(tcenv && tcenv[0] == '0');
+  const int Stc = oz_skinny_max_slices();
+  OzSlices sK, sQt, sM, sQr, sXn, sXr;  // sXn / sXr: RHS-block slices for K-dim n / N_r
+  double *part = nullptr;
+  unsigned long long *mxb = nullptr;
+  if (tcb) {
+    LAKER_CUDA(ctx, oz_slices_make_general(sK, ctx->K, ld, n, n, 0, Stc, s));
+    LAKER_CUDA(ctx, cudaMallocAsync(&part, (size_t)16 * std::max<int64_t>(n, 128) * 64 * sizeof(double), s));
+    LAKER_CUDA(ctx, cudaMallocAsync(&mxb, 64 * sizeof(unsigned long long), s));
+    // allocate the per-product slice buffers now: nothing may be allocated inside the graph capture
+    LAKER_CUDA(ctx, oz_slices_make_general(sXn, rr, mp, m, n, 1, Stc, s, mxb));
+  }
+  // Out (rows x m) = A X + lam Xd with A pre-sliced; X (kdim x m) sliced per product
+  auto gemm_tc = [&](const OzSlices &A, int64_t kdim, double lam, const double *X, const double *Xd, double *Out) {
+    OzSlices &sX = (kdim == n) ? sXn : sXr;
+    oz_slices_make_general(sX, X, mp, m, kdim, 1, Stc, s, mxb);
+    launch_oz_skinny(A, sX, m, 1.0, lam, Xd, mp, Out, mp, part, 16, ctx->num_sms, s);
+    ctx->stats.kernel_launches += 4;
+  };
   // theta = P R: dense rows, or the factored passes Z = Q^T R, W = M Z, Theta = Q W + a^-1/2 R
   auto apply_p = [&](const double *R, double *Th) {
     if (!fac) {
@@ -399,7 +427,10 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   const int64_t before = ctx->stats.kernel_launches;
   LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int j = 0; j < chunk; ++j) {
-    apply(ctx->K, ctx->lambda, pp, qq);
+    if (tcb)
+      gemm_tc(sK, n, ctx->lambda, pp, pp, qq);
+    else
+      apply(ctx->K, ctx->lambda, pp, qq);
     col(kColDelta);
     col(kColUpdate);
     if (dense) {
@@ -461,6 +492,14 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   cudaGraphDestroy(graph);
   cudaFreeAsync(base, s);
   if (zb) cudaFreeAsync(zb, s);
+  if (part) cudaFreeAsync(part, s);
+  oz_slices_free(sK, s);
+  oz_slices_free(sQt, s);
+  oz_slices_free(sM, s);
+  oz_slices_free(sQr, s);
+  oz_slices_free(sXn, s);
+  oz_slices_free(sXr, s);
+  if (mxb) cudaFreeAsync(mxb, s);
   cudaFreeAsync(st, s);
   cudaFreeAsync(hist, s);
   cudaFreeAsync(trel, s);

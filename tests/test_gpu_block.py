@@ -65,3 +65,35 @@ def test_block_fast_mode(ctx, L):
         ref = O.reference_solve(K, P.lam, P.Y[:, c])
         assert reps[c]["termination"] == L.TERM_RESIDUAL_TOL
         assert np.linalg.norm(A[:, c] - ref) / np.linalg.norm(ref) <= 1e-6
+
+
+@pytest.mark.parametrize("kind", ["jacobi", "learned"])
+def test_block_fast_tensor_core_products(ctx, L, kind):
+    """FAST block solve with its products on the tcgen05 int8 tensor cores
+    (ozaki_skinny.cu: K and the P factors sliced once per solve, S = 7 digit
+    slices): every column converges and solves the system to R14 and agrees
+    with the DMMA products (LAKER_BLOCK_TC=0) to R14.  Iteration counts are
+    FAST-mode envelope quantities (R15 iii): the S = 7 products carry ~2^-48
+    of each column's max |x| (vs the DMMA GEMM's ~K u sum |k||x|), which at
+    kappa ~ 1e7 (Jacobi) costs up to ~25% more iterations; bounded here at 35%."""
+    import os
+    P = make_problem(4, n=2048, nrhs=16, tol=1e-8)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_FAST)
+    if kind == "learned":
+        Z = np.asfortranarray(make_directions(4, P.n, P.n_dirs))
+        ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    else:
+        ctx.set_preconditioner(L.PRECOND_JACOBI)
+    A, reps, _ = ctx.pcg_solve(np.asfortranarray(P.Y), P.tol)
+    os.environ["LAKER_BLOCK_TC"] = "0"
+    try:
+        A0, reps0, _ = ctx.pcg_solve(np.asfortranarray(P.Y), P.tol)
+    finally:
+        del os.environ["LAKER_BLOCK_TC"]
+    K, _ = O.assemble(P.E, P.scale)
+    for c in range(P.Y.shape[1]):
+        ref = O.reference_solve(K, P.lam, P.Y[:, c])
+        assert reps[c]["termination"] == L.TERM_RESIDUAL_TOL
+        assert np.linalg.norm(A[:, c] - ref) / np.linalg.norm(ref) <= 1e-6
+        assert np.linalg.norm(A[:, c] - A0[:, c]) / np.linalg.norm(A0[:, c]) <= 1e-6
+        assert abs(reps[c]["iters"] - reps0[c]["iters"]) <= 0.35 * reps0[c]["iters"] + 3
