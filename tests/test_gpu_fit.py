@@ -34,7 +34,9 @@ def _fit_both(ctx, L, cid, n=None):
     return P, K, Pg, rep, Po, ro, st
 
 
-@pytest.mark.parametrize("cid,n", [(1, None), (2, None), (3, 2048), (3, 1000)])
+# (4, 2048): a draw of Z on which the coupled Newton-Schulz alone diverged after
+# reaching ||W - I|| ~ 6e-6 (fixed by the guarded uncoupled refinement, fit.cu)
+@pytest.mark.parametrize("cid,n", [(1, None), (2, None), (3, 2048), (3, 1000), (4, 2048)])
 def test_fit_matches_oracle(ctx, L, cid, n):
     P, K, Pg, rep, Po, ro, st = _fit_both(ctx, L, cid, n)
     assert rep["converged"] == 1 and ro.converged
