@@ -298,6 +298,19 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   else
     LAKER_CUDA(ctx, cudaMemcpyAsync(ctx->E, E, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
   LAKER_CUDA(ctx, cudaMemsetAsync(ctx->flags, 0, 2 * sizeof(unsigned long long), s));
+  // digit slices of E for the tcgen05 QK^T paths (FAST assembly, on-the-fly operator,
+  // predict); those paths use a branch-free exp, so they are enabled only when
+  // scale max ||e_i||^2 (a Cauchy-Schwarz bound of every argument) cannot overflow
+  ctx->ozE_valid = false;
+  if (d <= 128) {
+    double mx2 = 0.0;
+    LAKER_CUDA(ctx, laker::max_rownorm2(ctx->E, n, d, &mx2, s));
+    const char *tcenv = std::getenv("LAKER_OTF_TC");
+    if (std::fabs(scale) * mx2 < 700.0 && !(tcenv && tcenv[0] == '0') &&
+        laker::oz_slices_make(ctx->ozE, ctx->E, n, d, 7, s) == cudaSuccess)
+      ctx->ozE_valid = true;
+    ctx->stats.kernel_launches += 3;
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -314,6 +327,11 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
         laker::launch_assemble_exact_sym(ctx->E, n, d, scale, ctx->K, ctx->ld, ctx->flags, s);
       else
         laker::launch_assemble_exact_rows(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags, s);
+    } else if (ctx->ozE_valid && std::getenv("LAKER_ASSEMBLE_TC") && std::getenv("LAKER_ASSEMBLE_TC")[0] == '1') {
+      // QK^T on tcgen05 with the fused exp epilogue (otf_tc.cu).  Opt-in: it computes
+      // every tile (no mirroring) and measured 3.8 ms at C3 vs 1.24 ms for the DMMA
+      // kernel, which computes the upper triangle and mirrors it
+      LAKER_CUDA(ctx, laker::launch_assemble_tc(ctx->ozE, ctx->r0, rows, n, scale, ctx->K, ctx->ld, s));
     } else {
       laker::launch_assemble_fast(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags, s);
     }
@@ -332,13 +350,6 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   ctx->stats.exp_inconclusive += hf[0];
   ctx->stats.exp_overflow += hf[1];
   ctx->assembled = true;
-  // digit slices of E for the tcgen05 QK^T of the FAST on-the-fly operator / predict
-  ctx->ozE_valid = false;
-  if (d <= 128) {
-    if (laker::oz_slices_make(ctx->ozE, ctx->E, n, d, 7, s) == cudaSuccess) ctx->ozE_valid = true;
-    ctx->stats.kernel_launches += 2;
-    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
-  }
   if (hf[1] > 0) return set_err(ctx, LAKER_ERR_OVERFLOW, "scale*<e_i,e_j> exceeded ln(DBL_MAX)");
   LAKER_TRY(laker::refresh_symmetry(ctx, 0));
   return LAKER_OK;

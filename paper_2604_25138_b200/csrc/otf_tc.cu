@@ -67,6 +67,8 @@ __device__ __forceinline__ double pow2i(int k) {
 
 struct OtfArgs {
   int64_t a0, m, n;
+  double *K;    // MATERIALIZE: K[row][col] (local row, stride ldk) instead of row sums
+  int64_t ldk;
   int S;
   const int32_t *ea, *eb;
   double scale, lambda;
@@ -75,6 +77,7 @@ struct OtfArgs {
   const int32_t *done;
 };
 
+template <bool MATERIALIZE>
 __global__ void __launch_bounds__(kOThreads, 1)
     otf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const OtfArgs f) {
   if (f.done != nullptr && *(volatile const int32_t *)f.done) return;
@@ -187,14 +190,27 @@ __global__ void __launch_bounds__(kOThreads, 1)
       // lane l fetches column cb + l's weight and scale once; the row loop broadcasts them
       const int64_t cb = J * kON + qt * 32;
       const bool okl = cb + lane < f.n;
-      const double wl = okl ? f.w[cb + lane] : 0.0;
       const double pl = okl ? f.scale * pow2i(f.eb[cb + lane]) : 0.0;
+      if (MATERIALIZE) {
+        // K entries of this row segment: exp(scale 2^(e_i + e_j) acc) -- the same
+        // operations for (i, j) and (j, i), so K is bitwise symmetric
+        double *kr = f.K + row * f.ldk + cb;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const double wj = __shfl_sync(0xffffffffu, wl, j);
-        const double pj = __shfl_sync(0xffffffffu, pl, j);
-        rsum = fma(exp_fast(acc[j] * pe * pj), wj, rsum);
-        acc[j] = 0.0;
+        for (int j = 0; j < 32; ++j) {
+          const double pj = __shfl_sync(0xffffffffu, pl, j);
+          const double kv = exp_fast(acc[j] * pe * pj);
+          if (rok && cb + j < f.n) kr[j] = kv;
+          acc[j] = 0.0;
+        }
+      } else {
+        const double wl = okl ? f.w[cb + lane] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double wj = __shfl_sync(0xffffffffu, wl, j);
+          const double pj = __shfl_sync(0xffffffffu, pl, j);
+          rsum = fma(exp_fast(acc[j] * pe * pj), wj, rsum);
+          acc[j] = 0.0;
+        }
       }
     }
     red[qt * kOM + rl] = rsum;
@@ -202,7 +218,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, 256);
-  if (threadIdx.x >= 64 && threadIdx.x < 64 + kOM) {
+  if (!MATERIALIZE && threadIdx.x >= 64 && threadIdx.x < 64 + kOM) {
     const int rl = threadIdx.x - 64;
     const int64_t row = r0 + rl;
     if (row < f.m) {
@@ -215,7 +231,10 @@ __global__ void __launch_bounds__(kOThreads, 1)
 
 }  // namespace
 
-void otf_tc_init() { cudaFuncSetAttribute(otf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOSmem); }
+void otf_tc_init() {
+  cudaFuncSetAttribute(otf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOSmem);
+  cudaFuncSetAttribute(otf_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOSmem);
+}
 
 cudaError_t oz_slices_make(OzSlices &o, const double *X, int64_t rows, int32_t d, int S, cudaStream_t s) {
   if (d > kOK || S > kOSmax || S < 1) return cudaErrorInvalidValue;
@@ -260,13 +279,59 @@ cudaError_t launch_otf_tc(const OzSlices &A, int64_t a0, int64_t m, const OzSlic
   f.xdiag = xdiag;
   f.out = out;
   f.done = done;
-  otf_tc_kernel<<<(unsigned)((m + kOM - 1) / kOM), kOThreads, kOSmem, s>>>(ta, tb, f);
+  otf_tc_kernel<false><<<(unsigned)((m + kOM - 1) / kOM), kOThreads, kOSmem, s>>>(ta, tb, f);
   return cudaGetLastError();
 }
 
 }  // namespace laker
 
 namespace laker {
+
+__global__ void max_rownorm2_kernel(const double *__restrict__ E, int64_t n, int d, unsigned long long *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) s = fma(E[i * d + k], E[i * d + k], s);
+  atomicMax(out, (unsigned long long)__double_as_longlong(s));
+}
+
+// max_i ||e_i||^2 (bounds |<e_i, e_j>| by Cauchy-Schwarz): decides whether the
+// branch-free exp of the tensor-core paths may be used (no overflow possible)
+cudaError_t max_rownorm2(const double *E, int64_t n, int d, double *out, cudaStream_t s) {
+  unsigned long long *dv = nullptr, hv = 0;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&dv, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+  cudaMemsetAsync(dv, 0, sizeof(unsigned long long), s);
+  max_rownorm2_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(E, n, d, dv);
+  cudaMemcpyAsync(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(dv, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  *out = __builtin_bit_cast(double, hv);
+  return cudaSuccess;
+}
+
+// FAST assembly: K rows [a0, a0 + m) (local row index) x all n columns, from the slices
+// of E (ctx->ozE), entries exp(scale <e_i, e_j>) on the tcgen05 QK^T path
+cudaError_t launch_assemble_tc(const OzSlices &E, int64_t a0, int64_t m, int64_t n, double scale, double *K,
+                               int64_t ldk, cudaStream_t s) {
+  if (m <= 0) return cudaSuccess;
+  CUtensorMap ta, tb;
+  const int64_t ld = (int64_t)E.S * E.Kp;
+  if (!make_tmap_s8(&ta, E.s, E.rows, ld, ld, kOM) || !make_tmap_s8(&tb, E.s, E.rows, ld, ld, kON))
+    return cudaErrorInvalidValue;
+  OtfArgs f{};
+  f.a0 = a0;
+  f.m = m;
+  f.n = n;
+  f.S = E.S;
+  f.ea = E.e;
+  f.eb = E.e;
+  f.scale = scale;
+  f.K = K;
+  f.ldk = ldk;
+  otf_tc_kernel<true><<<(unsigned)((m + kOM - 1) / kOM), kOThreads, kOSmem, s>>>(ta, tb, f);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_kernel_matvec_ctx(laker_ctx ctx, int mode, const double *Eq, int64_t m, bool Eq_is_E,
                                      int64_t eq_row0, const double *w, double lambda, const double *xdiag,
