@@ -310,6 +310,7 @@ def run_ours(args, rank, world, local_rank):
                                                                            else args.precond),
                        "l2": "inputs larger than L2 (K = 2 GiB per solve pass >> 126 MB)"},
             "time_to_solution_s": pcg_total / args.steps, "pcg_iters_per_solve": its[0],
+            "kappa_PA_lanczos": rep["lanczos_lmax"] / rep["lanczos_lmin"] if rep["lanczos_lmin"] > 0 else None,
             "stage_ms": {k: v / args.steps for k, v in stage.items()},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps},

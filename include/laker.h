@@ -160,6 +160,12 @@ typedef struct {
   double rel_residual;      /* recursive ||r|| / ||y|| at exit */
   double true_rel_residual; /* ||y - (lambda I + K) alpha|| / ||y||, recomputed once */
   double seconds;           /* device time of the PCG loop (CUDA events) */
+  /* extreme eigenvalues of the preconditioned operator P^(1/2) (lambda I + K) P^(1/2)
+     estimated from the CG coefficients (the Lanczos tridiagonal T_k with
+     T_jj = 1/delta_j + beta_{j-1}/delta_{j-1}, T_j,j+1 = sqrt(beta_j)/delta_j;
+     Saad, Iterative Methods, 2nd ed., Sec. 6.7.3); their ratio estimates
+     kappa(P A) (the quantity of Table I / P:853-858).  0 for the block solve. */
+  double lanczos_lmin, lanczos_lmax;
 } laker_solve_report;
 
 /* Solve (lambda I + K) alpha = Y by Alg. 1's PCG:

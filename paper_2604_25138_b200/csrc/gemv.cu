@@ -56,7 +56,7 @@ __device__ __forceinline__ void run_epilogue(const GemvArgs &a, double v) {
         st->term = LAKER_TERM_BREAKDOWN;
         st->done = 1;
       } else {
-        st->delta = __ddiv_rn(st->rho, v);
+        pcg_set_delta(st, __ddiv_rn(st->rho, v));
       }
       break;
     case kEpiBeta:
@@ -64,7 +64,7 @@ __device__ __forceinline__ void run_epilogue(const GemvArgs &a, double v) {
         st->term = LAKER_TERM_INDEFINITE;
         st->done = 1;
       } else {
-        st->beta = __ddiv_rn(v, st->rho);
+        pcg_set_beta(st, __ddiv_rn(v, st->rho));
         st->rho = v;
       }
       break;
@@ -94,7 +94,7 @@ __device__ __forceinline__ void fused_p_epilogue(const GemvArgs &a, double rthet
     st->done = 1;
     return;
   }
-  st->beta = __ddiv_rn(rtheta, st->rho);
+  pcg_set_beta(st, __ddiv_rn(rtheta, st->rho));
   st->rho = rtheta;
   if (it >= st->max_iters) {
     st->term = LAKER_TERM_MAX_ITERS;

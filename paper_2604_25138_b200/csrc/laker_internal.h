@@ -31,7 +31,19 @@ struct PcgState {
   int32_t max_iters;
   int32_t done;    // 1 once terminated (later kernels of a captured chunk are no-ops)
   int32_t term;    // LAKER_TERM_*
+  double *dh, *bh; // nullable: per-iteration delta_k / beta_k (Lanczos coefficients of the solve)
 };
+
+// every write of the step length / direction coefficient goes through these, so the
+// solve keeps its CG coefficients for the Lanczos eigenvalue estimates (pcg.cu)
+__device__ __forceinline__ void pcg_set_delta(PcgState *st, double d) {
+  st->delta = d;
+  if (st->dh) st->dh[st->iters] = d;
+}
+__device__ __forceinline__ void pcg_set_beta(PcgState *st, double b) {
+  st->beta = b;
+  if (st->bh && st->iters > 0) st->bh[st->iters - 1] = b;
+}
 
 // Ticket counters for the "last CTA reduces" epilogues, one per reduction
 // site, reset by the last CTA.
@@ -322,6 +334,8 @@ void free_factors(laker_ctx ctx);
 laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha, const laker_solve_opts &o,
                               laker_solve_report *rep, double *history);
 laker_status apply_operator_device(laker_ctx ctx, const double *x, double *y);
+void lanczos_extremes(const std::vector<double> &dl, const std::vector<double> &bt, int k, double &lmin,
+                      double &lmax);
 
 // -------------------------------------------------------------- pcg_dist.cu
 // Row-sharded PCG over NCCL (ctx->comm != nullptr): identical recurrence,

@@ -12,11 +12,50 @@
 // CUDA graph and the host only polls the state between graph launches.
 
 
+#include <cmath>
 #include <cstdlib>
 
 #include "pcg_kernels.cuh"
 
 namespace laker {
+
+// extreme eigenvalues of the Lanczos tridiagonal of k CG steps (delta_0..k-1,
+// beta_0..k-2) by Sturm-sequence bisection
+void lanczos_extremes(const std::vector<double> &dl, const std::vector<double> &bt, int k, double &lmin,
+                      double &lmax) {
+  lmin = lmax = 0.0;
+  if (k <= 0) return;
+  std::vector<double> a(k), b2(k > 1 ? k - 1 : 1, 0.0);
+  for (int j = 0; j < k; ++j) a[j] = 1.0 / dl[j] + (j > 0 ? bt[j - 1] / dl[j - 1] : 0.0);
+  for (int j = 0; j + 1 < k; ++j) b2[j] = bt[j] / (dl[j] * dl[j]);  // (sqrt(beta_j)/delta_j)^2
+  double lo = INFINITY, hi = -INFINITY;
+  for (int j = 0; j < k; ++j) {
+    const double r = (j > 0 ? std::sqrt(b2[j - 1]) : 0.0) + (j + 1 < k ? std::sqrt(b2[j]) : 0.0);
+    lo = std::min(lo, a[j] - r);
+    hi = std::max(hi, a[j] + r);
+  }
+  auto count_below = [&](double x) {  // eigenvalues < x
+    int c = 0;
+    double q = a[0] - x;
+    if (q < 0) ++c;
+    for (int j = 1; j < k; ++j) {
+      if (q == 0.0) q = 1e-300;
+      q = (a[j] - x) - b2[j - 1] / q;
+      if (q < 0) ++c;
+    }
+    return c;
+  };
+  auto kth = [&](int idx) {  // idx-th smallest (0-based)
+    double l = lo, h = hi;
+    for (int it = 0; it < 200 && h - l > 1e-15 * std::max(std::fabs(l), std::fabs(h)); ++it) {
+      const double mid = 0.5 * (l + h);
+      if (count_below(mid) > idx) h = mid; else l = mid;
+    }
+    return 0.5 * (l + h);
+  };
+  lmin = kth(0);
+  lmax = kth(k - 1);
+}
 
 // The operator apply used by the solver: q = (lambda I + K) p.
 static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState *st, int epi, double *dot_out) {
@@ -134,12 +173,15 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   double *p2 = w.y + ld, *r2 = p2 + ld;  // ping-pong partners for the fused iteration
   w.scal = r2 + ld;
   LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 8 * vb + 2 * sizeof(double), s));
-  LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)max_iters * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)3 * max_iters * sizeof(double), s));
+  double *dh = w.hist + max_iters, *bh = dh + max_iters;  // CG coefficients (Lanczos estimates)
   LAKER_CUDA(ctx, cudaMallocAsync(&w.st, sizeof(PcgState), s));
   LAKER_CUDA(ctx, cudaMemcpyAsync(w.y, y, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   PcgState h0{};
   h0.tol = o.tol;
   h0.max_iters = max_iters;
+  h0.dh = dh;
+  h0.bh = bh;
   LAKER_CUDA(ctx, cudaMemcpyAsync(w.st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
 
   // vector kernels: ~4 elements per thread (n = 16384 -> 16 CTAs) keeps the last-CTA reduction short
@@ -267,6 +309,12 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
   ctx->stats.solve_ms = ms;
+  if (rep && hs->iters > 0) {
+    std::vector<double> hd(hs->iters), hb(hs->iters);
+    cudaMemcpy(hd.data(), dh, hs->iters * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaMemcpy(hb.data(), bh, hs->iters * sizeof(double), cudaMemcpyDeviceToHost);
+    lanczos_extremes(hd, hb, hs->iters, rep->lanczos_lmin, rep->lanczos_lmax);
+  }
   if (rep) {
     rep->iters = hs->iters;
     rep->termination = hs->term;

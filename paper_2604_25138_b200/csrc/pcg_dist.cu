@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kVecThreads) dist_update_kernel(
     }
     if (lane == 0) {
       *counter = 0u;
-      st->delta = delta;
+      pcg_set_delta(st, delta);
     }
   }
 }
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kVecThreads) dist_unpack_r_kernel(int64_t nloc
       st->done = 1;
       return;
     }
-    st->beta = __ddiv_rn(rho_new, st->rho);
+    pcg_set_beta(st, __ddiv_rn(rho_new, st->rho));
     st->rho = rho_new;
     if (it >= st->max_iters) {
       st->term = LAKER_TERM_MAX_ITERS;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kVecThreads) dist_unpack_theta_kernel(int64_t 
     st->rho = rho_new;
     return;
   }
-  st->beta = __ddiv_rn(rho_new, st->rho);
+  pcg_set_beta(st, __ddiv_rn(rho_new, st->rho));
   st->rho = rho_new;
   if (st->iters >= st->max_iters) {
     st->term = LAKER_TERM_MAX_ITERS;
@@ -294,12 +294,15 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
   PcgState *st = nullptr;
   double *hist = nullptr;
   LAKER_CUDA(ctx, cudaMallocAsync(&st, sizeof(PcgState), s));
-  LAKER_CUDA(ctx, cudaMallocAsync(&hist, (size_t)max_iters * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&hist, (size_t)3 * max_iters * sizeof(double), s));
+  double *dh = hist + max_iters, *bh = dh + max_iters;  // CG coefficients (Lanczos estimates)
   LAKER_CUDA(ctx, cudaMemcpyAsync(yf, y, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   LAKER_CUDA(ctx, cudaMemcpyAsync(rl, y + r0, nloc * sizeof(double), cudaMemcpyDeviceToDevice, s));
   PcgState h0{};
   h0.tol = o.tol;
   h0.max_iters = max_iters;
+  h0.dh = dh;
+  h0.bh = bh;
   LAKER_CUDA(ctx, cudaMemcpyAsync(st, &h0, sizeof(PcgState), cudaMemcpyHostToDevice, s));
 
   const int vg = (int)std::min<int64_t>(2 * ctx->num_sms, (n + kVecThreads - 1) / kVecThreads);
@@ -424,6 +427,13 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
   cudaEventElapsedTime(&ms, ev0, ev1);
   ctx->stats.solve_ms = ms;
   if (rep) {
+    if (hs->iters > 0) {
+      LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+      std::vector<double> hd(hs->iters), hb(hs->iters);
+      cudaMemcpy(hd.data(), dh, hs->iters * sizeof(double), cudaMemcpyDeviceToHost);
+      cudaMemcpy(hb.data(), bh, hs->iters * sizeof(double), cudaMemcpyDeviceToHost);
+      lanczos_extremes(hd, hb, hs->iters, rep->lanczos_lmin, rep->lanczos_lmax);
+    }
     rep->iters = hs->iters;
     rep->termination = hs->term;
     rep->rel_residual = hs->iters > 0 ? hs->rel : (hs->term == LAKER_TERM_ZERO_RHS ? 0.0 : 1.0);

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kVecThreads) pcg_update_kernel(
         st->done = 1;
         return;
       }
-      st->beta = __ddiv_rn(rho_new, st->rho);
+      pcg_set_beta(st, __ddiv_rn(rho_new, st->rho));
       st->rho = rho_new;
       if (it >= st->max_iters) {
         st->term = LAKER_TERM_MAX_ITERS;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kVecThreads) dot_delta_kernel(int64_t n, const
       st->term = LAKER_TERM_BREAKDOWN;
       st->done = 1;
     } else {
-      st->delta = __ddiv_rn(st->rho, tot[0]);
+      pcg_set_delta(st, __ddiv_rn(st->rho, tot[0]));
     }
   }
 }

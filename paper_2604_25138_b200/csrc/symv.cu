@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
         st->term = LAKER_TERM_BREAKDOWN;
         st->done = 1;
       } else {
-        st->delta = __ddiv_rn(st->rho, dv);
+        pcg_set_delta(st, __ddiv_rn(st->rho, dv));
       }
       break;
     case kEpiBeta:
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
         st->term = LAKER_TERM_INDEFINITE;
         st->done = 1;
       } else {
-        st->beta = __ddiv_rn(dv, st->rho);
+        pcg_set_beta(st, __ddiv_rn(dv, st->rho));
         st->rho = dv;
       }
       break;

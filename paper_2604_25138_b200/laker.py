@@ -64,7 +64,8 @@ class SolveOpts(ctypes.Structure):
 
 class SolveReport(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("termination", ctypes.c_int32), ("rel_residual", ctypes.c_double),
-                ("true_rel_residual", ctypes.c_double), ("seconds", ctypes.c_double)]
+                ("true_rel_residual", ctypes.c_double), ("seconds", ctypes.c_double),
+                ("lanczos_lmin", ctypes.c_double), ("lanczos_lmax", ctypes.c_double)]
 
 
 class Stats(ctypes.Structure):

@@ -60,6 +60,8 @@ def run_std(cid, kinds=("learned", "jacobi", "none")):
              k_apply_gbs=((4.0 * P.n * (P.n + 1) if st["symmetric_k"] else 8.0 * P.n * P.n) + 16 * P.n)
              / (st["op_ms"] / max(st["op_launches"], 1)) / 1e6,
              p_apply_ms=st["prec_ms"] / max(st["prec_launches"], 1) if st["prec_launches"] else None,
+             kappa_PA_lanczos=reps[0]["lanczos_lmax"] / reps[0]["lanczos_lmin"] if reps[0]["lanczos_lmin"] > 0
+             else None,
              exp_inconclusive=pst["exp_inconclusive"])
     c.close()
 
