@@ -172,6 +172,29 @@ def make_problem(cid: int, n: Optional[int] = None, d: Optional[int] = None,
                    X=X, E=E, Y=Y, Xq=Xq, Eq=Eq, truth=T, n_dirs=n_dirs)
 
 
+def make_paper_problem(n: int, grid: int = 45, d: int = 10, lam: float = 1e-2, tol: float = 1e-10,
+                       noise_db: float = 1.5, n_tx: int = 3) -> Problem:
+    """The paper's own regime (PAPER.md l.682-737, Table "Key simulation parameters";
+    SURVEY §8(f) NEXT-4): n locations uniform on [0,100]^2 m, superposed
+    transmitters with log-distance decay (R4 model, no shadowing) plus i.i.d.
+    N(0, 1.5^2) dB measurement noise, d_e = 10 embeddings, G = exp(E E^T)
+    (scale 1, as in the worked example), lambda = 1e-2, a 45 x 45 evaluation grid,
+    PCG tolerance 1e-10.  Config id 0 seeds it (streams as in make_problem, noise
+    on stream 3)."""
+    X = rng(0, 0).uniform(0.0, 1.0, (n, 2))
+    Xq = grid_points(grid)
+    tx = rng(0, 1).uniform(0.0, 1.0, (n_tx, 2)) * 100.0
+    p = rng(0, 2).uniform(20.0, 30.0, n_tx)
+    clean = _rss_dbm(100.0 * X, tx, p, F_CARRIER, None)
+    y = clean + noise_db * rng(0, 3).standard_normal(n)
+    T = _rss_dbm(100.0 * Xq, tx, p, F_CARRIER, None)
+    emb = make_embedding(0, d)
+    spec = ConfigSpec(0, n, d, lam, tol, "uniform", n_tx, 1, grid, nr_schedule(n), "learned", "materialized", 1)
+    return Problem(spec=spec, n=n, d=d, lam=lam, tol=tol, scale=1.0, X=X, E=embed(emb, X),
+                   Y=np.asfortranarray(y[:, None]), Xq=Xq, Eq=embed(emb, Xq),
+                   truth=np.asfortranarray(T[:, None]), n_dirs=nr_schedule(n))
+
+
 def nr_schedule(n: int) -> int:
     """N_r = min(n, max(ceil(8 sqrt n), ceil(n/4))) -- SPEC.md l.241 reading of
     PAPER.md l.743 ("O(sqrt n) for small n and linearly for large n")."""

@@ -1,0 +1,50 @@
+"""The paper's own regime: d_e = 10,
+G = exp(E E^T), lambda = 1e-2, PCG to 1e-10.  Staged parity with the oracle
+(same K and P -> same iterations and alpha, bitwise), alpha within R14 of the
+Cholesky solution, and the Table I trends: LAKER needs fewer iterations than
+Jacobi and its Lanczos kappa(PA) is far below kappa(lambda I + G)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from synth import make_paper_problem, make_directions  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2604_25138_b200 import laker
+    return laker
+
+
+@pytest.mark.parametrize("n", [50, 200, 500])
+def test_paper_regime(L, n):
+    P = make_paper_problem(n)
+    c = L.Context(0)
+    c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    K, _ = O.assemble(P.E, P.scale)
+    assert (c.get_kernel_rows() == K).all()
+    ref = O.reference_solve(K, P.lam, P.y)
+    res = {}
+    for kind in ("none", "jacobi", "learned"):
+        if kind == "learned":
+            Z = np.asfortranarray(make_directions(0, P.n, P.n_dirs))
+            c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+            Q, M, ai = c.get_preconditioner_factors()
+            ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, ai, tol=P.tol)
+        elif kind == "jacobi":
+            c.set_preconditioner(L.PRECOND_JACOBI)
+            ao, ro = O.pcg(K, P.lam, P.y, O.P_JACOBI, O.jacobi_diag(P.E, P.scale, P.lam), tol=P.tol)
+        else:
+            c.set_preconditioner(L.PRECOND_NONE)
+            ao, ro = O.pcg(K, P.lam, P.y, O.P_NONE, None, tol=P.tol)
+        a, reps, _ = c.pcg_solve(P.y, P.tol)
+        assert reps[0]["iters"] == ro.iters and (a == ao).all(), kind     # staged parity, bitwise
+        assert np.linalg.norm(a - ref) / np.linalg.norm(ref) <= 1e-6
+        res[kind] = reps[0]
+    c.close()
+    assert res["learned"]["iters"] < res["jacobi"]["iters"]
+    kn = res["none"]["lanczos_lmax"] / res["none"]["lanczos_lmin"]
+    kl = res["learned"]["lanczos_lmax"] / res["learned"]["lanczos_lmin"]
+    assert kl < kn / 10, (kn, kl)
