@@ -140,10 +140,13 @@ typedef struct {
    JACOBI: P = diag(lambda I + K)^{-1}.  NONE: P = I.
    LEARNED: u_k = (lambda I + K) z_k, ubar_k = u_k/||u_k||; CCCP
    with shrinkage and trace normalization in the exact structured
-   form Sigma_t = a_t I + Ubar diag(b_t) Ubar^T (O4'); the dense P
-   rows are stored row-sharded like K.  report: host, may be NULL.
-   Errors: NOT_READY (no kernel), NOT_POSITIVE_DEFINITE, INVALID_ARGUMENT
-   (LEARNED with ON_THE_FLY storage). */
+   form Sigma_t = a_t I + Ubar diag(b_t) Ubar^T (O4'); P kept as
+   p_layout says (dense rows are row-sharded like K).  With ON_THE_FLY storage
+   (LAKER at C5) the directions GEMM consumes K's rows
+   assembled chunk by chunk into a transient buffer of <= 4 GiB (EXACT: the same
+   correctly rounded entries as MATERIALIZED); K is still never stored.
+   report: host, may be NULL.
+   Errors: NOT_READY (no kernel), NOT_POSITIVE_DEFINITE, INVALID_ARGUMENT. */
 laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
                                       laker_fit_report *report);
 

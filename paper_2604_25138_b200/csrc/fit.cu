@@ -4,7 +4,9 @@
 // literal n x n iteration):
 //
 //  1. directions  U = (lambda I + K) Z, ubar_k = u_k / ||u_k||
-//     -- DMMA GEMM, Dot2 column norms;  Z from the caller or a Philox stream;
+//     -- DMMA / Ozaki GEMM, Dot2 column norms;  Z from the caller or a Philox
+//     stream; with ON_THE_FLY storage K's rows are assembled chunk by chunk
+//     into a transient buffer feeding the GEMM (K is never stored);
 //  2. thin QR  Ubar = Q R by shifted CholeskyQR3 (Fukaya et al., SIAM J. Sci.
 //     Comput. 2020): three Gram / Cholesky / triangular-solve passes, all
 //     GEMM-shaped; R = R3 R2 R1 with a positive diagonal (the oracle's sign
@@ -16,7 +18,8 @@
 //     stop on ||Sigma_{t+1}-Sigma_t||_F / ||Sigma_t||_F <= fp_tol (reading R8),
 //     evaluated exactly through C = Ubar^T Ubar;
 //  4. T^{-1/2} by the coupled Newton-Schulz iteration (GEMMs only);
-//  5. P = a^{-1/2} I + Q (T^{-1/2} - a^{-1/2} I) Q^T, dense, row-sharded like K.
+//  5. P = a^{-1/2} I + Q (T^{-1/2} - a^{-1/2} I) Q^T, kept factored (one rank)
+//     or dense and row-sharded like K.
 // N_r is padded to a multiple of 128 with an identity block in R (zero
 // directions), which leaves every quantity of the first N_r rows unchanged.
 #include <cmath>
@@ -512,13 +515,42 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     philox_normal_kernel<<<4 * ctx->num_sms, 256, 0, s>>>(Zt, ld, n, nr, o.seed);
     ++L;
   }
-  if (!ctx->comm) {
+  // columns [cb, ce) of U^T = Zt K^T + lambda Zt into C (leading dimension ldc).  K is
+  // symmetric, so K^T's columns [cb, ce) are K's rows [cb, ce): the stored local rows, or,
+  // when K is not stored (ON_THE_FLY: LAKER at C5), rows assembled
+  // chunk by chunk into a scratch buffer of <= 4 GiB by the assembly kernels of the
+  // ctx's mode (EXACT: correctly rounded, bitwise the stored K) and consumed by the GEMM
+  auto directions = [&](int64_t cb, int64_t ce, double *C, int64_t ldc) -> laker_status {
     GemmArgs g{};
-    g.M = nrp; g.N = n; g.K = ld;
-    g.A = Zt; g.lda = ld; g.B = ctx->K; g.ldb = ld;  // K symmetric: Zt K^T = Zt K
-    g.C = Ut; g.ldc = ld; g.alpha = 1.0; g.beta = ctx->lambda; g.Cin = Zt; g.ldcin = ld;
-    launch_dgemm(g, false, s);
-    ++L;
+    g.M = nrp; g.K = ld;
+    g.A = Zt; g.lda = ld; g.ldb = ld;
+    g.ldc = ldc; g.alpha = 1.0; g.beta = ctx->lambda; g.ldcin = ld;
+    if (ctx->storage == LAKER_STORE_MATERIALIZED) {
+      g.N = ce - cb; g.B = ctx->K; g.C = C; g.Cin = Zt + cb;
+      launch_dgemm(g, false, s);
+      ++L;
+      return LAKER_OK;
+    }
+    int64_t cap = std::max<int64_t>(128, ((int64_t)4 << 30) / (ld * 8) / 128 * 128);
+    if (const char *env = std::getenv("LAKER_FIT_OTF_CHUNK")) cap = std::max<int64_t>(1, std::atoll(env));  // tests
+    const int64_t cw = std::min(ce - cb, cap);
+    double *Kc;
+    LAKER_CUDA(ctx, mem.alloc(&Kc, (size_t)cw * ld));
+    LAKER_CUDA(ctx, cudaMemsetAsync(Kc, 0, (size_t)cw * ld * 8, s));  // padding columns [n, ld) stay zero
+    for (int64_t c0 = cb; c0 < ce; c0 += cw) {
+      const int64_t c1 = std::min(ce, c0 + cw);
+      if (ctx->mode == LAKER_MODE_EXACT)
+        launch_assemble_exact_rows(ctx->E, n, ctx->d, ctx->scale, c0, c1, Kc, ld, ctx->flags, s);
+      else
+        launch_assemble_fast(ctx->E, n, ctx->d, ctx->scale, c0, c1, Kc, ld, ctx->flags, s);
+      g.N = c1 - c0; g.B = Kc; g.C = C + (c0 - cb); g.Cin = Zt + c0;
+      launch_dgemm(g, false, s);
+      L += 2;
+    }
+    return LAKER_OK;
+  };
+  if (!ctx->comm) {
+    LAKER_TRY(directions(0, n, Ut, ld));
   } else {
     // row-sharded K: this rank forms the columns [r0, r1) of U^T = Zt K^T + lambda Zt,
     // the W column blocks are all-gathered and the rest of the fit runs replicated
@@ -527,11 +559,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     double *Uloc, *Urecv;
     LAKER_CUDA(ctx, mem.alloc(&Uloc, (size_t)nrp * nloc));
     LAKER_CUDA(ctx, mem.alloc(&Urecv, (size_t)nrp * nloc * ctx->world));
-    GemmArgs g{};
-    g.M = nrp; g.N = nloc; g.K = ld;
-    g.A = Zt; g.lda = ld; g.B = ctx->K; g.ldb = ld;
-    g.C = Uloc; g.ldc = nloc; g.alpha = 1.0; g.beta = ctx->lambda; g.Cin = Zt + ctx->r0; g.ldcin = ld;
-    launch_dgemm(g, false, s);
+    LAKER_TRY(directions(ctx->r0, ctx->r1, Uloc, nloc));
     LAKER_NCCL(ctx, ncclAllGather(Uloc, Urecv, (size_t)nrp * nloc, ncclDouble, ctx->comm, s));
     LAKER_CUDA(ctx, cudaMemsetAsync(Ut, 0, big * 8, s));
     for (int w = 0; w < ctx->world; ++w)

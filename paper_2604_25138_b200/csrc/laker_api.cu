@@ -375,8 +375,6 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
       LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
       return LAKER_OK;
     case LAKER_PRECOND_LEARNED:
-      if (ctx->storage != LAKER_STORE_MATERIALIZED)
-        return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: LEARNED needs MATERIALIZED storage");
       if (ctx->world > 1 && !ctx->comm)
         return set_err(ctx, LAKER_ERR_NOT_READY, "fit: detached shard (no NCCL communicator)");
       {
@@ -532,8 +530,6 @@ laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *dat
   }
   if (kind == LAKER_PRECOND_EXTERNAL_DENSE) {
     if (!data) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "set_preconditioner: dense P rows needed");
-    if (ctx->storage != LAKER_STORE_MATERIALIZED)
-      return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "dense P needs MATERIALIZED storage");
     if (!ctx->P) {
       LAKER_CUDA(ctx, cudaMalloc(&ctx->P, (size_t)rows * ctx->ld * sizeof(double)));
       LAKER_CUDA(ctx, cudaMemsetAsync(ctx->P, 0, (size_t)rows * ctx->ld * sizeof(double), ctx->stream));

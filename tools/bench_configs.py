@@ -1,7 +1,7 @@
 """Per-config measurements of the hot path on one B200 (BASELINE.json configs
 C1..C5), through the C ABI.  Prints one JSON line per (config, variant).
 
-    python tools/bench_configs.py [C1 C2 C3 C4 C5 ...]
+    python tools/bench_configs.py [C1 C2 C3 C4 C5 C5L ...]   (C5L: LEARNED at C5, on the fly)
 
 C1/C2/C3: assemble (EXACT) -> fit (LEARNED, device Philox Z) -> PCG -> predict,
 plus NONE/JACOBI solves; C4: 64-RHS block solve with the learned P, EXACT
@@ -118,6 +118,29 @@ def run_c5(iters=20, grid=True):
     c.close()
 
 
+def run_c5_learned(max_iters=4000):
+    """LAKER at C5: K on the fly, LEARNED P fitted through the
+    chunked directions GEMM and applied factored; full solve to the tolerance."""
+    import torch
+    P = make_problem(5)
+    dev = torch.device("cuda", 0)
+    c = L.Context(0)
+    E = torch.from_numpy(P.E).to(dev)
+    c.assemble_kernel(E, P.scale, P.lam, L.STORE_ON_THE_FLY, L.MODE_FAST)
+    fit = c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7, p_layout=L.P_FACTORED)
+    a, reps, _ = c.pcg_solve(torch.from_numpy(P.y).to(dev), P.tol, max_iters=max_iters, instrument=True)
+    r = reps[0]
+    st = c.stats()
+    emit(config="C5", n=P.n, d=P.d, mode="fast", precond="learned (factored)", storage="on_the_fly",
+         n_dirs=fit["n_dirs"], fit_s=fit["seconds"], fit_cccp_steps=fit["iters"], iters=r["iters"],
+         termination=r["termination"], rel_residual=r["rel_residual"], true_rel_residual=r["true_rel_residual"],
+         solve_s=r["seconds"], ms_per_iter=r["seconds"] / max(r["iters"], 1) * 1e3,
+         kappa_PA_lanczos=r["lanczos_lmax"] / r["lanczos_lmin"],
+         k_apply_ms=st["op_ms"] / max(st["op_launches"], 1), p_apply_ms=st["prec_ms"] / max(st["prec_launches"], 1),
+         n_gpus=1)
+    c.close()
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
     for w in which:
@@ -127,3 +150,5 @@ if __name__ == "__main__":
             run_c4()
         elif w == "C5":
             run_c5()
+        elif w == "C5L":
+            run_c5_learned()
