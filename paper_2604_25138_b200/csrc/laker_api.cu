@@ -196,6 +196,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   c->gemv_grid = laker::gemv_max_grid(c->num_sms);
   laker::gemv_init();
   laker::symv_init();
+  laker::otf_sym_init();
   laker::dgemm_init();
   laker::igemm_init();
   laker::otf_tc_init();
@@ -243,6 +244,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   cudaFree(ctx->partials);
   cudaFree(ctx->flags);
   laker::symv_free(ctx->symv);
+  laker::symv_free(ctx->otf_sym);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -350,6 +352,7 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   ctx->stats.exp_inconclusive += hf[0];
   ctx->stats.exp_overflow += hf[1];
   ctx->assembled = true;
+  LAKER_CUDA(ctx, laker::otf_sym_prepare(ctx));
   if (hf[1] > 0) return set_err(ctx, LAKER_ERR_OVERFLOW, "scale*<e_i,e_j> exceeded ln(DBL_MAX)");
   LAKER_TRY(laker::refresh_symmetry(ctx, 0));
   return LAKER_OK;

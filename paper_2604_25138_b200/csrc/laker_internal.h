@@ -96,6 +96,8 @@ struct laker_ctx_s {
   // symmetric (upper-triangle) GEMV, single rank: used for K / P only after a
   // device check found them bitwise symmetric (symv.cu)
   laker::SymvPlan *symv = nullptr;
+  // tile partition of the symmetric on-the-fly operator (otf_sym.cu), built at assembly
+  laker::SymvPlan *otf_sym = nullptr;
   bool k_sym = false, p_sym = false;
 
   // factored LEARNED P = f_ainv I + Q M Q^T (fit.cu; applied in pcg.cu)
@@ -181,6 +183,11 @@ bool symv_bind(SymvPlan *p, int which, const double *A);
 void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s);
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s);
 void symv_init();
+// ------------------------------------------------------------- otf_sym.cu
+void otf_sym_init();
+cudaError_t otf_sym_prepare(laker_ctx ctx);
+bool launch_operator_otf_sym(laker_ctx ctx, const double *p, double *q, PcgState *st, int epi, double *dot_out,
+                             cudaStream_t s);
 size_t symv_smem_bytes();
 // set ctx->k_sym / p_sym: bitwise-symmetry check of the (whole, single-rank) matrix
 laker_status refresh_symmetry(laker_ctx ctx, int which);

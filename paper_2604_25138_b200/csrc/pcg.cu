@@ -83,6 +83,8 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
     } else {
       launch_gemv(a, ctx->gemv_grid, ctx->stream);
     }
+  } else if (launch_operator_otf_sym(ctx, p, q, st, epi, dot_out, ctx->stream)) {
+    ctx->stats.kernel_launches++;  // tile kernel + finalize (with the epilogue)
   } else {
     launch_kernel_matvec_ctx(ctx, ctx->mode, ctx->E + ctx->r0 * ctx->d, ctx->r1 - ctx->r0, true, ctx->r0, p,
                              ctx->lambda, p + ctx->r0, q, st ? &st->done : nullptr, ctx->stream);

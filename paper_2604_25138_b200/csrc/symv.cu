@@ -37,6 +37,7 @@
 
 #include "laker_internal.h"
 #include "tma.cuh"
+#include "tri.cuh"
 
 namespace laker {
 namespace {
@@ -61,28 +62,6 @@ constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 64 * sizeof(uin
 constexpr int kFinThreads = 512;
 constexpr int kFinSub = 16;              // threads per row in the finalize kernel
 
-struct SymvArgs {
-  int64_t n;
-  int32_t nb, nct, maxseg;
-  int64_t T;
-  const int64_t *toff;   // [nb + 1] first tile of each block-row
-  const int32_t *segfirst;  // [nb] first CTA covering block-row I
-  const int32_t *nseg;   // [nb]
-  const double *x;       // padded to >= nct * 64 (zeros past n)
-  double *y;
-  double lambda;
-  PcgState *state;
-  int epi;
-  double *dot_out;
-  dd_pair *pair_out;
-  dd_pair *colpart;      // [nb][ldcp]
-  int64_t ldcp;
-  dd_pair *rowpart;      // [nb][maxseg][128]
-  dd_pair *partials;     // finalize: per-CTA pairs
-  unsigned int *counter;
-  int evict_first;
-};
-
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int32_t c0, int32_t c1,
                                             uint64_t *bar, uint64_t policy) {
   asm volatile(
@@ -94,15 +73,6 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, in
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
-}
-
-__device__ __forceinline__ int find_block_row(const int64_t *toff, int nb, int64_t t) {
-  int lo = 0, hi = nb - 1;  // largest I with toff[I] <= t
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (toff[mid] <= t) lo = mid; else hi = mid - 1;
-  }
-  return lo;
 }
 
 __global__ void __launch_bounds__(kSymThreads, 1)
@@ -292,6 +262,7 @@ __device__ __forceinline__ dd_pair ldcg_pair(const dd_pair *p) {
   return dd_pair{__ldcg(&p->s), __ldcg(&p->c)};
 }
 
+template <int BR>
 __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   constexpr int kRowsPerPass = kFinThreads / kFinSub;
@@ -304,7 +275,7 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
   for (int64_t base = (int64_t)blockIdx.x * kRowsPerPass; base < a.n; base += (int64_t)gridDim.x * kRowsPerPass) {
     const int64_t i = base + tid / kFinSub;
     const bool valid = i < a.n;
-    const int J = valid ? (int)(i / kSR) : 0, r = valid ? (int)(i % kSR) : 0;
+    const int J = valid ? (int)(i / BR) : 0, r = valid ? (int)(i % BR) : 0;
     dd_pair v = {0.0, 0.0};
     // column partials of the tiles (I, .) above this row's diagonal block, I = sub (mod kFinSub)
     for (int I0 = sub; I0 < J; I0 += kFinSub * kMaxLd) {
@@ -320,7 +291,7 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
     // row partials of this block-row's segments
     if (valid) {
       const int ns = a.nseg[J];
-      for (int q = sub; q < ns; q += kFinSub) pair_add(v, ldcg_pair(a.rowpart + ((int64_t)J * a.maxseg + q) * kSR + r));
+      for (int q = sub; q < ns; q += kFinSub) pair_add(v, ldcg_pair(a.rowpart + ((int64_t)J * a.maxseg + q) * BR + r));
     }
     // combine the kFinSub sub-sums in sub order; all lanes shuffle
 #pragma unroll
@@ -439,7 +410,7 @@ PFN_encodeTiled get_encode() {
 
 struct SymvPlan {
   int64_t n = 0, ld = 0, T = 0, ldcp = 0;
-  int nb = 0, nct = 0, maxseg = 0, grid = 0, fin_grid = 0;
+  int nb = 0, nct = 0, maxseg = 0, grid = 0, fin_grid = 0, br = 0, tc = 0;
   int64_t *toff = nullptr;
   int32_t *segfirst = nullptr, *nseg = nullptr;
   dd_pair *colpart = nullptr, *rowpart = nullptr;
@@ -464,18 +435,20 @@ void symv_free(SymvPlan *&p) {
   p = nullptr;
 }
 
-cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
-  if (p && p->n == n && p->ld == ld) return cudaSuccess;
+cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
+  if (p && p->n == n && p->br == br && p->tc == tc && p->grid == (int)std::max<int64_t>(1, grid)) return cudaSuccess;
   symv_free(p);
   p = new SymvPlan();
   p->n = n;
-  p->ld = ld;
-  p->nb = (int)((n + kSR - 1) / kSR);
-  p->nct = (int)((n + kSC - 1) / kSC);
+  p->br = br;
+  p->tc = tc;
+  p->nb = (int)((n + br - 1) / br);
+  p->nct = (int)((n + tc - 1) / tc);
+  const int tpd = br / tc;
   std::vector<int64_t> toff(p->nb + 1, 0);
-  for (int I = 0; I < p->nb; ++I) toff[I + 1] = toff[I] + (p->nct - kTPD * I);
+  for (int I = 0; I < p->nb; ++I) toff[I + 1] = toff[I] + (p->nct - tpd * I);
   p->T = toff[p->nb];
-  p->grid = (int)std::min<int64_t>(num_sms, p->T);
+  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->T));
   std::vector<int32_t> segfirst(p->nb), nseg(p->nb);
   auto cta_of = [&](int64_t t) {  // CTA b with floor(T b / G) <= t < floor(T (b+1) / G)
     int64_t b = (t * p->grid) / p->T;
@@ -489,19 +462,52 @@ cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
     nseg[I] = cta_of(toff[I + 1] - 1) - segfirst[I] + 1;
     p->maxseg = std::max(p->maxseg, (int)nseg[I]);
   }
-  p->ldcp = (int64_t)p->nct * kSC;
+  p->ldcp = (int64_t)p->nct * tc;
   const int64_t passes = (n + kFinThreads / kFinSub - 1) / (kFinThreads / kFinSub);
-  p->fin_grid = (int)std::min<int64_t>(2 * num_sms, passes);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  p->fin_grid = (int)std::min<int64_t>(2 * sms, passes);
   cudaError_t e;
   if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&p->segfirst, segfirst.size() * sizeof(int32_t))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&p->nseg, nseg.size() * sizeof(int32_t))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&p->colpart, (size_t)p->nb * p->ldcp * sizeof(dd_pair))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&p->rowpart, (size_t)p->nb * p->maxseg * kSR * sizeof(dd_pair))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->rowpart, (size_t)p->nb * p->maxseg * br * sizeof(dd_pair))) != cudaSuccess) return e;
   cudaMemcpy(p->toff, toff.data(), toff.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
   cudaMemcpy(p->segfirst, segfirst.data(), segfirst.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
   cudaMemcpy(p->nseg, nseg.data(), nseg.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
   return cudaSuccess;
+}
+
+cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
+  if (p && p->n == n && p->ld == ld && p->br == kSR && p->tc == kSC) return cudaSuccess;
+  cudaError_t e = tri_plan(p, n, kSR, kSC, num_sms);
+  p->ld = ld;
+  return e;
+}
+
+void tri_fill(const SymvPlan *p, SymvArgs &a) {
+  a.n = p->n;
+  a.nb = p->nb;
+  a.nct = p->nct;
+  a.maxseg = p->maxseg;
+  a.T = p->T;
+  a.toff = p->toff;
+  a.segfirst = p->segfirst;
+  a.nseg = p->nseg;
+  a.colpart = p->colpart;
+  a.ldcp = p->ldcp;
+  a.rowpart = p->rowpart;
+}
+
+int tri_grid(const SymvPlan *p) { return p->grid; }
+int64_t tri_n(const SymvPlan *p) { return p->n; }
+
+void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s) {
+  if (p->br == 128)
+    symv_finalize_kernel<128><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+  else
+    symv_finalize_kernel<64><<<p->fin_grid, kFinThreads, 0, s>>>(a);
 }
 
 int symv_finalize_grid(const SymvPlan *p) { return p->fin_grid; }
@@ -525,14 +531,7 @@ bool symv_bind(SymvPlan *p, int which, const double *A) {
 
 void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s) {
   SymvArgs a{};
-  a.n = p->n;
-  a.nb = p->nb;
-  a.nct = p->nct;
-  a.maxseg = p->maxseg;
-  a.T = p->T;
-  a.toff = p->toff;
-  a.segfirst = p->segfirst;
-  a.nseg = p->nseg;
+  tri_fill(p, a);
   a.x = g.x;
   a.y = g.y;
   a.lambda = g.lambda;
@@ -540,14 +539,11 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   a.epi = g.epi;
   a.dot_out = g.dot_out;
   a.pair_out = g.pair_out;
-  a.colpart = p->colpart;
-  a.ldcp = p->ldcp;
-  a.rowpart = p->rowpart;
   a.partials = g.partials;
   a.counter = g.counter;
   a.evict_first = g.evict_first ? 1 : 0;
   symv_dot2_kernel<<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
-  symv_finalize_kernel<<<p->fin_grid, kFinThreads, 0, s>>>(a);
+  symv_finalize_kernel<kSR><<<p->fin_grid, kFinThreads, 0, s>>>(a);
 }
 
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s) {
