@@ -197,6 +197,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   laker::gemv_init();
   laker::symv_init();
   laker::otf_sym_init();
+  laker::otf_tc2_init();
   laker::dgemm_init();
   laker::igemm_init();
   laker::otf_tc_init();
@@ -245,6 +246,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   cudaFree(ctx->flags);
   laker::symv_free(ctx->symv);
   laker::symv_free(ctx->otf_sym);
+  if (ctx->cf) cudaFree(ctx->cf);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -311,6 +313,14 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
     if (std::fabs(scale) * mx2 < 700.0 && !(tcenv && tcenv[0] == '0') &&
         laker::oz_slices_make(ctx->ozE, ctx->E, n, d, 7, s) == cudaSuccess)
       ctx->ozE_valid = true;
+    const int64_t cfl = (n + 127) / 128 * 128;
+    if (ctx->ozE_valid && ctx->cf_len != cfl) {
+      if (ctx->cf) cudaFree(ctx->cf);
+      ctx->cf = nullptr;
+      ctx->cf_len = 0;
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->cf, (size_t)cfl * sizeof(double2)));
+      ctx->cf_len = cfl;
+    }
     ctx->stats.kernel_launches += 3;
   }
   cudaEvent_t e0, e1;
@@ -333,7 +343,7 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
       // QK^T on tcgen05 with the fused exp epilogue (otf_tc.cu).  Opt-in: it computes
       // every tile (no mirroring) and measured 3.8 ms at C3 vs 1.24 ms for the DMMA
       // kernel, which computes the upper triangle and mirrors it
-      LAKER_CUDA(ctx, laker::launch_assemble_tc(ctx->ozE, ctx->r0, rows, n, scale, ctx->K, ctx->ld, s));
+      LAKER_CUDA(ctx, laker::launch_assemble_tc(ctx->ozE, ctx->r0, rows, n, scale, ctx->K, ctx->ld, s, ctx->cf));
     } else {
       laker::launch_assemble_fast(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags, s);
     }

@@ -11,6 +11,7 @@
 // rowpart / colpart and the shared finalize kernel forms q_i (and the PCG
 // epilogue, so the on-the-fly operator gets the fused p.q like the stored one).
 //
+// FAST: the tcgen05 tiles of otf_tc2.cu (kSym).
 // EXACT (this file, otf_sym_exact_kernel): each entry exactly as assembly forms it
 // (sequential Dot2 over k, RN(scale x), correctly rounded exp -- the (i, j) and
 // (j, i) entries are the same bits), accumulated as Dot2 pairs; so q equals the
@@ -165,8 +166,13 @@ void otf_sym_init() {
 // the tile partition of the symmetric on-the-fly apply (at assembly: plans allocate,
 // which a captured solve may not)
 cudaError_t otf_sym_prepare(laker_ctx ctx) {
-  if (ctx->world != 1 || ctx->storage != LAKER_STORE_ON_THE_FLY || ctx->mode != LAKER_MODE_EXACT || ctx->d > 128)
-    return cudaSuccess;
+  if (ctx->world != 1 || ctx->storage != LAKER_STORE_ON_THE_FLY) return cudaSuccess;
+  if (ctx->mode == LAKER_MODE_FAST) {
+    // tcgen05 tiles of 128 x 128, one persistent CTA per SM (otf_tc2.cu)
+    if (!(ctx->ozE_valid && ctx->ozE.Kp == 64)) return cudaSuccess;
+    return tri_plan(ctx->otf_sym, ctx->n, 128, 128, ctx->num_sms);
+  }
+  if (ctx->d > 128) return cudaSuccess;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, otf_sym_exact_kernel, kXThreads, exact_smem(ctx->d));
   return tri_plan(ctx->otf_sym, ctx->n, kXT, kXT, std::max(1, per_sm) * ctx->num_sms);
@@ -182,25 +188,37 @@ bool launch_operator_otf_sym(laker_ctx ctx, const double *p, double *q, PcgState
     const char *v = std::getenv("LAKER_OTF_SYM");
     enabled = (v && v[0] == '0') ? 0 : 1;
   }
-  if (!enabled || ctx->world != 1 || ctx->storage != LAKER_STORE_ON_THE_FLY) return false;
-  if (ctx->mode != LAKER_MODE_EXACT || ctx->d > 128 || !ctx->otf_sym || tri_n(ctx->otf_sym) != ctx->n) return false;
-  OtfSymArgs f{};
-  tri_fill(ctx->otf_sym, f.t);
-  f.t.x = p;
-  f.t.y = q;
-  f.t.lambda = ctx->lambda;
-  f.t.state = st;
-  f.t.epi = epi;
-  f.t.dot_out = dot_out;
-  f.t.partials = ctx->partials;
-  f.t.counter = ctx->counters + kCtrGemv;
-  f.E = ctx->E;
-  f.d = ctx->d;
-  f.ldE = ctx->d + 1;
-  f.scale = ctx->scale;
-  f.flags = ctx->flags;
-  otf_sym_exact_kernel<<<tri_grid(ctx->otf_sym), kXThreads, exact_smem(ctx->d), s>>>(f);
-  launch_tri_finalize(ctx->otf_sym, f.t, s);
+  if (!enabled || ctx->world != 1 || ctx->storage != LAKER_STORE_ON_THE_FLY || !ctx->otf_sym ||
+      tri_n(ctx->otf_sym) != ctx->n)
+    return false;
+  const bool fast = ctx->mode == LAKER_MODE_FAST;
+  if (fast ? !(ctx->ozE_valid && ctx->ozE.Kp == 64 && tri_br(ctx->otf_sym) == 128)
+           : (ctx->d > 128 || tri_br(ctx->otf_sym) != kXT))
+    return false;
+  SymvArgs t{};
+  tri_fill(ctx->otf_sym, t);
+  t.x = p;
+  t.y = q;
+  t.lambda = ctx->lambda;
+  t.state = st;
+  t.epi = epi;
+  t.dot_out = dot_out;
+  t.partials = ctx->partials;
+  t.counter = ctx->counters + kCtrGemv;
+  if (fast) {
+    if (launch_otf_tc2_sym(ctx->ozE, ctx->n, ctx->scale, p, ctx->cf, t, tri_grid(ctx->otf_sym), s) != cudaSuccess)
+      return false;
+  } else {
+    OtfSymArgs f{};
+    f.t = t;
+    f.E = ctx->E;
+    f.d = ctx->d;
+    f.ldE = ctx->d + 1;
+    f.scale = ctx->scale;
+    f.flags = ctx->flags;
+    otf_sym_exact_kernel<<<tri_grid(ctx->otf_sym), kXThreads, exact_smem(ctx->d), s>>>(f);
+  }
+  launch_tri_finalize(ctx->otf_sym, t, s);
   return true;
 }
 

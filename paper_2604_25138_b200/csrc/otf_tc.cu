@@ -238,7 +238,7 @@ void otf_tc_init() {
 
 cudaError_t oz_slices_make(OzSlices &o, const double *X, int64_t rows, int32_t d, int S, cudaStream_t s) {
   if (d > kOK || S > kOSmax || S < 1) return cudaErrorInvalidValue;
-  const int64_t Kp = kOK;
+  const int64_t Kp = d <= 64 ? 64 : kOK;  // 64: the K = 64 slices of otf_tc2.cu
   if (!(o.s && o.rows == rows && o.S == S)) {
     oz_slices_free(o, s);
     cudaError_t e;
@@ -313,8 +313,9 @@ cudaError_t max_rownorm2(const double *E, int64_t n, int d, double *out, cudaStr
 // FAST assembly: K rows [a0, a0 + m) (local row index) x all n columns, from the slices
 // of E (ctx->ozE), entries exp(scale <e_i, e_j>) on the tcgen05 QK^T path
 cudaError_t launch_assemble_tc(const OzSlices &E, int64_t a0, int64_t m, int64_t n, double scale, double *K,
-                               int64_t ldk, cudaStream_t s) {
+                               int64_t ldk, cudaStream_t s, double2 *cf) {
   if (m <= 0) return cudaSuccess;
+  if (E.Kp == 64) return launch_assemble_tc2(E, a0, m, n, scale, cf, K, ldk, s);
   CUtensorMap ta, tb;
   const int64_t ld = (int64_t)E.S * E.Kp;
   if (!make_tmap_s8(&ta, E.s, E.rows, ld, ld, kOM) || !make_tmap_s8(&tb, E.s, E.rows, ld, ld, kON))
@@ -340,6 +341,18 @@ cudaError_t launch_kernel_matvec_ctx(laker_ctx ctx, int mode, const double *Eq, 
   if (use_tc < 0) {
     const char *v = std::getenv("LAKER_OTF_TC");
     use_tc = (v && v[0] == '0') ? 0 : 1;
+  }
+  if (mode == LAKER_MODE_FAST && ctx->d <= kOK && use_tc && ctx->ozE_valid && ctx->ozE.Kp == 64) {
+    // second-generation kernel (otf_tc2.cu), d <= 64
+    if (Eq_is_E)
+      return launch_otf_tc2_rect(ctx->ozE, eq_row0, m, ctx->ozE, ctx->n, ctx->scale, w, ctx->cf, lambda, xdiag, out,
+                                 done, s);
+    OzSlices q;
+    cudaError_t e = oz_slices_make(q, Eq, m, ctx->d, ctx->ozE.S, s);
+    if (e == cudaSuccess)
+      e = launch_otf_tc2_rect(q, 0, m, ctx->ozE, ctx->n, ctx->scale, w, ctx->cf, lambda, xdiag, out, done, s);
+    oz_slices_free(q, s);
+    return e;
   }
   if (mode == LAKER_MODE_FAST && ctx->d <= kOK && use_tc && ctx->ozE_valid) {
     if (Eq_is_E)

@@ -502,6 +502,7 @@ void tri_fill(const SymvPlan *p, SymvArgs &a) {
 
 int tri_grid(const SymvPlan *p) { return p->grid; }
 int64_t tri_n(const SymvPlan *p) { return p->n; }
+int tri_br(const SymvPlan *p) { return p->br; }
 
 void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s) {
   if (p->br == 128)

@@ -44,6 +44,10 @@ cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid);
 void tri_fill(const SymvPlan *p, SymvArgs &a);
 int tri_grid(const SymvPlan *p);
 int64_t tri_n(const SymvPlan *p);
+int tri_br(const SymvPlan *p);
+// otf_tc2.cu: the FAST symmetric on-the-fly tiles of a (128, 128) plan
+cudaError_t launch_otf_tc2_sym(const OzSlices &E, int64_t n, double scale, const double *w, double2 *cf,
+                               const SymvArgs &ta, int grid, cudaStream_t s);
 // y (and the epilogue of a.epi) from the partials written by a tile kernel of this plan
 void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s);
 
