@@ -11,8 +11,8 @@
 //  * 4 TMEM level buffers (512 columns): the MMAs of the next tile's first four
 //    levels overlap the exp phase of the current one;
 //  * two adjacent digit levels are combined exactly in int32 (v_{h-1} 2^7 + v_h,
-//    |v| <= 7 * 64 * 64^2 < 2^21) and converted to fp64 by the exponent-bias trick
-//    on the fp64 pipe (no I2F on the XU pipe): 4 conversions per entry, not 7;
+//    |v| <= 7 * 64 * 64^2 < 2^21): 4 int -> fp64 conversions per entry, not 7
+//    (the XU pipe that runs them is then ~20% busy instead of saturated);
 //  * exp by a 16-entry table of 2^(j/16) and a degree-7 polynomial (12 fp64 ops);
 //  * per-column factors {scale 2^(e_j), w_j} read as one broadcast 16-byte load;
 //  * kSym: the tiles of the block upper triangle over a persistent grid (tri.cuh):
@@ -87,11 +87,6 @@ __device__ __forceinline__ double exp_tab(double x, const double *tab) {
   const double tj = tab[k & 15];
   const double sc = __hiloint2double(__double2hiint(tj) + ((k >> 4) << 20), __double2loint(tj));
   return p * sc;
-}
-
-// v (|v| < 2^31) as a double on the fp64 pipe: bits 0x43300000:(v ^ 2^31) = 2^52 + 2^31 + v
-__device__ __forceinline__ double i2d(int32_t v) {
-  return __hiloint2double(0x43300000, v ^ (int32_t)0x80000000) - 0x1.000008p52;
 }
 
 __device__ __forceinline__ double pow2d(int k) {
@@ -181,7 +176,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         const int64_t J = KIND == kSym ? I + (t - rbeg) : t - t0;
         if (newI) {
-          if (aload > 0) mbar_wait(aempty, (uint32_t)((aload - 1) & 1));
+          if (aload > 0) mbar_wait_sleep(aempty, (uint32_t)((aload - 1) & 1));
           mbar_arrive_expect_tx(afull, (uint32_t)S * kQChunk);
           for (int c = 0; c < S; ++c)
             tc::tma_load_2d(sA + c * kQChunk, &tmA, c * kQK, (int32_t)(arow0 + (int64_t)I * kQM), afull);
@@ -189,7 +184,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         const int64_t lt = t - t0;
         for (int s = S - 1; s >= 0; --s) {
-          if (lt > 0) mbar_wait(&empty[s], (uint32_t)((lt - 1) & 1));
+          if (lt > 0) mbar_wait_sleep(&empty[s], (uint32_t)((lt - 1) & 1));
           mbar_arrive_expect_tx(&full[s], kQChunk);
           tc::tma_load_2d(sB + s * kQChunk, &tmB, s * kQK, (int32_t)(J * kQM), &full[s]);
         }
@@ -210,18 +205,18 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         if (newI) {
           if (aload > 0) tc::mma_commit(aempty);  // every MMA on the previous query block issued
-          mbar_wait(afull, (uint32_t)(aload & 1));
+          mbar_wait_sleep(afull, (uint32_t)(aload & 1));
           ++aload;
         }
         const int64_t lt = t - t0;
         for (int h = S - 1; h >= 0; --h, ++job) {
           const int b = (int)(job & (kQBufs - 1));
-          if (job >= kQBufs) mbar_wait(&tempty[b], (uint32_t)(((job / kQBufs) - 1) & 1));
+          if (job >= kQBufs) mbar_wait_sleep(&tempty[b], (uint32_t)(((job / kQBufs) - 1) & 1));
           tc::fence_after();
           const uint32_t td = tmem + (uint32_t)(b * kQM);
           for (int c = 0; c <= h; ++c) {
             const int tt = h - c;
-            mbar_wait(&full[tt], (uint32_t)(lt & 1));
+            mbar_wait_sleep(&full[tt], (uint32_t)(lt & 1));
             tc::fence_after();
             const uint32_t a0s = smem_u32(sA + c * kQChunk), b0s = smem_u32(sB + tt * kQChunk);
 #pragma unroll
@@ -283,8 +278,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
       for (int h = S - 1; h >= 0; h -= 2) {
         const bool two = h >= 1;
         const int b0 = (int)(job & (kQBufs - 1)), b1 = (int)((job + 1) & (kQBufs - 1));
-        mbar_wait(&tfull[b0], (uint32_t)((job / kQBufs) & 1));
-        if (two) mbar_wait(&tfull[b1], (uint32_t)(((job + 1) / kQBufs) & 1));
+        mbar_wait_sleep(&tfull[b0], (uint32_t)((job / kQBufs) & 1));
+        if (two) mbar_wait_sleep(&tfull[b1], (uint32_t)(((job + 1) / kQBufs) & 1));
         tc::fence_after();
         const double sc = pow2d(ea - 12 - 7 * h);  // 2^(e_row) folded into the level scale
 #pragma unroll
@@ -297,7 +292,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int32_t w = two ? (int32_t)v1[j] * 128 + (int32_t)v0[j] : (int32_t)v0[j];
-            acc[hh * 8 + j] = fma(i2d(w), sc, acc[hh * 8 + j]);
+            acc[hh * 8 + j] = fma((double)w, sc, acc[hh * 8 + j]);
           }
         }
         tc::fence_before();
