@@ -49,6 +49,27 @@ __device__ __forceinline__ void dot2_step(dd_pair &acc, double a, double b) {
   acc.c = __dadd_rn(acc.c, __dadd_rn(pe, se));
 }
 
+// acc += a * b with acc.s carrying a power-of-two offset C >= 2 sum|a b| over the whole
+// accumulation (so |acc.s| >= C/2 >= |a b| and Fast2Sum is error-free): 7 fp64 ops
+// instead of Dot2's 10.  The caller subtracts C (exactly, Sterbenz) at the end; the
+// rounding errors are still captured exactly, they are just O(u C) instead of
+// O(u |partial sum|) before the compensation sum (symv.cu).
+__device__ __forceinline__ void dot2_step_off(dd_pair &acc, double a, double b) {
+  double p, pe, s, se;
+  two_prod(a, b, p, pe);
+  fast_two_sum(acc.s, p, s, se);
+  acc.s = s;
+  acc.c = __dadd_rn(acc.c, __dadd_rn(pe, se));
+}
+
+// the smallest power of two above v (v >= 0 finite); 0 for v == 0
+__device__ __forceinline__ double pow2_above(double v) {
+  const long long b = __double_as_longlong(v);
+  if (b == 0) return 0.0;
+  const long long e = ((b >> 52) & 0x7ff) + 1;
+  return __longlong_as_double((e < 2046 ? e : 2046) << 52);
+}
+
 // acc += (o.s + o.c)  without rounding the incoming pair first
 __device__ __forceinline__ void pair_add(dd_pair &acc, const dd_pair &o) {
   double s, e;

@@ -40,7 +40,14 @@ laker_status refresh_symmetry(laker_ctx ctx, int which) {
   int h = 1;
   LAKER_CUDA(ctx, cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  if (h == 0) flag = symv_bind(ctx->symv, which, A);
+  if (h == 0) {
+    flag = symv_bind(ctx->symv, which, A);
+    if (flag) {
+      symv_rowmax(ctx->symv, which, A, ctx->stream);
+      ctx->stats.kernel_launches++;
+      LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+  }
   return LAKER_OK;
 }
 

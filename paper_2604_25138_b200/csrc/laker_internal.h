@@ -183,6 +183,7 @@ size_t gemv_smem_bytes();
 cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms);
 void symv_free(SymvPlan *&p);
 bool symv_bind(SymvPlan *p, int which, const double *A);
+void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s);
 void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s);
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s);
 void symv_init();

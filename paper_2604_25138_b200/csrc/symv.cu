@@ -48,9 +48,9 @@ constexpr int kTPD = kSR / kSC;          // tiles per diagonal block
 constexpr int kRPT = 8;                  // rows per consumer thread
 constexpr int kCons = 512;               // consumer threads
 constexpr int kConsWarps = kCons / 32;   // 16
-constexpr int kRedWarps = 4;             // warps 16..19: column reducers (one per SM sub-partition)
+constexpr int kRedWarps = 2;             // warps 16, 17: column reducers (19 warps -> 96 registers)
 constexpr int kRedWarp0 = kConsWarps;
-constexpr int kProdWarp = kConsWarps + kRedWarps;  // warp 20: TMA producer
+constexpr int kProdWarp = kConsWarps + kRedWarps;  // warp 18: TMA producer
 constexpr int kSymThreads = (kConsWarps + kRedWarps + 1) * 32;
 constexpr int kSStages = 6;
 constexpr uint32_t kTileBytes = kSR * kSC * 8;   // 32768
@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(kSymThreads, 1)
   uint64_t *rfull = empty + kSStages;  // [kRedBufs]
   uint64_t *rempty = rfull + kRedBufs;  // [kRedBufs]
   __shared__ int s_I0;
-  __shared__ double s_xr[kConsWarps][kRPT];  // x at the consumer warp's 16 rows (warp-private)
+  __shared__ double s_xr[kConsWarps][kRPT];  // x at the consumer warp's 8 rows (warp-private)
+  __shared__ double s_rm[kConsWarps][kRPT];  // rowmax at those rows
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t t0 = a.T * blockIdx.x / gridDim.x;
@@ -125,9 +126,10 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         const int jt = kTPD * I + (int)(t - rbeg);
         if (!first) mbar_wait_sleep(&empty[slot], ph ^ 1u);
         unsigned char *st = smem + slot * kStageBytes;
-        mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
+        mbar_arrive_expect_tx(&full[slot], kTileBytes + 2 * kXBytes);
         tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
         bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
+        bulk_g2s(st + kTileBytes + kXBytes, a.rowmax + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
         if (++slot == kSStages) {
           slot = 0;
           ph ^= 1u;
@@ -140,9 +142,9 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 
   if (warp >= kRedWarp0) {
     // ------------------------------------------------ column reducers: warp r owns columns
-    // 8r .. 8r+7; lane l sums the pairs of warps 4q .. 4q+3 (q = l / 8) of column 8r + l % 8,
-    // then the four q-partials are combined by shuffles -- a fixed-shape tree.
-    const int r = warp - kRedWarp0, q = lane >> 3, col = 8 * r + (lane & 7);
+    // 16r .. 16r+15; lane l sums the pairs of warps 8q .. 8q+7 (q = l / 16) of column
+    // 16r + l % 16 in warp order, then the two q-partials are combined by one shuffle.
+    const int r = warp - kRedWarp0, q = lane >> 4, col = 16 * r + (lane & 15);
     int I = I0;
     int64_t rbeg = a.toff[I], rend = a.toff[I + 1];
     int b = 0;
@@ -155,19 +157,25 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       const int jt = kTPD * I + (int)(t - rbeg);
       if (jt / kTPD == I) continue;  // diagonal-block tile: rows only
       mbar_wait_sleep(&rfull[b], rph);
-      const dd_pair *rb = red + b * kConsWarps * kSC + 4 * q * kSC + col;
-      dd_pair v0 = rb[0], v1 = rb[kSC], v2 = rb[2 * kSC], v3 = rb[3 * kSC];
+      const dd_pair *rb = red + b * kConsWarps * kSC + 8 * q * kSC + col;
+      dd_pair w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = rb[k * kSC];
       __syncwarp();
       if (lane == 0) mbar_arrive(&rempty[b]);
-      pair_add(v0, v1);
-      pair_add(v2, v3);
-      pair_add(v0, v2);
-#pragma unroll
-      for (int off = 8; off < 32; off <<= 1) {
+      pair_add(w[0], w[1]);
+      pair_add(w[2], w[3]);
+      pair_add(w[4], w[5]);
+      pair_add(w[6], w[7]);
+      pair_add(w[0], w[2]);
+      pair_add(w[4], w[6]);
+      pair_add(w[0], w[4]);
+      dd_pair v0 = w[0];
+      {
         dd_pair o;
-        o.s = __shfl_down_sync(0xffffffffu, v0.s, off);
-        o.c = __shfl_down_sync(0xffffffffu, v0.c, off);
-        if ((q & ((2 * off >> 3) - 1)) == 0) pair_add(v0, o);
+        o.s = __shfl_down_sync(0xffffffffu, v0.s, 16);
+        o.c = __shfl_down_sync(0xffffffffu, v0.c, 16);
+        if (q == 0) pair_add(v0, o);
       }
       if (q == 0) a.colpart[(int64_t)I * a.ldcp + (int64_t)jt * kSC + col] = v0;
       if (++b == kRedBufs) {
@@ -179,9 +187,16 @@ __global__ void __launch_bounds__(kSymThreads, 1)
   }
 
   // -------------------------------------------------- consumer warps
+  // Every accumulator carries a power-of-two offset C >= 2 sum |a_ij x_j| of what it will
+  // add (row: <= nct products of |a| <= rowmax_i, |x| <= xmax; column: 8 products), so
+  // each step is TwoProd + Fast2Sum (dot2_step_off, 7 fp64 ops instead of 10); the offset
+  // is removed exactly before the pair leaves the thread.
   const int c = lane;  // column within the tile; rows 8 warp .. 8 warp + 7
   dd_pair acc[kRPT];
   double *xr = s_xr[warp];
+  double *rmr = s_rm[warp];
+  const double xm = *a.xmax;
+  const double mrow = 2.0 * (double)a.nct;
   int curI = -1;
   int64_t rbeg = 0, rend = 0;
   int slot = 0, b = 0;
@@ -194,7 +209,9 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     dd_pair *dst = a.rowpart + ((int64_t)I * a.maxseg + s) * kSR + warp * kRPT;
 #pragma unroll
     for (int k = 0; k < kRPT; ++k) {
-      dd_pair v = warp_reduce_pair(acc[k]);
+      dd_pair v = acc[k];
+      v.s = __dsub_rn(v.s, pow2_above(rmr[k] * xm * mrow));  // exact: v.s in [C/2, 3C/2]
+      v = warp_reduce_pair(v);
       v.s = __shfl_sync(0xffffffffu, v.s, 0);
       v.c = __shfl_sync(0xffffffffu, v.c, 0);
       if (lane == k) dst[k] = v;
@@ -208,11 +225,14 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       while (t >= a.toff[curI + 1]) ++curI;
       rbeg = a.toff[curI];
       rend = a.toff[curI + 1];
+      __syncwarp();
+      if (lane < kRPT) {
+        xr[lane] = a.x[(int64_t)curI * kSR + warp * kRPT + lane];
+        rmr[lane] = a.rowmax[(int64_t)curI * kSR + warp * kRPT + lane];
+      }
+      __syncwarp();
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{0.0, 0.0};
-      __syncwarp();
-      if (lane < kRPT) xr[lane] = a.x[(int64_t)curI * kSR + warp * kRPT + lane];
-      __syncwarp();
+      for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{pow2_above(rmr[k] * xm * mrow), 0.0};
     }
     const int I = curI;
     const int jt = kTPD * I + (int)(t - rbeg);
@@ -221,17 +241,36 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     const double *tile = reinterpret_cast<const double *>(smem + slot * kStageBytes);
     const double xc = tile[kSR * kSC + c];
     const double *tp = tile + warp * kRPT * kSC + c;
-    dd_pair cacc = {0.0, 0.0};
+    const double ccol = diag ? 0.0 : pow2_above(tile[kSR * kSC + kSC + c] * xm * 16.0);
+    dd_pair cacc = {ccol, 0.0};
     if (diag) {
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) dot2_step(acc[k], tp[k * kSC], xc);
+      for (int k = 0; k < kRPT; ++k) dot2_step_off(acc[k], tp[k * kSC], xc);
     } else {
+      // phased so that the 8 independent row steps (and the products of the column
+      // chain) are in flight together: loads, TwoProds, then the Fast2Sum chains
+      double v[kRPT], p[kRPT], pe[kRPT];
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) v[k] = tp[k * kSC];
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) two_prod(v[k], xc, p[k], pe[k]);
 #pragma unroll
       for (int k = 0; k < kRPT; ++k) {
-        const double v = tp[k * kSC];
-        dot2_step(acc[k], v, xc);
-        dot2_step(cacc, v, xr[k]);
+        double s, se;
+        fast_two_sum(acc[k].s, p[k], s, se);
+        acc[k].s = s;
+        acc[k].c = __dadd_rn(acc[k].c, __dadd_rn(pe[k], se));
       }
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) two_prod(v[k], xr[k], p[k], pe[k]);
+#pragma unroll
+      for (int k = 0; k < kRPT; ++k) {
+        double s, se;
+        fast_two_sum(cacc.s, p[k], s, se);
+        cacc.s = s;
+        cacc.c = __dadd_rn(cacc.c, __dadd_rn(pe[k], se));
+      }
+      cacc.s = __dsub_rn(cacc.s, ccol);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -370,6 +409,37 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
   }
 }
 
+// rm[i] = max_j |A_ij| (one warp per row)
+__global__ void rowmax_kernel(const double *__restrict__ A, int64_t n, int64_t ld, double *__restrict__ rm) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  double m = 0.0;
+  for (int64_t j = lane; j < n; j += 32) m = fmax(m, fabs(A[i * ld + j]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) rm[i] = m;
+}
+
+// *out = max_i |x_i| (one CTA)
+__global__ void __launch_bounds__(1024) absmax_kernel(const double *__restrict__ x, int64_t n, double *out,
+                                                      const PcgState *state) {
+  if (state != nullptr && *(volatile const int32_t *)&state->done) return;
+  __shared__ double sm[32];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) m = fmax(m, fabs(x[i]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = sm[threadIdx.x];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (threadIdx.x == 0) *out = m;
+  }
+}
+
 // flag[0] = 1 if A (n x n, row stride ld) is not bitwise symmetric
 __global__ void symv_check_kernel(const double *__restrict__ A, int64_t n, int64_t ld, int *flag) {
   __shared__ double tI[32][33];
@@ -414,6 +484,8 @@ struct SymvPlan {
   int64_t *toff = nullptr;
   int32_t *segfirst = nullptr, *nseg = nullptr;
   dd_pair *colpart = nullptr, *rowpart = nullptr;
+  double *rowmax[2] = {nullptr, nullptr};  // symv: per-row max |A_ij| of K / P, zero-padded
+  double *xmax = nullptr;
   CUtensorMap tm[2];
   const void *tm_base[2] = {nullptr, nullptr};
 };
@@ -431,6 +503,9 @@ void symv_free(SymvPlan *&p) {
   cudaFree(p->nseg);
   cudaFree(p->colpart);
   cudaFree(p->rowpart);
+  cudaFree(p->rowmax[0]);
+  cudaFree(p->rowmax[1]);
+  cudaFree(p->xmax);
   delete p;
   p = nullptr;
 }
@@ -482,8 +557,14 @@ cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
 cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
   if (p && p->n == n && p->ld == ld && p->br == kSR && p->tc == kSC) return cudaSuccess;
   cudaError_t e = tri_plan(p, n, kSR, kSC, num_sms);
+  if (e != cudaSuccess) return e;
   p->ld = ld;
-  return e;
+  const size_t len = (size_t)p->nct * kSC;
+  for (int w = 0; w < 2; ++w) {
+    if ((e = cudaMalloc(&p->rowmax[w], len * sizeof(double))) != cudaSuccess) return e;
+    if ((e = cudaMemset(p->rowmax[w], 0, len * sizeof(double))) != cudaSuccess) return e;
+  }
+  return cudaMalloc(&p->xmax, sizeof(double));
 }
 
 void tri_fill(const SymvPlan *p, SymvArgs &a) {
@@ -512,6 +593,11 @@ void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s) {
 }
 
 int symv_finalize_grid(const SymvPlan *p) { return p->fin_grid; }
+
+// which = 0 (K) or 1 (P): the row maxima of the (new) contents of A
+void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s) {
+  rowmax_kernel<<<(unsigned)((p->n + 7) / 8), 256, 0, s>>>(A, p->n, p->ld, p->rowmax[which]);
+}
 
 // which = 0 (K) or 1 (P); (re)encodes the tensor map when the base pointer changed
 bool symv_bind(SymvPlan *p, int which, const double *A) {
@@ -543,6 +629,9 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   a.partials = g.partials;
   a.counter = g.counter;
   a.evict_first = g.evict_first ? 1 : 0;
+  a.rowmax = p->rowmax[which];
+  a.xmax = p->xmax;
+  absmax_kernel<<<1, 1024, 0, s>>>(g.x, p->n, p->xmax, g.state);
   symv_dot2_kernel<<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
   symv_finalize_kernel<kSR><<<p->fin_grid, kFinThreads, 0, s>>>(a);
 }

@@ -36,6 +36,10 @@ struct SymvArgs {
   dd_pair *partials;  // finalize: per-CTA pairs
   unsigned int *counter;
   int evict_first;
+  // symv: per-row max |A_ij| (padded with zeros to nct * TC) and max |x_j| (device
+  // scalar): the offsets of the Fast2Sum accumulation (dot2_step_off); null -> Dot2
+  const double *rowmax;
+  const double *xmax;
 };
 
 // partition of an n x n symmetric apply into BR x TC tiles over `grid` CTAs
