@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       for (int64_t rb = rbeg; rb < rend; rb += ROWS) {
         const int nr = (int)imin64(ROWS, rend - rb);
         for (int64_t c = 0; c < nchunks; ++c) {
-          if (!first) mbar_wait_sleep(&empty[slot], ph ^ 1u);
+          if (!first) mbar_wait(&empty[slot], ph ^ 1u);
           const int64_t col0 = c * kChunk;
           const int width = (int)imin64(kChunk, ncp - col0);
           const uint32_t bytes = (uint32_t)width * 8u;

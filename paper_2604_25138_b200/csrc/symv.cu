@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
           rend = a.toff[++I + 1];
         }
         const int jt = kTPD * I + (int)(t - rbeg);
-        if (!first) mbar_wait_sleep(&empty[slot], ph ^ 1u);
+        if (!first) mbar_wait(&empty[slot], ph ^ 1u);
         unsigned char *st = smem + slot * kStageBytes;
         mbar_arrive_expect_tx(&full[slot], kTileBytes + 2 * kXBytes);
         tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       }
       const int jt = kTPD * I + (int)(t - rbeg);
       if (jt / kTPD == I) continue;  // diagonal-block tile: rows only
-      mbar_wait_sleep(&rfull[b], rph);
+      mbar_wait(&rfull[b], rph);
       const dd_pair *rb = red + b * kConsWarps * kSC + 8 * q * kSC + col;
       dd_pair w[8];
 #pragma unroll
