@@ -171,6 +171,10 @@ struct GemvArgs {
   // non-square applies (factored P): when set, the diagonal term lambda xd_i and the
   // epilogue dot use xd (global row index row0 + i) instead of the streamed x
   const double *xd;
+  // symv: per-CTA maxima of |x| written by the kernel that produced x (nxparts of them);
+  // null -> launch_symv computes them
+  const double *xparts;
+  int nxparts;
 };
 void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
 void gemv_init();

@@ -60,7 +60,8 @@ void lanczos_extremes(const std::vector<double> &dl, const std::vector<double> &
 }
 
 // The operator apply used by the solver: q = (lambda I + K) p.
-static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState *st, int epi, double *dot_out) {
+static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState *st, int epi, double *dot_out,
+                            const double *pmax = nullptr, int npmax = 0) {
   if (ctx->storage == LAKER_STORE_MATERIALIZED) {
     GemvArgs a{};
     a.A = ctx->K;
@@ -78,6 +79,8 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
     a.epi = epi;
     a.evict_first = true;
     if (ctx->k_sym) {
+      a.xparts = pmax;
+      a.nxparts = npmax;
       launch_symv(ctx->symv, 0, a, ctx->stream);
       ctx->stats.kernel_launches++;
     } else {
@@ -175,7 +178,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
 
   Workspace w;
   const size_t vb = (size_t)ld * sizeof(double);
-  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 8 * vb + 2 * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 8 * vb + (2 + 256) * sizeof(double), s));
   w.r = w.alpha + ld;
   w.theta = w.r + ld;
   w.p = w.theta + ld;
@@ -183,7 +186,8 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   w.y = w.q + ld;
   double *p2 = w.y + ld, *r2 = p2 + ld;  // ping-pong partners for the fused iteration
   w.scal = r2 + ld;
-  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 8 * vb + 2 * sizeof(double), s));
+  double *pmax = w.scal + 2;  // per-CTA max |p| from the vector kernels (vg <= 148 entries), for symv
+  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 8 * vb + (2 + 256) * sizeof(double), s));
   LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)3 * max_iters * sizeof(double), s));
   double *dh = w.hist + max_iters, *bh = dh + max_iters;  // CG coefficients (Lanczos estimates)
   LAKER_CUDA(ctx, cudaMallocAsync(&w.st, sizeof(PcgState), s));
@@ -206,7 +210,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   pcg_init_kernel<<<vg, kVecThreads, 0, s>>>(n, w.y, w.alpha, w.r, w.st, ctx->partials, ctx->counters + kCtrInit);
   if (dense) launch_precond(ctx, w.r, w.theta, w.st, kEpiStoreDot, &w.st->rho);
   pcg_first_dir_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.r, w.theta, w.p, w.st, ctx->partials,
-                                                  ctx->counters + kCtrInit);
+                                                  ctx->counters + kCtrInit, pmax);
   ctx->stats.kernel_launches += 2;
   LAKER_CUDA(ctx, cudaGetLastError());
 
@@ -252,7 +256,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
       return;
     }
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
-    launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr);
+    launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, vg);
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
     pcg_update_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.p, w.q, w.alpha, w.r, w.theta, w.st,
                                                  w.hist, ctx->partials, ctx->counters + kCtrUpdate);
@@ -261,7 +265,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
       launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
     }
-    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0);
+    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
     ctx->stats.kernel_launches += 2;
   };
 
@@ -277,11 +281,40 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec, graph, 0));
   tmark("instantiated");
 
-  PcgState *hs = nullptr;
-  LAKER_CUDA(ctx, cudaMallocHost(&hs, sizeof(PcgState)));
+  // One chunk is always queued ahead of the host's check of the previous one, so the
+  // GPU never idles for the state read-back + relaunch; a chunk queued after the solve
+  // finished runs as early-exiting no-op kernels (every kernel tests st->done).  The
+  // instrumented run (event timings per chunk) keeps the synchronous loop.
+  PcgState *hs = nullptr, *hs2 = nullptr;
+  LAKER_CUDA(ctx, cudaMallocHost(&hs, 2 * sizeof(PcgState)));
+  hs2 = hs + 1;
   LAKER_CUDA(ctx, cudaMemcpyAsync(hs, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
   LAKER_CUDA(ctx, cudaStreamSynchronize(s));
   int32_t iters_prev = 0;
+  if (!instr && !hs->done) {
+    cudaEvent_t ce[2];
+    cudaEventCreateWithFlags(&ce[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ce[1], cudaEventDisableTiming);
+    PcgState *slot[2] = {hs, hs2};
+    int cur = 0;
+    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
+    ctx->stats.kernel_launches += per_chunk;
+    LAKER_CUDA(ctx, cudaMemcpyAsync(slot[0], w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    cudaEventRecord(ce[0], s);
+    for (;;) {
+      LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));  // speculative next chunk
+      ctx->stats.kernel_launches += per_chunk;
+      LAKER_CUDA(ctx, cudaMemcpyAsync(slot[cur ^ 1], w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      cudaEventRecord(ce[cur ^ 1], s);
+      LAKER_CUDA(ctx, cudaEventSynchronize(ce[cur]));
+      if (slot[cur]->done) break;
+      cur ^= 1;
+    }
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    *hs = *slot[cur ^ 1];  // the state after the last queued chunk (== final state)
+    cudaEventDestroy(ce[0]);
+    cudaEventDestroy(ce[1]);
+  }
   while (!hs->done) {
     LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
     ctx->stats.kernel_launches += per_chunk;

@@ -83,12 +83,27 @@ __global__ void __launch_bounds__(kVecThreads) pcg_init_kernel(int64_t n, const 
 
 // theta^0 = P r^0 (none: r, jacobi: d o r; dense: already in theta), p^0 = theta^0,
 // rho = r.theta.  For dense, rho_in_state = 1 (the P gemv stored it).
+// per-block max of m over the block's threads -> pmax[blockIdx.x] (pmax may be null)
+__device__ __forceinline__ void block_absmax(double m, double *pmax) {
+  if (pmax == nullptr) return;
+  __shared__ double sm[kVecThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kVecThreads / 32; ++w) m = fmax(m, sm[w]);
+    pmax[blockIdx.x] = m;
+  }
+}
+
 __global__ void __launch_bounds__(kVecThreads) pcg_first_dir_kernel(
     int64_t n, int pk, const double *__restrict__ dvec, const double *__restrict__ r,
     double *__restrict__ theta, double *__restrict__ p, PcgState *st, dd_pair *partials,
-    unsigned int *counter) {
+    unsigned int *counter, double *pmax = nullptr) {
   if (*(volatile int32_t *)&st->done) return;
   dd_pair v[1] = {{0.0, 0.0}};
+  double m = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double ri = r[i];
     double th;
@@ -101,8 +116,10 @@ __global__ void __launch_bounds__(kVecThreads) pcg_first_dir_kernel(
       th = theta[i];
     }
     p[i] = th;
+    m = fmax(m, fabs(th));
     dot2_step(v[0], ri, th);
   }
+  block_absmax(m, pmax);
   double tot[1];
   if (reduce_pairs_last_block<1>(v, partials, counter, tot)) {
     st->rho = tot[0];
@@ -174,11 +191,16 @@ __global__ void pcg_budget_kernel(PcgState *st) {
 // also closes the iteration budget (MAX_ITERS after the last allowed update).
 __global__ void __launch_bounds__(kVecThreads) pcg_pupdate_kernel(int64_t n, const double *__restrict__ theta,
                                                                   double *__restrict__ p, PcgState *st,
-                                                                  int budget = 0) {
+                                                                  int budget = 0, double *pmax = nullptr) {
   if (*(volatile const int32_t *)&st->done) return;
   const double beta = st->beta;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = __fma_rn(beta, p[i], theta[i]);
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pi = __fma_rn(beta, p[i], theta[i]);
+    p[i] = pi;
+    m = fmax(m, fabs(pi));
+  }
+  block_absmax(m, pmax);
   if (budget && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0 && st->iters >= st->max_iters) {
     st->term = LAKER_TERM_MAX_ITERS;
     st->done = 1;

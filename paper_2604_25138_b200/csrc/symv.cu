@@ -61,6 +61,7 @@ constexpr size_t kRedBytes = kRedBufs * kConsWarps * kSC * sizeof(dd_pair);  // 
 constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 64 * sizeof(uint64_t);
 constexpr int kFinThreads = 512;
 constexpr int kFinSub = 16;              // threads per row in the finalize kernel
+constexpr int kXParts = 32;              // CTAs of absmax_parts_kernel
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int32_t c0, int32_t c1,
                                             uint64_t *bar, uint64_t policy) {
@@ -195,7 +196,8 @@ __global__ void __launch_bounds__(kSymThreads, 1)
   dd_pair acc[kRPT];
   double *xr = s_xr[warp];
   double *rmr = s_rm[warp];
-  const double xm = *a.xmax;
+  double xm = 0.0;
+  for (int k = 0; k < a.nxparts; ++k) xm = fmax(xm, a.xparts[k]);
   const double mrow = 2.0 * (double)a.nct;
   int curI = -1;
   int64_t rbeg = 0, rend = 0;
@@ -421,22 +423,21 @@ __global__ void rowmax_kernel(const double *__restrict__ A, int64_t n, int64_t l
   if (lane == 0) rm[i] = m;
 }
 
-// *out = max_i |x_i| (one CTA)
-__global__ void __launch_bounds__(1024) absmax_kernel(const double *__restrict__ x, int64_t n, double *out,
-                                                      const PcgState *state) {
+// parts[b] = max |x_i| over CTA b's grid-stride share
+__global__ void __launch_bounds__(256) absmax_parts_kernel(const double *__restrict__ x, int64_t n, double *parts,
+                                                           const PcgState *state) {
   if (state != nullptr && *(volatile const int32_t *)&state->done) return;
-  __shared__ double sm[32];
+  __shared__ double sm[8];
   double m = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += 1024) m = fmax(m, fabs(x[i]));
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+    m = fmax(m, fabs(x[i]));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    m = sm[threadIdx.x];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (threadIdx.x == 0) *out = m;
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmax(m, sm[w]);
+    parts[blockIdx.x] = m;
   }
 }
 
@@ -485,7 +486,7 @@ struct SymvPlan {
   int32_t *segfirst = nullptr, *nseg = nullptr;
   dd_pair *colpart = nullptr, *rowpart = nullptr;
   double *rowmax[2] = {nullptr, nullptr};  // symv: per-row max |A_ij| of K / P, zero-padded
-  double *xmax = nullptr;
+  double *xparts = nullptr;  // [kXParts] when the caller supplies none
   CUtensorMap tm[2];
   const void *tm_base[2] = {nullptr, nullptr};
 };
@@ -505,7 +506,7 @@ void symv_free(SymvPlan *&p) {
   cudaFree(p->rowpart);
   cudaFree(p->rowmax[0]);
   cudaFree(p->rowmax[1]);
-  cudaFree(p->xmax);
+  cudaFree(p->xparts);
   delete p;
   p = nullptr;
 }
@@ -564,7 +565,7 @@ cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
     if ((e = cudaMalloc(&p->rowmax[w], len * sizeof(double))) != cudaSuccess) return e;
     if ((e = cudaMemset(p->rowmax[w], 0, len * sizeof(double))) != cudaSuccess) return e;
   }
-  return cudaMalloc(&p->xmax, sizeof(double));
+  return cudaMalloc(&p->xparts, kXParts * sizeof(double));
 }
 
 void tri_fill(const SymvPlan *p, SymvArgs &a) {
@@ -630,8 +631,14 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   a.counter = g.counter;
   a.evict_first = g.evict_first ? 1 : 0;
   a.rowmax = p->rowmax[which];
-  a.xmax = p->xmax;
-  absmax_kernel<<<1, 1024, 0, s>>>(g.x, p->n, p->xmax, g.state);
+  if (g.xparts) {
+    a.xparts = g.xparts;
+    a.nxparts = g.nxparts;
+  } else {
+    absmax_parts_kernel<<<kXParts, 256, 0, s>>>(g.x, p->n, p->xparts, g.state);
+    a.xparts = p->xparts;
+    a.nxparts = kXParts;
+  }
   symv_dot2_kernel<<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
   symv_finalize_kernel<kSR><<<p->fin_grid, kFinThreads, 0, s>>>(a);
 }

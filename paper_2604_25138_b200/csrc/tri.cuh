@@ -36,10 +36,11 @@ struct SymvArgs {
   dd_pair *partials;  // finalize: per-CTA pairs
   unsigned int *counter;
   int evict_first;
-  // symv: per-row max |A_ij| (padded with zeros to nct * TC) and max |x_j| (device
-  // scalar): the offsets of the Fast2Sum accumulation (dot2_step_off); null -> Dot2
+  // symv: per-row max |A_ij| (padded with zeros to nct * TC) and per-CTA maxima of |x_j|
+  // (max over nxparts values = max |x|): the offsets of dot2_step_off
   const double *rowmax;
-  const double *xmax;
+  const double *xparts;
+  int nxparts;
 };
 
 // partition of an n x n symmetric apply into BR x TC tiles over `grid` CTAs
