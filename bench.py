@@ -272,7 +272,7 @@ def run_ours(args, rank, world, local_rank):
     # triangle of the symmetric K (symv) or the local rows (gemv), plus x read and y written
     if sym:
         bytes_per_launch = 8.0 * n * (n + 1) / 2 + 16.0 * n
-        kname = "symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, Dot2)"
+        kname = "symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, offset-Fast2Sum compensated sums)"
     else:
         bytes_per_launch = 8.0 * rows * n + 16.0 * n
         kname = "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)"
