@@ -367,6 +367,7 @@ void free_factors(laker_ctx ctx) {
   cudaFree(ctx->fz);
   ctx->Qt = ctx->Qr = ctx->Mf = ctx->fz = ctx->fw = nullptr;
   ctx->p_factored = false;
+  ctx->m_sym = false;
   ctx->f_nr = ctx->f_nrp = ctx->f_ldq = 0;
   ctx->f_alloc_nrp = ctx->f_alloc_n = 0;
 }
@@ -848,6 +849,26 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     ctx->f_ldq = ldq;
     ctx->f_ainv = ainv;
     ctx->p_factored = true;
+    // M is formed bitwise symmetric (the Newton-Schulz iterates are lower + mirror): with
+    // LAKER_MSYM=1, w = M z streams only its block upper triangle (67 MB at N_r = 4096,
+    // below the 126 MB L2).  Opt-in: measured equal to the dense pass at C3 (2050 vs 2050
+    // it/s median, tools/ab_solve.py) -- the saved bytes are eaten by the extra launches
+    ctx->m_sym = false;
+    const char *senv = std::getenv("LAKER_SYMV"), *menv = std::getenv("LAKER_MSYM");
+    if (!(senv && senv[0] == '0') && (menv && menv[0] == '1') && ctx->world == 1) {
+      LAKER_CUDA(ctx, symv_plan(ctx->symv_m, nrp, ldq, ctx->num_sms));
+      int *dflag = reinterpret_cast<int *>(ctx->flags + 2);
+      LAKER_CUDA(ctx, cudaMemsetAsync(dflag, 0, sizeof(int), s));
+      launch_symv_check(ctx->Mf, nrp, ldq, dflag, s);
+      int h = 1;
+      LAKER_CUDA(ctx, cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+      LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+      if (h == 0 && symv_bind(ctx->symv_m, 0, ctx->Mf)) {
+        symv_rowmax(ctx->symv_m, 0, ctx->Mf, s);
+        ctx->m_sym = true;
+      }
+      L += 2;
+    }
   } else {
     free_factors(ctx);
     LAKER_TRY(form_dense_p(ctx, Ut, Zm, nrp, nrp, ainv));

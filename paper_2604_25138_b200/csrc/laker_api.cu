@@ -253,6 +253,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   cudaFree(ctx->flags);
   laker::symv_free(ctx->symv);
   laker::symv_free(ctx->otf_sym);
+  laker::symv_free(ctx->symv_m);
   if (ctx->cf) cudaFree(ctx->cf);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);

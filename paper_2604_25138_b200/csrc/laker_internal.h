@@ -102,6 +102,10 @@ struct laker_ctx_s {
   double2 *cf = nullptr;
   int64_t cf_len = 0;
   bool k_sym = false, p_sym = false;
+  // factored P: the middle factor M (N_r x N_r) applied by the symmetric GEMV when it is
+  // bitwise symmetric -- half of M's bytes, which then stay resident in L2 (fit.cu)
+  bool m_sym = false;
+  laker::SymvPlan *symv_m = nullptr;
 
   // factored LEARNED P = f_ainv I + Q M Q^T (fit.cu; applied in pcg.cu)
   bool p_factored = false;
