@@ -57,6 +57,25 @@ def test_factored_staged_pcg_bitwise(ctx, L, cid, n):
         assert np.linalg.norm(ag - ref) / np.linalg.norm(ref) <= 1e-6
 
 
+@pytest.mark.parametrize("cid,n", [(2, None), (3, 1000)])
+def test_factored_symmetric_M_staged_bitwise(ctx, L, monkeypatch, cid, n):
+    """LAKER_MSYM=1: w = M z through the symmetric GEMV (M is formed bitwise
+    symmetric) -- the same Dot2-exact row sums, so the staged parity stays bitwise."""
+    monkeypatch.setenv("LAKER_MSYM", "1")
+    P = make_problem(cid, n=n)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
+    ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    Q, M, ainv = ctx.get_preconditioner_factors()
+    assert (M == M.T).all()
+    K, _ = O.assemble(P.E, P.scale)
+    ag, reps, hist = ctx.pcg_solve(P.y, P.tol, want_history=True)
+    ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, ainv, tol=P.tol)
+    assert reps[0]["iters"] == ro.iters
+    _bitwise(hist, ro.history, "history")
+    _bitwise(ag, ao, "alpha")
+
+
 def test_factored_equals_dense_layout_P(ctx, L):
     """The dense rows formed from the factors equal the rows of a DENSE-layout
     fit bitwise (same factors, same formation), and both solves converge to
