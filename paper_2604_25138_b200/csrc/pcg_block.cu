@@ -24,14 +24,54 @@ constexpr int kBR = 32;   // rows of A per CTA
 constexpr int kBK = 32;   // k chunk
 constexpr int kBM = 64;   // RHS per CTA (columns)
 
-// Q[i][c] = RN(lambda Xd[row0+i][c] + sum_j A[i][j] X[j][c]), Dot2 per entry (Xd = X
-// for the operator; Xd = R for the last pass of the factored P, Q (M (Q^T R)) + a^-1/2 R).
+// rm[i] = max_j |A[i][j]| (one warp per row)
+__global__ void rowmax_abs_kernel(const double *__restrict__ A, int64_t rows, int64_t cols, int64_t lda,
+                                  double *__restrict__ rm) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= rows) return;
+  double v = 0.0;
+  for (int64_t j = lane; j < cols; j += 32) v = fmax(v, fabs(A[i * lda + j]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+  if (lane == 0) rm[i] = v;
+}
+
+// cm[c] = max_j |X[j][c]| (c < m; X row-major, ldx): block of 64 columns x 4 row lanes,
+// atomicMax on the bits (non-negative doubles order as integers); cm zeroed beforehand
+__global__ void __launch_bounds__(256) colmax_abs_kernel(const double *__restrict__ X, int64_t rows, int64_t m,
+                                                         int64_t ldx, unsigned long long *cm,
+                                                         const int32_t *__restrict__ all_done) {
+  if (all_done && *(volatile const int32_t *)all_done) return;
+  const int c = (int)blockIdx.y * 64 + (threadIdx.x & 63), rl = threadIdx.x >> 6;
+  double v = 0.0;
+  if (c < m)
+    for (int64_t j = (int64_t)blockIdx.x * 4 + rl; j < rows; j += (int64_t)gridDim.x * 4) v = fmax(v, fabs(X[j * ldx + c]));
+  __shared__ double sv[4][64];
+  const int cl = threadIdx.x & 63;
+  sv[rl][cl] = v;
+  __syncthreads();
+  if (rl == 0 && c < m) {
+    v = fmax(fmax(sv[0][cl], sv[1][cl]), fmax(sv[2][cl], sv[3][cl]));
+    atomicMax(&cm[c], (unsigned long long)__double_as_longlong(v));
+  }
+}
+
+// Q[i][c] = RN(lambda Xd[row0+i][c] + sum_j A[i][j] X[j][c]), one compensated sum per entry
+// (Xd = X for the operator; Xd = R for the last pass of the factored P, Q (M (Q^T R)) +
+// a^-1/2 R).  With rmax / cmax (row maxima of A, column maxima of X) each accumulator
+// carries the power-of-two offset C >= 2 kdim rmax_i cmax_c and every step is TwoProd +
+// Fast2Sum (dot2_step_off, 7 fp64 ops instead of Dot2's 10; exact error capture, see
+// symv.cu); the offset is removed exactly before lambda Xd is added.
+template <bool OFF>
 __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict__ A, int64_t lda, int64_t rows,
                                                         int64_t kdim, const double *__restrict__ X, int64_t ldx,
                                                         int64_t m, double *__restrict__ Q, int64_t ldq,
                                                         double lambda, int64_t row0,
                                                         const int32_t *__restrict__ all_done,
-                                                        const double *__restrict__ Xd) {
+                                                        const double *__restrict__ Xd,
+                                                        const double *__restrict__ rmax,
+                                                        const double *__restrict__ cmax) {
   if (all_done && *(volatile const int32_t *)all_done) return;
   __shared__ double As[kBR][kBK + 1];
   __shared__ __align__(16) double Xs[kBK][kBM];
@@ -40,19 +80,26 @@ __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict
   const int tc = (tid & 15) * 4;       // 4 columns
   const int64_t R0 = (int64_t)blockIdx.x * kBR;
   const int64_t C0 = (int64_t)blockIdx.y * kBM;
-  dd_pair acc[2][4];
+  // offset accumulators cover kOffChunk products each and are folded into the Dot2 pair
+  // `tot` at chunk ends: the offset-sum error grows with the products per accumulator
+  // (~k^2 u^2 max|a x|), which at k = 512 stays far below ulp(q) as in symv.cu
+  constexpr int kOffChunk = 512;
+  constexpr bool off = OFF;
+  double ra[2] = {0.0, 0.0}, cb[4] = {0.0, 0.0, 0.0, 0.0};
+  if (off) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a) ra[a] = R0 + tr + a < rows ? rmax[R0 + tr + a] * (2.0 * (double)kOffChunk) : 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) cb[b] = C0 + tc + b < m ? cmax[C0 + tc + b] : 0.0;
+  }
+  dd_pair acc[2][4], tot[2][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = dd_pair{0.0, 0.0};
-  if (lambda != 0.0) {
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (R0 + tr + a < rows && C0 + tc + b < m)
-          dot2_step(acc[a][b], lambda, Xd[(row0 + R0 + tr + a) * ldx + C0 + tc + b]);
-  }
+    for (int b = 0; b < 4; ++b) {
+      acc[a][b] = dd_pair{off ? pow2_above(ra[a] * cb[b]) : 0.0, 0.0};
+      tot[a][b] = dd_pair{0.0, 0.0};
+    }
   for (int64_t k0 = 0; k0 < kdim; k0 += kBK) {
     __syncthreads();
     for (int e = tid; e < kBR * kBK; e += 256) {
@@ -64,26 +111,62 @@ __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict
       Xs[r][c] = (k0 + r < kdim && C0 + c < m) ? X[(k0 + r) * ldx + C0 + c] : 0.0;
     }
     __syncthreads();
+    if constexpr (OFF) {
+      if (k0 > 0 && k0 % kOffChunk == 0) {  // fold the finished chunk (offset removed exactly)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const double cab = pow2_above(ra[a] * cb[b]);
+            pair_add(tot[a][b], dd_pair{__dsub_rn(acc[a][b].s, cab), acc[a][b].c});
+            acc[a][b] = dd_pair{cab, 0.0};
+          }
+      }
 #pragma unroll 4
-    for (int j = 0; j < kBK; ++j) {
-      const double a0 = As[tr][j], a1 = As[tr + 1][j];
-      const double2 x01 = *reinterpret_cast<const double2 *>(&Xs[j][tc]);
-      const double2 x23 = *reinterpret_cast<const double2 *>(&Xs[j][tc + 2]);
-      dot2_step(acc[0][0], a0, x01.x);
-      dot2_step(acc[0][1], a0, x01.y);
-      dot2_step(acc[0][2], a0, x23.x);
-      dot2_step(acc[0][3], a0, x23.y);
-      dot2_step(acc[1][0], a1, x01.x);
-      dot2_step(acc[1][1], a1, x01.y);
-      dot2_step(acc[1][2], a1, x23.x);
-      dot2_step(acc[1][3], a1, x23.y);
+      for (int j = 0; j < kBK; ++j) {
+        const double a0 = As[tr][j], a1 = As[tr + 1][j];
+        const double2 x01 = *reinterpret_cast<const double2 *>(&Xs[j][tc]);
+        const double2 x23 = *reinterpret_cast<const double2 *>(&Xs[j][tc + 2]);
+        dot2_step_off(acc[0][0], a0, x01.x);
+        dot2_step_off(acc[0][1], a0, x01.y);
+        dot2_step_off(acc[0][2], a0, x23.x);
+        dot2_step_off(acc[0][3], a0, x23.y);
+        dot2_step_off(acc[1][0], a1, x01.x);
+        dot2_step_off(acc[1][1], a1, x01.y);
+        dot2_step_off(acc[1][2], a1, x23.x);
+        dot2_step_off(acc[1][3], a1, x23.y);
+      }
+    } else {
+#pragma unroll 4
+      for (int j = 0; j < kBK; ++j) {
+        const double a0 = As[tr][j], a1 = As[tr + 1][j];
+        const double2 x01 = *reinterpret_cast<const double2 *>(&Xs[j][tc]);
+        const double2 x23 = *reinterpret_cast<const double2 *>(&Xs[j][tc + 2]);
+        dot2_step(acc[0][0], a0, x01.x);
+        dot2_step(acc[0][1], a0, x01.y);
+        dot2_step(acc[0][2], a0, x23.x);
+        dot2_step(acc[0][3], a0, x23.y);
+        dot2_step(acc[1][0], a1, x01.x);
+        dot2_step(acc[1][1], a1, x01.y);
+        dot2_step(acc[1][2], a1, x23.x);
+        dot2_step(acc[1][3], a1, x23.y);
+      }
     }
   }
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b)
-      if (R0 + tr + a < rows && C0 + tc + b < m) Q[(R0 + tr + a) * ldq + C0 + tc + b] = pair_value(acc[a][b]);
+      if (R0 + tr + a < rows && C0 + tc + b < m) {
+        dd_pair v = acc[a][b];
+        if constexpr (OFF) {
+          v.s = __dsub_rn(v.s, pow2_above(ra[a] * cb[b]));  // exact (Sterbenz)
+          pair_add(tot[a][b], v);
+          v = tot[a][b];
+        }
+        if (lambda != 0.0) dot2_step(v, lambda, Xd[(row0 + R0 + tr + a) * ldx + C0 + tc + b]);
+        Q[(R0 + tr + a) * ldq + C0 + tc + b] = pair_value(v);
+      }
 }
 
 enum ColMode { kColInit = 0, kColDelta = 1, kColUpdate = 2, kColBeta = 3, kColTrue = 4 };
@@ -353,13 +436,61 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     ctx->stats.kernel_launches++;
   };
   const bool exact = ctx->mode == LAKER_MODE_EXACT;
+  // EXACT: row maxima of every matrix the solve multiplies (once) and a column-maxima
+  // buffer for the right-hand-side blocks (per product): the offsets of gemm_dot2_kernel
+  const char *offenv = std::getenv("LAKER_BLOCK_OFFSET");
+  const bool use_off = exact && !(offenv && offenv[0] == '0');
+  double *rmK = nullptr, *rmP = nullptr, *rmQt = nullptr, *rmM = nullptr, *rmQr = nullptr;
+  unsigned long long *cmx = nullptr;
+  if (use_off) {
+    const int64_t nrp = fac ? ctx->f_nrp : 0;
+    LAKER_CUDA(ctx, cudaMallocAsync(&rmK, (size_t)(3 * n + 2 * nrp) * sizeof(double) + 256 * sizeof(double), s));
+    rmP = rmK + n;
+    rmQt = rmP + n;
+    rmM = rmQt + nrp;
+    rmQr = rmM + nrp;
+    cmx = reinterpret_cast<unsigned long long *>(rmQr + n);
+    auto rowmax = [&](const double *A, int64_t rows, int64_t cols, int64_t lda, double *out) {
+      rowmax_abs_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(A, rows, cols, lda, out);
+      ctx->stats.kernel_launches++;
+    };
+    rowmax(ctx->K, n, n, ld, rmK);
+    if (dense && !fac) rowmax(ctx->P, n, n, ld, rmP);
+    if (fac) {
+      rowmax(ctx->Qt, nrp, n, ld, rmQt);
+      rowmax(ctx->Mf, nrp, nrp, ctx->f_ldq, rmM);
+      rowmax(ctx->Qr, n, nrp, ctx->f_ldq, rmQr);
+    }
+  }
+  auto rowmax_of = [&](const double *Amat) -> const double * {
+    if (!use_off) return nullptr;
+    if (Amat == ctx->K) return rmK;
+    if (Amat == ctx->P) return rmP;
+    if (fac && Amat == ctx->Qt) return rmQt;
+    if (fac && Amat == ctx->Mf) return rmM;
+    if (fac && Amat == ctx->Qr) return rmQr;
+    return nullptr;
+  };
   // Out (rows x m) = A (rows x kdim, lda) X + lam Xd
   auto gemm = [&](const double *Amat, int64_t lda, int64_t rows, int64_t kdim, double lam, const double *X,
                   const double *Xd, double *Out, bool gated) {
     if (exact) {
       dim3 grid((unsigned)((rows + kBR - 1) / kBR), (unsigned)((m + kBM - 1) / kBM));
-      gemm_dot2_kernel<<<grid, 256, 0, s>>>(Amat, lda, rows, kdim, X, mp, m, Out, mp, lam, 0,
-                                            gated ? all_done : nullptr, Xd);
+      const double *rmx = rowmax_of(Amat);
+      if (rmx) {
+        cudaMemsetAsync(cmx, 0, 256 * sizeof(unsigned long long), s);
+        colmax_abs_kernel<<<dim3((unsigned)std::min<int64_t>(2 * ctx->num_sms, (kdim + 3) / 4),
+                                 (unsigned)((m + 63) / 64)), 256, 0, s>>>(X, kdim, m, mp, cmx,
+                                                                          gated ? all_done : nullptr);
+        ctx->stats.kernel_launches++;
+      }
+      if (rmx)
+        gemm_dot2_kernel<true><<<grid, 256, 0, s>>>(Amat, lda, rows, kdim, X, mp, m, Out, mp, lam, 0,
+                                                    gated ? all_done : nullptr, Xd, rmx,
+                                                    reinterpret_cast<const double *>(cmx));
+      else
+        gemm_dot2_kernel<false><<<grid, 256, 0, s>>>(Amat, lda, rows, kdim, X, mp, m, Out, mp, lam, 0,
+                                                     gated ? all_done : nullptr, Xd, nullptr, nullptr);
     } else {
       GemmArgs g{};
       g.M = rows; g.N = mp; g.K = kdim; g.A = Amat; g.lda = lda; g.B = X; g.ldb = mp; g.C = Out; g.ldc = mp;
@@ -492,6 +623,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   cudaGraphDestroy(graph);
   cudaFreeAsync(base, s);
   if (zb) cudaFreeAsync(zb, s);
+  if (rmK) cudaFreeAsync(rmK, s);
   if (part) cudaFreeAsync(part, s);
   oz_slices_free(sK, s);
   oz_slices_free(sQt, s);

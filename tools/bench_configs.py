@@ -148,6 +148,8 @@ if __name__ == "__main__":
             run_std(int(w[1]))
         elif w == "C4":
             run_c4()
+        elif w == "C4E":
+            run_c4(modes=("exact",))
         elif w == "C5":
             run_c5()
         elif w == "C5L":
