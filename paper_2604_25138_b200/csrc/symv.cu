@@ -76,6 +76,11 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
 }
 
+// ROWOFF: the row accumulators carry offsets (at most kMaxOffTiles products each, n <=
+// 16384); otherwise they are plain Dot2 pairs (the offset-sum error grows with the
+// products per accumulator) and only the 8-product column chains use offsets
+constexpr int kMaxOffTiles = 512;
+template <bool ROWOFF>
 __global__ void __launch_bounds__(kSymThreads, 1)
     symv_dot2_kernel(const __grid_constant__ CUtensorMap tm, const SymvArgs a) {
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 #pragma unroll
     for (int k = 0; k < kRPT; ++k) {
       dd_pair v = acc[k];
-      v.s = __dsub_rn(v.s, pow2_above(rmr[k] * xm * mrow));  // exact: v.s in [C/2, 3C/2]
+      if (ROWOFF) v.s = __dsub_rn(v.s, pow2_above(rmr[k] * xm * mrow));  // exact: v.s in [C/2, 3C/2]
       v = warp_reduce_pair(v);
       v.s = __shfl_sync(0xffffffffu, v.s, 0);
       v.c = __shfl_sync(0xffffffffu, v.c, 0);
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{pow2_above(rmr[k] * xm * mrow), 0.0};
+      for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{ROWOFF ? pow2_above(rmr[k] * xm * mrow) : 0.0, 0.0};
     }
     const int I = curI;
     const int jt = kTPD * I + (int)(t - rbeg);
@@ -247,7 +252,12 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     dd_pair cacc = {ccol, 0.0};
     if (diag) {
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) dot2_step_off(acc[k], tp[k * kSC], xc);
+      for (int k = 0; k < kRPT; ++k) {
+        if (ROWOFF)
+          dot2_step_off(acc[k], tp[k * kSC], xc);
+        else
+          dot2_step(acc[k], tp[k * kSC], xc);
+      }
     } else {
       // phased so that the 8 independent row steps (and the products of the column
       // chain) are in flight together: loads, TwoProds, then the Fast2Sum chains
@@ -259,7 +269,10 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 #pragma unroll
       for (int k = 0; k < kRPT; ++k) {
         double s, se;
-        fast_two_sum(acc[k].s, p[k], s, se);
+        if (ROWOFF)
+          fast_two_sum(acc[k].s, p[k], s, se);
+        else
+          two_sum(acc[k].s, p[k], s, se);
         acc[k].s = s;
         acc[k].c = __dadd_rn(acc[k].c, __dadd_rn(pe[k], se));
       }
@@ -494,7 +507,8 @@ struct SymvPlan {
 size_t symv_smem_bytes() { return kSymSmem; }
 
 void symv_init() {
-  cudaFuncSetAttribute(symv_dot2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
+  cudaFuncSetAttribute(symv_dot2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
+  cudaFuncSetAttribute(symv_dot2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
 }
 
 void symv_free(SymvPlan *&p) {
@@ -639,7 +653,10 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     a.xparts = p->xparts;
     a.nxparts = kXParts;
   }
-  symv_dot2_kernel<<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
+  if (p->nct <= kMaxOffTiles)
+    symv_dot2_kernel<true><<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
+  else
+    symv_dot2_kernel<false><<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
   symv_finalize_kernel<kSR><<<p->fin_grid, kFinThreads, 0, s>>>(a);
 }
 

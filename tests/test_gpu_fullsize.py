@@ -67,3 +67,21 @@ def test_c4_block_exact_products_fullsize(L, monkeypatch):
     c.close()
     _bitwise(a_off, a_d2, "block alpha after 6 iterations: offset-Fast2Sum vs Dot2 products")
     assert [r["rel_residual"] for r in r_off] == [r["rel_residual"] for r in r_d2]
+
+
+def test_symmetric_apply_beyond_offset_range(L, monkeypatch):
+    """n = 20000 (> 512 column tiles per block-row): the row accumulators fall back to
+    plain Dot2 (the column chains keep their offsets); still bitwise the full-row GEMV."""
+    P = make_problem(3, n=20000)
+    rng = np.random.default_rng(5)
+    xs = [rng.standard_normal(P.n), np.where(rng.random(P.n) < 0.5, -1.0, 1.0) * np.exp(rng.uniform(-8, 8, P.n))]
+    c = L.Context(0)
+    c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    assert c.stats()["symmetric_k"] == 1
+    q_sym = [c.apply_operator(x) for x in xs]
+    monkeypatch.setenv("LAKER_SYMV", "0")
+    c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    q_full = [c.apply_operator(x) for x in xs]
+    c.close()
+    for k, (a, b) in enumerate(zip(q_sym, q_full)):
+        _bitwise(a, b, f"n=20000 symmetric vs full-row apply, x #{k}")
