@@ -2,10 +2,12 @@
 // Alg. 1 l.3) and the Jacobi diagonal
 // d_i = 1 / (lambda + K_ii) (row a2).
 //
-// EXACT mode: each entry is RN(exp_cr(RN(scale * Dot2_k(e_ik, e_jk)))) with the
-// Dot2 taken sequentially over k -- the same operation sequence as the
-// oracle's, so entries are bitwise equal by construction (and exp_cr is
-// correctly rounded, exp_cr.cuh).  64 x 64 tiles, 256 threads, 4 x 4 entries
+// EXACT mode: each entry is RN(exp_cr(RN(scale * <e_i, e_j>))) with the dot product
+// correctly rounded in practice -- a compensated sum over k whose accumulator carries
+// the power-of-two offset C_ij >= 2 d max_k|e_ik| max_k|e_jk| (emax), so each step is
+// TwoProd + Fast2Sum (dot2_step_off: exact error capture, 7 fp64 ops instead of Dot2's
+// 10), the offset removed exactly before rounding -- bitwise the oracle's sequential
+// Dot2 (and exp_cr is correctly rounded, exp_cr.cuh).  64 x 64 tiles, 256 threads, 4 x 4 entries
 // per thread, E tiles staged through shared memory in 32-wide k chunks.
 // Single-rank: only tiles J >= I are computed and mirrored through a shared-
 // memory transpose, so K is bitwise symmetric and half the exps are saved.
@@ -31,7 +33,8 @@ __global__ void __launch_bounds__(256) assemble_exact_kernel(const double *__res
                                                              int d, double scale, int64_t r0,
                                                              int64_t r1, double *__restrict__ K,
                                                              int64_t ld, int sym,
-                                                             unsigned long long *flags) {
+                                                             unsigned long long *flags,
+                                                             const double *__restrict__ emax) {
   __shared__ double buf[2 * kT * (kKC + 1)];
   double(*Ei)[kKC + 1] = reinterpret_cast<double(*)[kKC + 1]>(buf);
   double(*Ej)[kKC + 1] = reinterpret_cast<double(*)[kKC + 1]>(buf + kT * (kKC + 1));
@@ -42,11 +45,18 @@ __global__ void __launch_bounds__(256) assemble_exact_kernel(const double *__res
   const int64_t rowEnd = sym ? n : r1;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
 
+  double ei[4], ej[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gi = I0 + ty + 16 * i, gj = J0 + tx + 16 * i;
+    ei[i] = gi < rowEnd ? emax[gi] * (2.0 * d) : 0.0;
+    ej[i] = gj < n ? emax[gj] : 0.0;
+  }
   dd_pair acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = dd_pair{0.0, 0.0};
+    for (int j = 0; j < 4; ++j) acc[i][j] = dd_pair{pow2_above(ei[i] * ej[j]), 0.0};
 
   for (int k0 = 0; k0 < d; k0 += kKC) {
     const int kc = min(kKC, d - k0);
@@ -66,7 +76,7 @@ __global__ void __launch_bounds__(256) assemble_exact_kernel(const double *__res
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dot2_step(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < 4; ++j) dot2_step_off(acc[i][j], av[i], bv[j]);
     }
     __syncthreads();
   }
@@ -76,7 +86,11 @@ __global__ void __launch_bounds__(256) assemble_exact_kernel(const double *__res
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[i][j] = exp_cr(__dmul_rn(scale, pair_value(acc[i][j])), inc, ovf);
+    for (int j = 0; j < 4; ++j) {
+      dd_pair a = acc[i][j];
+      a.s = __dsub_rn(a.s, pow2_above(ei[i] * ej[j]));  // exact (Sterbenz)
+      v[i][j] = exp_cr(__dmul_rn(scale, pair_value(a)), inc, ovf);
+    }
   flag_add(flags, inc, ovf);
 
   const int64_t rowBase = sym ? 0 : r0;
@@ -121,17 +135,30 @@ __global__ void jacobi_diag_kernel(const double *__restrict__ E, int64_t n, int 
 }  // namespace
 
 void launch_assemble_exact_sym(const double *E, int64_t n, int32_t d, double scale, double *K,
-                               int64_t ld, unsigned long long *flags, cudaStream_t s) {
+                               int64_t ld, unsigned long long *flags, const double *emax, cudaStream_t s) {
   const unsigned nt = (unsigned)((n + kT - 1) / kT);
-  assemble_exact_kernel<<<dim3(nt, nt), 256, 0, s>>>(E, n, d, scale, 0, n, K, ld, 1, flags);
+  assemble_exact_kernel<<<dim3(nt, nt), 256, 0, s>>>(E, n, d, scale, 0, n, K, ld, 1, flags, emax);
 }
 
 void launch_assemble_exact_rows(const double *E, int64_t n, int32_t d, double scale, int64_t r0,
                                 int64_t r1, double *K, int64_t ld, unsigned long long *flags,
-                                cudaStream_t s) {
+                                const double *emax, cudaStream_t s) {
   const unsigned ntc = (unsigned)((n + kT - 1) / kT);
   const unsigned ntr = (unsigned)((r1 - r0 + kT - 1) / kT);
-  assemble_exact_kernel<<<dim3(ntc, ntr), 256, 0, s>>>(E, n, d, scale, r0, r1, K, ld, 0, flags);
+  assemble_exact_kernel<<<dim3(ntc, ntr), 256, 0, s>>>(E, n, d, scale, r0, r1, K, ld, 0, flags, emax);
+}
+
+// out[i] = max_k |X_ik| (the offsets of the EXACT entry kernels)
+__global__ void rowabsmax_kernel(const double *__restrict__ X, int64_t rows, int d, double *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double m = 0.0;
+  for (int k = 0; k < d; ++k) m = fmax(m, fabs(X[i * d + k]));
+  out[i] = m;
+}
+
+void launch_rowabsmax(const double *X, int64_t rows, int32_t d, double *out, cudaStream_t s) {
+  if (rows > 0) rowabsmax_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(X, rows, d, out);
 }
 
 void launch_jacobi_diag(const double *E, int64_t n, int32_t d, double scale, double lambda,

@@ -541,7 +541,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     for (int64_t c0 = cb; c0 < ce; c0 += cw) {
       const int64_t c1 = std::min(ce, c0 + cw);
       if (ctx->mode == LAKER_MODE_EXACT)
-        launch_assemble_exact_rows(ctx->E, n, ctx->d, ctx->scale, c0, c1, Kc, ld, ctx->flags, s);
+        launch_assemble_exact_rows(ctx->E, n, ctx->d, ctx->scale, c0, c1, Kc, ld, ctx->flags, ctx->emax, s);
       else
         launch_assemble_fast(ctx->E, n, ctx->d, ctx->scale, c0, c1, Kc, ld, ctx->flags, s);
       g.N = c1 - c0; g.B = Kc; g.C = C + (c0 - cb); g.Cin = Zt + c0;

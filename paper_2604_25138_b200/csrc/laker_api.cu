@@ -255,6 +255,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   laker::symv_free(ctx->otf_sym);
   laker::symv_free(ctx->symv_m);
   if (ctx->cf) cudaFree(ctx->cf);
+  if (ctx->emax) cudaFree(ctx->emax);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -310,6 +311,14 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   else
     LAKER_CUDA(ctx, cudaMemcpyAsync(ctx->E, E, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
   LAKER_CUDA(ctx, cudaMemsetAsync(ctx->flags, 0, 2 * sizeof(unsigned long long), s));
+  if (ctx->emax_len != n) {
+    if (ctx->emax) cudaFree(ctx->emax);
+    ctx->emax = nullptr;
+    ctx->emax_len = 0;
+    LAKER_CUDA(ctx, cudaMalloc(&ctx->emax, (size_t)n * sizeof(double)));
+    ctx->emax_len = n;
+  }
+  laker::launch_rowabsmax(ctx->E, n, d, ctx->emax, s);
   // digit slices of E for the tcgen05 QK^T paths (FAST assembly, on-the-fly operator,
   // predict); those paths use a branch-free exp, so they are enabled only when
   // scale max ||e_i||^2 (a Cauchy-Schwarz bound of every argument) cannot overflow
@@ -344,9 +353,10 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
     const bool whole = (rows == n);
     if (mode == LAKER_MODE_EXACT) {
       if (whole)
-        laker::launch_assemble_exact_sym(ctx->E, n, d, scale, ctx->K, ctx->ld, ctx->flags, s);
+        laker::launch_assemble_exact_sym(ctx->E, n, d, scale, ctx->K, ctx->ld, ctx->flags, ctx->emax, s);
       else
-        laker::launch_assemble_exact_rows(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags, s);
+        laker::launch_assemble_exact_rows(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags,
+                                          ctx->emax, s);
     } else if (ctx->ozE_valid && std::getenv("LAKER_ASSEMBLE_TC") && std::getenv("LAKER_ASSEMBLE_TC")[0] == '1') {
       // QK^T on tcgen05 with the fused exp epilogue (otf_tc.cu).  Opt-in: it computes
       // every tile (no mirroring) and measured 3.8 ms at C3 vs 1.24 ms for the DMMA

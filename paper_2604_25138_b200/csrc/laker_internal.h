@@ -101,6 +101,9 @@ struct laker_ctx_s {
   // per-column factors {scale 2^(e_j), w_j} of the FAST tcgen05 on-the-fly kernels (otf_tc2.cu)
   double2 *cf = nullptr;
   int64_t cf_len = 0;
+  // max_k |e_ik| per row of E (offsets of the EXACT entry kernels), set at assembly
+  double *emax = nullptr;
+  int64_t emax_len = 0;
   bool k_sym = false, p_sym = false;
   // factored P: the middle factor M (N_r x N_r) applied by the symmetric GEMV when it is
   // bitwise symmetric -- half of M's bytes, which then stay resident in L2 (fit.cu)
@@ -205,11 +208,13 @@ size_t symv_smem_bytes();
 laker_status refresh_symmetry(laker_ctx ctx, int which);
 
 // -------------------------------------------------------------- assemble.cu
+// emax: max_k |e_ik| per row of E (launch_rowabsmax), the offsets of the compensated dots
 void launch_assemble_exact_sym(const double *E, int64_t n, int32_t d, double scale, double *K,
-                               int64_t ld, unsigned long long *flags, cudaStream_t s);
+                               int64_t ld, unsigned long long *flags, const double *emax, cudaStream_t s);
 void launch_assemble_exact_rows(const double *E, int64_t n, int32_t d, double scale, int64_t r0,
                                 int64_t r1, double *K, int64_t ld, unsigned long long *flags,
-                                cudaStream_t s);
+                                const double *emax, cudaStream_t s);
+void launch_rowabsmax(const double *X, int64_t rows, int32_t d, double *out, cudaStream_t s);
 void launch_assemble_fast(const double *E, int64_t n, int32_t d, double scale, int64_t r0,
                           int64_t r1, double *K, int64_t ld, unsigned long long *flags,
                           cudaStream_t s);
@@ -221,7 +226,7 @@ void launch_jacobi_diag(const double *E, int64_t n, int32_t d, double scale, dou
 void launch_kernel_matvec_exact(const double *Eq, int64_t m, const double *E, int64_t n, int32_t d,
                                 double scale, const double *w, double lambda, const double *xdiag,
                                 double *out, unsigned long long *flags, const int32_t *done,
-                                cudaStream_t s);
+                                cudaStream_t s, const double *emq, const double *emE);
 
 // -------------------------------------------------------------- otf_fast.cu
 // FAST (DMMA + CUDA exp) version of launch_kernel_matvec_exact; d <= 128.
@@ -238,11 +243,12 @@ cudaError_t launch_kernel_matvec_ctx(laker_ctx ctx, int mode, const double *Eq, 
 // mode dispatch for the on-the-fly matvec (EXACT: correctly rounded entries + Dot2)
 inline void launch_kernel_matvec(int mode, const double *Eq, int64_t m, const double *E, int64_t n, int32_t d,
                                  double scale, const double *w, double lambda, const double *xdiag, double *out,
-                                 unsigned long long *flags, const int32_t *done, cudaStream_t s) {
+                                 unsigned long long *flags, const int32_t *done, cudaStream_t s,
+                                 const double *emq, const double *emE) {
   if (mode == LAKER_MODE_FAST && d <= 128)
     launch_kernel_matvec_fast(Eq, m, E, n, d, scale, w, lambda, xdiag, out, done, s);
   else
-    launch_kernel_matvec_exact(Eq, m, E, n, d, scale, w, lambda, xdiag, out, flags, done, s);
+    launch_kernel_matvec_exact(Eq, m, E, n, d, scale, w, lambda, xdiag, out, flags, done, s, emq, emE);
 }
 
 // ----------------------------------------------------------------- dgemm.cu

@@ -36,6 +36,7 @@ struct OtfSymArgs {
   int d, ldE;  // smem row stride (d + 1)
   double scale;
   unsigned long long *flags;
+  const double *emax;  // max_k |e_ik| per row (offsets of the compensated dots, assemble.cu)
 };
 
 __global__ void __launch_bounds__(kXThreads) otf_sym_exact_kernel(const OtfSymArgs f) {
@@ -98,11 +99,17 @@ __global__ void __launch_bounds__(kXThreads) otf_sym_exact_kernel(const OtfSymAr
     __syncthreads();  // previous tile's EJ / cred consumers done
     load_rows(EJ, wJ, J);
     __syncthreads();
+    double ei[4], ej[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ei[i] = (int64_t)I * kXT + ty + 16 * i < n ? f.emax[(int64_t)I * kXT + ty + 16 * i] * (2.0 * d) : 0.0;
+      ej[i] = (int64_t)J * kXT + tx + 16 * i < n ? f.emax[(int64_t)J * kXT + tx + 16 * i] : 0.0;
+    }
     dd_pair acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = dd_pair{0.0, 0.0};
+      for (int j = 0; j < 4; ++j) acc[i][j] = dd_pair{pow2_above(ei[i] * ej[j]), 0.0};
     for (int k = 0; k < d; ++k) {
       double av[4], bv[4];
 #pragma unroll
@@ -112,7 +119,7 @@ __global__ void __launch_bounds__(kXThreads) otf_sym_exact_kernel(const OtfSymAr
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dot2_step(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < 4; ++j) dot2_step_off(acc[i][j], av[i], bv[j]);
     }
     dd_pair col[4];
 #pragma unroll
@@ -126,7 +133,9 @@ __global__ void __launch_bounds__(kXThreads) otf_sym_exact_kernel(const OtfSymAr
       for (int i = 0; i < 4; ++i) {
         const bool rok = ib + ty + 16 * i < n;
         if (!(rok && cok)) continue;
-        const double kv = exp_cr(__dmul_rn(f.scale, pair_value(acc[i][j])), inc, ovf);
+        dd_pair ac = acc[i][j];
+        ac.s = __dsub_rn(ac.s, pow2_above(ei[i] * ej[j]));  // exact (Sterbenz)
+        const double kv = exp_cr(__dmul_rn(f.scale, pair_value(ac)), inc, ovf);
         dot2_step(row[i], kv, wj);
         if (!diag) dot2_step(col[j], kv, wI[ty + 16 * i]);
       }
@@ -216,6 +225,7 @@ bool launch_operator_otf_sym(laker_ctx ctx, const double *p, double *q, PcgState
     f.ldE = ctx->d + 1;
     f.scale = ctx->scale;
     f.flags = ctx->flags;
+    f.emax = ctx->emax;
     otf_sym_exact_kernel<<<tri_grid(ctx->otf_sym), kXThreads, exact_smem(ctx->d), s>>>(f);
   }
   launch_tri_finalize(ctx->otf_sym, t, s);

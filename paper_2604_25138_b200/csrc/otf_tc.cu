@@ -363,7 +363,18 @@ cudaError_t launch_kernel_matvec_ctx(laker_ctx ctx, int mode, const double *Eq, 
     oz_slices_free(q, s);
     return e;
   }
-  launch_kernel_matvec(mode, Eq, m, ctx->E, ctx->n, ctx->d, ctx->scale, w, lambda, xdiag, out, ctx->flags, done, s);
+  if (mode != LAKER_MODE_FAST && !Eq_is_E) {  // EXACT predict: the query rows' maxima
+    double *emq = nullptr;
+    cudaError_t e = cudaMallocAsync(&emq, (size_t)std::max<int64_t>(m, 1) * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    launch_rowabsmax(Eq, m, ctx->d, emq, s);
+    launch_kernel_matvec(mode, Eq, m, ctx->E, ctx->n, ctx->d, ctx->scale, w, lambda, xdiag, out, ctx->flags, done, s,
+                         emq, ctx->emax);
+    cudaFreeAsync(emq, s);
+    return cudaGetLastError();
+  }
+  launch_kernel_matvec(mode, Eq, m, ctx->E, ctx->n, ctx->d, ctx->scale, w, lambda, xdiag, out, ctx->flags, done, s,
+                       ctx->emax + (Eq_is_E ? eq_row0 : 0), ctx->emax);
   return cudaGetLastError();
 }
 

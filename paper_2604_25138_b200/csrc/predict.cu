@@ -4,8 +4,8 @@
 // and, with Eq = E and the lambda term, the matrix-free operator apply
 // (lambda I + K) p of P:517-519 (row a11).
 //
-// EXACT: every entry exactly as in assembly (sequential Dot2 over k, then the
-// correctly rounded exp), accumulated as Dot2 pairs; the pairs of the 16
+// EXACT: every entry exactly as in assembly (the compensated dot over k with the
+// emax offsets of assemble.cu, then the correctly rounded exp), accumulated as Dot2 pairs; the pairs of the 16
 // threads sharing a query row are combined in a fixed butterfly order.  The
 // result equals the oracle's Dot2 row sum in practice (R16: same-alpha map
 // parity), and the on-the-fly apply equals the materialized one (T19).
@@ -22,7 +22,8 @@ constexpr int kKC = 32;
 __global__ void __launch_bounds__(256) kernel_matvec_exact_kernel(
     const double *__restrict__ Eq, int64_t m, const double *__restrict__ E, int64_t n, int d,
     double scale, const double *__restrict__ w, double lambda, const double *__restrict__ xdiag,
-    double *__restrict__ out, unsigned long long *flags, const int32_t *done) {
+    double *__restrict__ out, unsigned long long *flags, const int32_t *done,
+    const double *__restrict__ emq, const double *__restrict__ emE) {
   if (done != nullptr && *(volatile const int32_t *)done) return;
   __shared__ double Ea[kT][kKC + 1];
   __shared__ double Eb[kT][kKC + 1];
@@ -48,12 +49,19 @@ __global__ void __launch_bounds__(256) kernel_matvec_exact_kernel(
       Ea[r][c] = (A0 + r < m && c < d) ? Eq[(A0 + r) * d + c] : 0.0;
     }
   }
+  double eq[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) eq[i] = A0 + ty + 16 * i < m ? emq[A0 + ty + 16 * i] * (2.0 * d) : 0.0;
   for (int64_t J0 = 0; J0 < n; J0 += kT) {
+    // the compensated dots carry offsets C >= 2 d max|eq_a| max|e_j| (dot2_step_off, assemble.cu)
+    double ee[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ee[j] = J0 + tx + 16 * j < n ? emE[J0 + tx + 16 * j] : 0.0;
     dd_pair acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = dd_pair{0.0, 0.0};
+      for (int j = 0; j < 4; ++j) acc[i][j] = dd_pair{pow2_above(eq[i] * ee[j]), 0.0};
     for (int k0 = 0; k0 < d; k0 += kKC) {
       const int kc = min(kKC, d - k0);
       __syncthreads();
@@ -73,7 +81,7 @@ __global__ void __launch_bounds__(256) kernel_matvec_exact_kernel(
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dot2_step(acc[i][j], av[i], bv[j]);
+          for (int j = 0; j < 4; ++j) dot2_step_off(acc[i][j], av[i], bv[j]);
       }
     }
 #pragma unroll
@@ -82,7 +90,9 @@ __global__ void __launch_bounds__(256) kernel_matvec_exact_kernel(
       const double wj = ws[tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const double kv = exp_cr(__dmul_rn(scale, pair_value(acc[i][j])), inc, ovf);
+        dd_pair a = acc[i][j];
+        a.s = __dsub_rn(a.s, pow2_above(eq[i] * ee[j]));  // exact (Sterbenz)
+        const double kv = exp_cr(__dmul_rn(scale, pair_value(a)), inc, ovf);
         dot2_step(row[i], kv, wj);
       }
     }
@@ -110,10 +120,10 @@ __global__ void __launch_bounds__(256) kernel_matvec_exact_kernel(
 void launch_kernel_matvec_exact(const double *Eq, int64_t m, const double *E, int64_t n, int32_t d,
                                 double scale, const double *w, double lambda, const double *xdiag,
                                 double *out, unsigned long long *flags, const int32_t *done,
-                                cudaStream_t s) {
+                                cudaStream_t s, const double *emq, const double *emE) {
   const unsigned grid = (unsigned)((m + kT - 1) / kT);
   kernel_matvec_exact_kernel<<<grid, 256, 0, s>>>(Eq, m, E, n, d, scale, w, lambda, xdiag, out, flags,
-                                                  done);
+                                                  done, emq, emE);
 }
 
 }  // namespace laker
