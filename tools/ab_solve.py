@@ -21,7 +21,10 @@ c.assemble_kernel(torch.from_numpy(P.E).to(dev), P.scale, P.lam, L.STORE_MATERIA
 c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7)
 y = torch.from_numpy(P.y).to(dev)
 ts, its = [], []
+fit_each = os.environ.get("FIT_EACH", "0") == "1"  # the bench step's order: fit, then solve
 for _ in range(reps + 1):
+    if fit_each:
+        c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7)
     a, r, _ = c.pcg_solve(y, P.tol)
     ts.append(r[0]["seconds"])
     its.append(r[0]["iters"])
