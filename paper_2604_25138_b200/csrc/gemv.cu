@@ -27,6 +27,7 @@
 // fused iteration is bitwise the same recurrence.
 #include "laker_internal.h"
 #include "tma.cuh"
+#include "pdl.cuh"
 
 namespace laker {
 namespace {
@@ -104,6 +105,7 @@ __device__ __forceinline__ void fused_p_epilogue(const GemvArgs &a, double rthet
 
 template <int FUSE>
 __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a) {
+  pdl_prologue();
   using C = Cfg<FUSE>;
   constexpr int ROWS = C::ROWS;
   constexpr int kCPT = C::CPT;
@@ -406,7 +408,7 @@ void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s) {
       gemv_dot2_kernel<FUSE_P><<<g, kThreads, Cfg<FUSE_P>::SMEM, s>>>(a);
       break;
     default:
-      gemv_dot2_kernel<FUSE_NONE><<<g, kThreads, Cfg<FUSE_NONE>::SMEM, s>>>(a);
+      launch_pdl(gemv_dot2_kernel<FUSE_NONE>, dim3(g), dim3(kThreads), Cfg<FUSE_NONE>::SMEM, s, a);
   }
 }
 

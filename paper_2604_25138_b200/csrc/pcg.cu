@@ -261,14 +261,15 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
     launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, vg);
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
-    pcg_update_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.p, w.q, w.alpha, w.r, w.theta, w.st,
-                                                 w.hist, ctx->partials, ctx->counters + kCtrUpdate);
+    launch_pdl(pcg_update_kernel, dim3(vg), dim3(kVecThreads), 0, s, n, pk, (const double *)ctx->Pdiag,
+               (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials,
+               ctx->counters + kCtrUpdate);
     if (dense) {
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
       launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
     }
-    pcg_pupdate_kernel<<<vg, kVecThreads, 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
+    launch_pdl(pcg_pupdate_kernel, dim3(vg), dim3(kVecThreads), 0, s, n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
     ctx->stats.kernel_launches += 2;
   };
 

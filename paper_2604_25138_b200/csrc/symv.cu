@@ -38,6 +38,7 @@
 #include "laker_internal.h"
 #include "tma.cuh"
 #include "tri.cuh"
+#include "pdl.cuh"
 
 namespace laker {
 namespace {
@@ -83,6 +84,7 @@ constexpr int kMaxOffTiles = 512;
 template <bool ROWOFF>
 __global__ void __launch_bounds__(kSymThreads, 1)
     symv_dot2_kernel(const __grid_constant__ CUtensorMap tm, const SymvArgs a) {
+  pdl_prologue();
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   extern __shared__ __align__(128) unsigned char smem[];  // 128 B suffices for unswizzled TMA
   dd_pair *red = reinterpret_cast<dd_pair *>(smem + kSStages * kStageBytes);
@@ -318,6 +320,7 @@ __device__ __forceinline__ dd_pair ldcg_pair(const dd_pair *p) {
 
 template <int BR>
 __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
+  pdl_prologue();
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   constexpr int kRowsPerPass = kFinThreads / kFinSub;
   constexpr int kMaxLd = 8;  // colpart loads batched per thread (nb <= kFinSub * kMaxLd handled per batch)
@@ -439,6 +442,7 @@ __global__ void rowmax_kernel(const double *__restrict__ A, int64_t n, int64_t l
 // parts[b] = max |x_i| over CTA b's grid-stride share
 __global__ void __launch_bounds__(256) absmax_parts_kernel(const double *__restrict__ x, int64_t n, double *parts,
                                                            const PcgState *state) {
+  pdl_prologue();
   if (state != nullptr && *(volatile const int32_t *)&state->done) return;
   __shared__ double sm[8];
   double m = 0.0;
@@ -649,15 +653,16 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     a.xparts = g.xparts;
     a.nxparts = g.nxparts;
   } else {
-    absmax_parts_kernel<<<kXParts, 256, 0, s>>>(g.x, p->n, p->xparts, g.state);
+    launch_pdl(absmax_parts_kernel, dim3(kXParts), dim3(256), 0, s, g.x, (int64_t)p->n, p->xparts,
+               (const PcgState *)g.state);
     a.xparts = p->xparts;
     a.nxparts = kXParts;
   }
   if (p->nct <= kMaxOffTiles)
-    symv_dot2_kernel<true><<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
+    launch_pdl(symv_dot2_kernel<true>, dim3(p->grid), dim3(kSymThreads), kSymSmem, s, p->tm[which], a);
   else
-    symv_dot2_kernel<false><<<p->grid, kSymThreads, kSymSmem, s>>>(p->tm[which], a);
-  symv_finalize_kernel<kSR><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+    launch_pdl(symv_dot2_kernel<false>, dim3(p->grid), dim3(kSymThreads), kSymSmem, s, p->tm[which], a);
+  launch_pdl(symv_finalize_kernel<kSR>, dim3(p->fin_grid), dim3(kFinThreads), 0, s, a);
 }
 
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s) {
