@@ -115,7 +115,7 @@ def _traffic_per_launch(kind: str):
         return None
 
 
-def cpu_baseline_sample(prob, iters: int = 12):
+def cpu_baseline_sample(prob, iters: int = 48):
     """The oracle as it stands on this host's cores: orc_pcg at n = 16384 with a
     dense P (identity stored densely -- the same per-iteration work, two Dot2
     GEMVs over n^2 entries, as the learned P), `iters` iterations; K assembled
