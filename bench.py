@@ -115,6 +115,16 @@ def _traffic_per_launch(kind: str):
         return None
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_sample(prob, iters: int = 48):
     """The oracle as it stands on this host's cores: orc_pcg at n = 16384 with a
     dense P (identity stored densely -- the same per-iteration work, two Dot2
@@ -129,7 +139,7 @@ def cpu_baseline_sample(prob, iters: int = 48):
     _, rep = O.pcg(K, prob.lam, prob.y, O.P_DENSE, Pd, tol=prob.tol, max_iters=iters)
     dt = time.perf_counter() - t0
     del K, Pd
-    return {"value": rep.iters / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+    return {"value": rep.iters / dt, "unit": UNIT, "cores": O.num_threads(), "cpu": cpu_model(), "kind": "oracle",
             "sample": f"oracle orc_pcg at n={prob.n}: {rep.iters} iterations with a dense P "
                       f"(2 Dot2 GEMVs / iteration, as LEARNED); oracle EXACT assembly of K "
                       f"took {t_asm:.1f} s (not in value)",
@@ -162,7 +172,7 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "C3 (BASELINE.json configs[2]) n=16384 d=64 "
                                                         "lambda=1e-4 tol=1e-8, bounded sample"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "cpu": cpu_model(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
