@@ -34,8 +34,9 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *A, int64_t lda,
       d = 1.0;
     }
     const double piv = __dsqrt_rn(d);
+    const double rpiv = __drcp_rn(piv);  // one reciprocal per step: the 63 divisions become products
     // column j below the diagonal (rows j+1+tid), the pivot itself by thread 63
-    if (tid < NB - 1 - j) S[j + 1 + tid][j] = __ddiv_rn(S[j + 1 + tid][j], piv);
+    if (tid < NB - 1 - j) S[j + 1 + tid][j] = __dmul_rn(S[j + 1 + tid][j], rpiv);
     __syncthreads();
     if (tid == NB - 1) S[j][j] = piv;
 #pragma unroll
@@ -68,11 +69,14 @@ constexpr int kPanelRows = kPanelThreads / 4;
 __global__ void __launch_bounds__(kPanelThreads) potrf_panel_kernel(double *A, int64_t lda, int64_t j0, int64_t r0,
                                                                     int64_t nrows) {
   __shared__ double Ls[NB][NB + 1];
+  __shared__ double rd[NB];  // 1 / L_cc: the 64-step chain multiplies instead of dividing
 #pragma unroll 8
   for (int e = threadIdx.x; e < NB * NB; e += kPanelThreads) {
     const int r = e / NB, c = e % NB;
     Ls[r][c] = A[(j0 + r) * lda + j0 + c];
   }
+  __syncthreads();
+  if (threadIdx.x < NB) rd[threadIdx.x] = __drcp_rn(Ls[threadIdx.x][threadIdx.x]);
   __syncthreads();
   const int lane = threadIdx.x & 31, k = lane & 3;
   const int64_t row = r0 + (int64_t)blockIdx.x * kPanelRows + (threadIdx.x >> 2);
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(kPanelThreads) potrf_panel_kernel(double *A, i
   for (int c = 0; c < NB; ++c) {
     double xc = 0.0;
     if (k == (c & 3)) {
-      xc = __ddiv_rn(x[c >> 2], Ls[c][c]);
+      xc = __dmul_rn(x[c >> 2], rd[c]);
       x[c >> 2] = xc;
     }
     xc = __shfl_sync(0xffffffffu, xc, (lane & ~3) | (c & 3));
@@ -118,11 +122,14 @@ constexpr int kTrsmCols = kTrsmThreads / 4;
 __global__ void __launch_bounds__(kTrsmThreads) trsm_diag_kernel(const double *L, int64_t ldl, int64_t b0, double *B,
                                                                  int64_t ldb, int64_t ncols) {
   __shared__ double Ls[NB][NB + 1];
+  __shared__ double rd[NB];  // 1 / L_rr
 #pragma unroll 8
   for (int e = threadIdx.x; e < NB * NB; e += kTrsmThreads) {
     const int r = e / NB, c = e % NB;
     Ls[r][c] = L[(b0 + r) * ldl + b0 + c];
   }
+  __syncthreads();
+  if (threadIdx.x < NB) rd[threadIdx.x] = __drcp_rn(Ls[threadIdx.x][threadIdx.x]);
   __syncthreads();
   const int lane = threadIdx.x & 31, k = lane & 3;
   const int64_t j = (int64_t)blockIdx.x * kTrsmCols + (threadIdx.x >> 2);
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_diag_kernel(const double *L
     // owner k == r % 4 holds row r in x[r / 4]
     double xr = 0.0;
     if (k == (r & 3)) {
-      xr = __ddiv_rn(x[r >> 2], Ls[r][r]);
+      xr = __dmul_rn(x[r >> 2], rd[r]);
       x[r >> 2] = xr;
     }
     xr = __shfl_sync(0xffffffffu, xr, (lane & ~3) | (r & 3));
