@@ -29,6 +29,7 @@
 
 namespace laker {
 bool make_tmap_s8(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
+bool make_tmap_s8_k64(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
 namespace {
 
 // ------------------------------------------------------------------ fused levels
@@ -201,6 +202,197 @@ __global__ void __launch_bounds__(kFThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 256);
 }
 
+// ------------------------------------------------------------------ level groups
+// One CTA = one 128 x 128 output tile; the S digit levels in groups of <= 4 (4 TMEM
+// buffers x 128 columns = 512): for each 64-wide K chunk the S (or fewer) A slices and B
+// slices are loaded ONCE and every slice pair (c, t) whose level c + t falls in the
+// group is issued into that level's buffer.  The fused kernel above streams the pairs
+// level by level -- A_c and B_t are re-read for every level they meet, 4.5x the slice
+// traffic at S = 8, which left it L2-bandwidth bound; here the traffic is 3 chunk
+// loads per (c, t) square cell instead of 2 per pair.  Levels are accumulated in the
+// same order (S-1 .. 0) with the same fp64 operations, so C is bitwise the fused
+// kernel's.  B chunks double-buffered per K chunk, A chunks through a 6-slot ring.
+constexpr int kLM = 128, kLN = 128, kLK = 64;
+constexpr int kLSmax = 8;
+constexpr uint32_t kLChunk = 128 * kLK;  // 8 KiB: 128 rows x 64 int8 (64B-swizzled)
+constexpr int kLARing = 6;
+constexpr size_t kLSmem = 1024 + (2 * kLSmax + kLARing) * kLChunk + 256;
+constexpr int kLThreads = 10 * 32;  // producer, MMA, 8 epilogue warps
+
+__global__ void __launch_bounds__(kLThreads, 1)
+    ozaki_lv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const FusedArgs f) {
+  constexpr int kGroupM = 12;
+  const int64_t tm = (f.M + kLM - 1) / kLM, tn = (f.N + kLN - 1) / kLN;
+  const int64_t pid = blockIdx.x;
+  const int64_t gsize = (int64_t)kGroupM * tn;
+  const int64_t g0 = (pid / gsize) * kGroupM;
+  const int64_t gm = (tm - g0) < kGroupM ? (tm - g0) : kGroupM;
+  const int64_t m0 = (g0 + (pid % gsize) % gm) * kLM, n0 = ((pid % gsize) / gm) * kLN;
+  if (f.tri == 1 && m0 + kLM - 1 + f.tri_off < n0) return;
+  if (f.tri == 2 && m0 + f.tri_off >= n0 + kLN - 1) return;
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t base_s = smem_u32(smem_raw);
+  unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);
+  unsigned char *sB = smem;                                // [2][kLSmax] chunks
+  unsigned char *sA = smem + 2 * kLSmax * kLChunk;         // [kLARing] chunks
+  uint64_t *bfull = reinterpret_cast<uint64_t *>(sA + kLARing * kLChunk);  // [2]
+  uint64_t *bempty = bfull + 2;                                            // [2]
+  uint64_t *afull = bempty + 2;                                            // [kLARing]
+  uint64_t *aempty = afull + kLARing;                                      // [kLARing]
+  uint64_t *tfull = aempty + kLARing;                                      // [4]
+  uint64_t *tempty = tfull + 4;                                            // [4]
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = f.S;
+  const int nkb = (int)(f.Kp / kLK);
+  const int ngrp = (S + 3) / 4;
+
+  if (warp == 0 && lane == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bfull[b], 1);
+      mbar_init(&bempty[b], 1);
+    }
+    for (int r = 0; r < kLARing; ++r) {
+      mbar_init(&afull[r], 1);
+      mbar_init(&aempty[r], 1);
+    }
+    for (int j = 0; j < 4; ++j) {
+      mbar_init(&tfull[j], 1);
+      mbar_init(&tempty[j], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int bcount = 0, aslot = 0, auses = 0;
+      for (int g = 0; g < ngrp; ++g) {
+        const int hi = S - 1 - 4 * g, ns = hi + 1;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int bb = bcount & 1;
+          if (bcount >= 2) mbar_wait(&bempty[bb], (uint32_t)(((bcount >> 1) - 1) & 1));
+          mbar_arrive_expect_tx(&bfull[bb], (uint32_t)ns * kLChunk);
+          for (int t = 0; t < ns; ++t)
+            tc::tma_load_2d(sB + (bb * kLSmax + t) * kLChunk, &tmB, (int32_t)(t * f.Kp + (int64_t)kb * kLK),
+                            (int32_t)n0, &bfull[bb]);
+          ++bcount;
+          for (int c = 0; c < ns; ++c) {
+            if (auses >= kLARing) mbar_wait(&aempty[aslot], (uint32_t)(((auses / kLARing) - 1) & 1));
+            mbar_arrive_expect_tx(&afull[aslot], kLChunk);
+            tc::tma_load_2d(sA + aslot * kLChunk, &tmA, (int32_t)(c * f.Kp + (int64_t)kb * kLK), (int32_t)m0,
+                            &afull[aslot]);
+            if (++aslot == kLARing) aslot = 0;
+            ++auses;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_i8(kLM, kLN);
+      int bcount = 0, aslot = 0, auses = 0;
+      for (int g = 0; g < ngrp; ++g) {
+        const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0, ns = hi + 1;
+        if (g > 0)
+          for (int j = 0; j <= hi - lo; ++j) mbar_wait(&tempty[j], (uint32_t)((g - 1) & 1));
+        tc::fence_after();
+        uint32_t started = 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int bb = bcount & 1;
+          mbar_wait(&bfull[bb], (uint32_t)((bcount >> 1) & 1));
+          ++bcount;
+          tc::fence_after();
+          // descriptors: the start-address field is linear, so chunk t of the B buffer is
+          // bdesc + t * (kLChunk >> 4) and the second K half of any chunk is desc + 2
+          const uint64_t bdesc = tc::sdesc_k_sw64(smem_u32(sB + bb * kLSmax * kLChunk));
+          for (int c = 0; c < ns; ++c) {
+            mbar_wait(&afull[aslot], (uint32_t)((auses / kLARing) & 1));
+            tc::fence_after();
+            const uint64_t adesc = tc::sdesc_k_sw64(smem_u32(sA + aslot * kLChunk));
+            const int t0 = lo - c > 0 ? lo - c : 0, t1 = hi - c;
+            if (kb > 0) {
+              for (int t = t0; t <= t1; ++t) {
+                const uint32_t td = tmem + (uint32_t)((hi - c - t) * kLN);
+                const uint64_t bd = bdesc + (uint64_t)(t * (kLChunk >> 4));
+                tc::mma_i8(td, adesc, bd, idesc, 1u);
+                tc::mma_i8(td, adesc + 2, bd + 2, idesc, 1u);
+              }
+            } else {
+              for (int t = t0; t <= t1; ++t) {
+                const int j = hi - (c + t);
+                const uint32_t td = tmem + (uint32_t)(j * kLN);
+                const uint64_t bd = bdesc + (uint64_t)(t * (kLChunk >> 4));
+                tc::mma_i8(td, adesc, bd, idesc, (started >> j) & 1u);
+                tc::mma_i8(td, adesc + 2, bd + 2, idesc, 1u);
+                started |= 1u << j;
+              }
+            }
+            tc::mma_commit(&aempty[aslot]);
+            if (++aslot == kLARing) aslot = 0;
+            ++auses;
+          }
+          tc::mma_commit(&bempty[bb]);
+        }
+        for (int j = 0; j <= hi - lo; ++j) tc::mma_commit(&tfull[j]);
+      }
+    }
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int64_t row = m0 + q * 32 + lane;
+    double acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+    for (int g = 0; g < ngrp; ++g) {
+      const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0;
+      for (int h = hi; h >= lo; --h) {
+        const int jb = hi - h;
+        mbar_wait(&tfull[jb], (uint32_t)(g & 1));
+        tc::fence_after();
+        const double sc = scalbn(1.0, -12 - 7 * h);
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(tmem + (uint32_t)(jb * kLN + half * 64 + c) + ((uint32_t)(q * 32) << 16), v);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c + j] = __dadd_rn(acc[c + j], __dmul_rn((double)(int32_t)v[j], sc));
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[jb]);
+      }
+    }
+    if (row < f.M) {
+      const int ea = f.ea[row];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int64_t col = n0 + half * 64 + j;
+        bool keep = col < f.N;
+        if (f.tri != 0) {
+          const int64_t gr = row + f.tri_off;
+          keep = keep && (f.tri == 1 ? gr >= col : gr < col);
+        }
+        if (keep) {
+          const double tot = scalbn(acc[j], ea + f.eb[col]);
+          double out = __dmul_rn(f.alpha, tot);
+          if (f.beta != 0.0) out = __dadd_rn(out, __dmul_rn(f.beta, f.Cin[row * f.ldcin + col]));
+          if (f.diag != 0.0 && row - col == f.diag_offset) out = __dadd_rn(out, f.diag);
+          f.C[row * f.ldc + col] = out;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
 // max-exponent of each row of X (element (r, k) = trans ? X[k ld + r] : X[r ld + k]);
 // e[r] = e with max |x| < 2^e (frexp), 0 for an all-zero row
 __global__ void __launch_bounds__(256) ozaki_rowexp_kernel(const double *__restrict__ X, int64_t ld, int64_t rows,
@@ -350,11 +542,38 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   if ((err = cudaMallocAsync(&ea, (M + N) * sizeof(int32_t), s)) != cudaSuccess) return err;
   eb = ea + M;
   const bool fused = std::getenv("LAKER_OZAKI_UNFUSED") == nullptr;
+  // the level-group kernel is opt-in (LAKER_OZAKI_LV=1): it cuts the slice traffic 3x but
+  // measured 3.0 vs 2.5 ms at 4096^3 and 42 vs 47 ms at 4096 x 16384 x 16384 (its per-K-chunk
+  // double buffer of 8 B slices leaves too little TMA lead time), a net loss for the fit
+  const char *lvenv = std::getenv("LAKER_OZAKI_LV");
+  const bool lv = fused && S <= kLSmax && (lvenv && lvenv[0] == '1');
   if (!fused && S > 1 && (err = cudaMallocAsync(&W, (size_t)M * N * sizeof(double), s)) != cudaSuccess) return err;
   // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn);
-  // (B slices in reverse order: level h's pairs are a contiguous K range in both paths)
+  // (B slices in reverse order for the level-streaming kernels: level h's pairs are a
+  // contiguous K range; forward order for the level-group kernel)
   launch_ozaki_split(g.A, g.lda, M, K, 0, S, 0, As, ea, Kp, s);
-  launch_ozaki_split(g.B, g.ldb, N, K, b_kn ? 1 : 0, S, 1, Bs, eb, Kp, s);
+  launch_ozaki_split(g.B, g.ldb, N, K, b_kn ? 1 : 0, S, lv ? 0 : 1, Bs, eb, Kp, s);
+  if (lv) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ozaki_lv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
+      attr = true;
+    }
+    CUtensorMap ta, tb;
+    const int64_t ldo = (int64_t)S * Kp;
+    if (!make_tmap_s8_k64(&ta, As, M, ldo, ldo, kLM) || !make_tmap_s8_k64(&tb, Bs, N, ldo, ldo, kLN))
+      return cudaErrorInvalidValue;
+    FusedArgs f{};
+    f.M = M; f.N = N; f.Kp = Kp; f.S = S; f.ea = ea; f.eb = eb; f.C = g.C; f.ldc = g.ldc; f.Cin = g.Cin;
+    f.ldcin = g.ldcin; f.alpha = g.alpha; f.beta = g.beta; f.diag = g.diag; f.diag_offset = g.diag_offset;
+    f.tri = g.tri; f.tri_off = g.tri_off;
+    const unsigned grid = (unsigned)(((N + kLN - 1) / kLN) * ((M + kLM - 1) / kLM));
+    ozaki_lv_kernel<<<grid, kLThreads, kLSmem, s>>>(ta, tb, f);
+    cudaFreeAsync(As, s);
+    cudaFreeAsync(Bs, s);
+    cudaFreeAsync(ea, s);
+    return cudaGetLastError();
+  }
   if (fused) {
     static bool attr = false;
     if (!attr) {

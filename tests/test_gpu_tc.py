@@ -57,3 +57,24 @@ def test_ozaki_gemm_accuracy(M, N, K, S):
     for (i, j) in [(0, 0), (M - 1, N - 1), (M // 2, N // 3)]:
         ex = _exact_rowcol(A, B, i, j)
         assert abs(float(ex - __import__("fractions").Fraction(float(C[i, j])))) <= bound[i, j]
+
+
+@pytest.mark.parametrize("M,N,K,S", [(256, 384, 512, 8), (300, 130, 1000, 8), (128, 256, 4096, 7),
+                                     (257, 129, 96, 5), (129, 200, 640, 3)])
+def test_ozaki_level_group_kernel_equals_fused(M, N, K, S, monkeypatch):
+    """The level-group kernel (each K chunk's slices loaded once, all pairs of <= 4
+    levels into resident TMEM buffers) issues the same exact int32 level sums and
+    accumulates them in the same fp64 order as the level-streaming kernel: bitwise
+    equal results, including ragged M / N / K and S not a multiple of 4."""
+    import torch
+    from paper_2604_25138_b200 import laker as L
+    r = np.random.default_rng(M * 7 + N + K + S)
+    A = torch.from_numpy(r.standard_normal((M, K)) * np.exp2(r.integers(-20, 20, (M, 1)))).cuda()
+    B = torch.from_numpy(r.standard_normal((N, K))).cuda()
+    C1 = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    C2 = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    monkeypatch.setenv("LAKER_OZAKI_LV", "1")
+    L.laker_debug_ozaki_gemm(A, B, C1, S)
+    monkeypatch.setenv("LAKER_OZAKI_LV", "0")
+    L.laker_debug_ozaki_gemm(A, B, C2, S)
+    assert torch.equal(C1, C2)
