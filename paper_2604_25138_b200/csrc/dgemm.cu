@@ -13,6 +13,8 @@
 // conflict-free (row stride = 8 words mod 32 for the 4 x 4 lane pattern of a
 // half warp).  M and N may be ragged (zero-filled loads, masked stores);
 // K must be a multiple of 16 (callers keep operands zero padded).
+#include <algorithm>
+
 #include "laker_internal.h"
 
 namespace laker {
@@ -103,17 +105,19 @@ __global__ void __launch_bounds__(TL::THREADS) dgemm_kernel(const GemmArgs g) {
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int KT = g.K / BK;
+  const int64_t kbase = (int64_t)blockIdx.z * g.kchunk;  // split-K: this CTA's K range
+  const int64_t kend = gridDim.z > 1 ? (kbase + g.kchunk < g.K ? kbase + g.kchunk : g.K) : g.K;
+  const int KT = (int)((kend - kbase) / BK);
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
-    if (s < KT) load_stage(s, s * BK);
+    if (s < KT) load_stage(s, (int)(kbase + s * BK));
     cp_commit();
   }
   for (int kt = 0; kt < KT; ++kt) {
     cp_wait<ST - 2>();
     __syncthreads();
     const int nk = kt + ST - 1;
-    if (nk < KT) load_stage(nk % ST, nk * BK);
+    if (nk < KT) load_stage(nk % ST, (int)(kbase + nk * BK));
     cp_commit();
     const double *as = As + (kt % ST) * TL::A_ELEMS;
     const double *bs = Bs + (kt % ST) * BSZ;
@@ -133,6 +137,22 @@ __global__ void __launch_bounds__(TL::THREADS) dgemm_kernel(const GemmArgs g) {
   }
   cp_wait<0>();
 
+  if (gridDim.z > 1) {  // split-K partial: raw sums, the reduction applies the epilogue
+    double *w = g.ws + (int64_t)blockIdx.z * g.M * g.N;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = row0 + wm + 8 * i + fr;
+      if (r >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int64_t c = col0 + wn + 8 * j + 2 * fk;
+        if (c >= g.N) continue;
+        w[r * g.N + c] = acc[i][j][0];
+        if (c + 1 < g.N) w[r * g.N + c + 1] = acc[i][j][1];
+      }
+    }
+    return;
+  }
   // epilogue
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
@@ -165,6 +185,22 @@ __global__ void __launch_bounds__(TL::THREADS) dgemm_kernel(const GemmArgs g) {
   }
 }
 
+// C = alpha sum_z ws[z] (z in order) + beta Cin (+ diag): the split-K epilogue
+__global__ void splitk_reduce_kernel(const GemmArgs g, int ks) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= g.M * g.N) return;
+  const int64_t r = e / g.N, c = e % g.N;
+  double v = g.ws[e];
+  for (int z = 1; z < ks; ++z) v += g.ws[(int64_t)z * g.M * g.N + e];
+  v = g.alpha * v;
+  if (g.beta != 0.0) v = v + g.beta * g.Cin[r * g.ldcin + c];
+  if (g.diag != 0.0 && r - c == g.diag_offset) v = v + g.diag;
+  g.C[r * g.ldc + c] = v;
+}
+
+double *g_splitk_ws = nullptr;
+constexpr size_t kSplitWsDoubles = (size_t)4 << 20;  // 32 MiB
+
 __global__ void mirror_lower_kernel(double *A, int64_t lda, int64_t n) {
   __shared__ double t[32][33];
   const int64_t bi = blockIdx.y, bj = blockIdx.x;  // tile (bi, bj) with bj > bi: upper tile <- lower tile (bj, bi)
@@ -189,6 +225,7 @@ void launch_mirror_lower(double *A, int64_t lda, int64_t n, cudaStream_t s) {
 }
 
 void dgemm_init() {
+  if (!g_splitk_ws) cudaMalloc(&g_splitk_ws, kSplitWsDoubles * sizeof(double));
   cudaFuncSetAttribute(dgemm_kernel<TileL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileL::smem(false));
   cudaFuncSetAttribute(dgemm_kernel<TileL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileL::smem(true));
   cudaFuncSetAttribute(dgemm_kernel<TileS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileS::smem(false));
@@ -209,11 +246,28 @@ void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s) {
     else
       dgemm_kernel<TileL, false><<<grid, TileL::THREADS, TileL::smem(false), s>>>(g);
   } else {  // skinny or small: 64 x 64 tiles, 4 warps (more CTAs in flight)
-    dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
+    const int64_t tiles_s = ((g.N + 63) / 64) * ((g.M + 63) / 64);
+    // skinny products with a long K (the block solve's Q^T R, M Z: 64 output tiles on 148
+    // SMs): split K over ks CTAs per tile, partials summed in a fixed order
+    int ks = 1;
+    if (g.N <= 256 && g.tri == 0 && g.K >= 2048 && tiles_s < sms && g_splitk_ws) {
+      ks = (int)std::min<int64_t>({(2 * sms + tiles_s - 1) / tiles_s, g.K / 1024,
+                                   (int64_t)(kSplitWsDoubles / (size_t)(g.M * g.N))});
+      if (ks < 2) ks = 1;
+    }
+    GemmArgs gs = g;
+    if (ks > 1) {
+      gs.ws = g_splitk_ws;
+      gs.kchunk = (g.K / ks + BK - 1) / BK * BK;
+      ks = (int)((g.K + gs.kchunk - 1) / gs.kchunk);
+    }
+    dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64), (unsigned)ks);
     if (b_kn)
-      dgemm_kernel<TileS, true><<<grid, TileS::THREADS, TileS::smem(true), s>>>(g);
+      dgemm_kernel<TileS, true><<<grid, TileS::THREADS, TileS::smem(true), s>>>(gs);
     else
-      dgemm_kernel<TileS, false><<<grid, TileS::THREADS, TileS::smem(false), s>>>(g);
+      dgemm_kernel<TileS, false><<<grid, TileS::THREADS, TileS::smem(false), s>>>(gs);
+    if (ks > 1)
+      splitk_reduce_kernel<<<(unsigned)((g.M * g.N + 255) / 256), 256, 0, s>>>(gs, ks);
   }
 }
 

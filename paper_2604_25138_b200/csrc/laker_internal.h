@@ -268,6 +268,10 @@ struct GemmArgs {
   bool lower_only;        // skip CTA tiles strictly above the block diagonal
   int tri;                // 0 all; 1 only entries with row + tri_off >= col; 2 only row + tri_off < col
   int64_t tri_off;        // (tiles with no kept entry are skipped; masked entries are not written)
+  // internal (launch_dgemm's split-K for skinny products): CTA z covers k in
+  // [z kchunk, (z+1) kchunk) and writes its raw partial to ws[z] (M x N)
+  double *ws;
+  int64_t kchunk;
 };
 // copy the strict lower triangle of the n x n matrix A onto its upper triangle
 void launch_mirror_lower(double *A, int64_t lda, int64_t n, cudaStream_t s);

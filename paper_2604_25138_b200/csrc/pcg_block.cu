@@ -185,7 +185,7 @@ struct BlockArgs {
   unsigned int *counter;
 };
 
-__device__ void column_epilogue(const BlockArgs &a, int col);
+__device__ void column_epilogue(const BlockArgs &a, int col, dd_pair t0, dd_pair t1);
 
 // Column Dot2 reductions over the n x m blocks with the per-element work and
 // the per-column scalar logic of each PCG phase.  Block b owns a contiguous
@@ -268,7 +268,48 @@ __global__ void __launch_bounds__(256) block_col_kernel(const BlockArgs a) {
   if (threadIdx.x == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
   __syncthreads();
   const bool last = s_last != 0;
-  if (last && threadIdx.x < m) column_epilogue(a, threadIdx.x);
+  if (last) {
+    // the per-block pairs of each column: thread groups g = 0..G-1 (G = 256 / m) take the
+    // blocks b = g, g + G, ... with their loads issued in batches of 8, then group 0 adds
+    // the G group sums in group order -- a fixed order for every run
+    __threadfence();
+    const int G = 256 / (int)m;
+    const int col = threadIdx.x % (int)m, grp = threadIdx.x / (int)m;
+    dd_pair t0 = {0.0, 0.0}, t1 = {0.0, 0.0};
+    if (grp < G) {
+      for (unsigned b0 = grp; b0 < gridDim.x; b0 += 8u * G) {
+        dd_pair o0[8], o1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const unsigned b = b0 + (unsigned)(u * G);
+          if (b < gridDim.x) {
+            const dd_pair *pp = a.partials + ((int64_t)b * m + col) * 2;
+            o0[u] = dd_pair{__ldcg(&pp[0].s), __ldcg(&pp[0].c)};
+            o1[u] = dd_pair{__ldcg(&pp[1].s), __ldcg(&pp[1].c)};
+          } else {
+            o0[u] = o1[u] = dd_pair{0.0, 0.0};
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          pair_add(t0, o0[u]);
+          pair_add(t1, o1[u]);
+        }
+      }
+    }
+    __syncthreads();  // red[] reused for the group sums
+    red[threadIdx.x][0] = t0;
+    red[threadIdx.x][1] = t1;
+    __syncthreads();
+    if (threadIdx.x < m) {
+      dd_pair s0 = red[threadIdx.x][0], s1 = red[threadIdx.x][1];
+      for (int g = 1; g < G; ++g) {
+        pair_add(s0, red[g * m + threadIdx.x][0]);
+        pair_add(s1, red[g * m + threadIdx.x][1]);
+      }
+      column_epilogue(a, threadIdx.x, s0, s1);
+    }
+  }
   __syncthreads();
   if (last && threadIdx.x == 0) {
     int all = 1;
@@ -278,16 +319,7 @@ __global__ void __launch_bounds__(256) block_col_kernel(const BlockArgs a) {
   }
 }
 
-__device__ void column_epilogue(const BlockArgs &a, int col) {
-  const int64_t m = a.m;
-  __threadfence();
-  dd_pair t0 = {0.0, 0.0}, t1 = {0.0, 0.0};
-  for (unsigned b = 0; b < gridDim.x; ++b) {
-    const dd_pair *pp = a.partials + ((int64_t)b * m + col) * 2;
-    dd_pair o0 = {__ldcg(&pp[0].s), __ldcg(&pp[0].c)}, o1 = {__ldcg(&pp[1].s), __ldcg(&pp[1].c)};
-    pair_add(t0, o0);
-    pair_add(t1, o1);
-  }
+__device__ void column_epilogue(const BlockArgs &a, int col, dd_pair t0, dd_pair t1) {
   const double s0 = pair_value(t0), s1 = pair_value(t1);
   PcgState &S = a.st[col];
   switch (a.mode) {
