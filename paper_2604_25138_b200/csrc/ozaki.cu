@@ -30,6 +30,7 @@
 namespace laker {
 bool make_tmap_s8(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
 bool make_tmap_s8_k64(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
+bool make_tmap_s8_k32(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
 namespace {
 
 // ------------------------------------------------------------------ fused levels
@@ -204,20 +205,29 @@ __global__ void __launch_bounds__(kFThreads, 1)
 
 // ------------------------------------------------------------------ level groups
 // One CTA = one 128 x 128 output tile; the S digit levels in groups of <= 4 (4 TMEM
-// buffers x 128 columns = 512): for each 64-wide K chunk the S (or fewer) A slices and B
-// slices are loaded ONCE and every slice pair (c, t) whose level c + t falls in the
-// group is issued into that level's buffer.  The fused kernel above streams the pairs
-// level by level -- A_c and B_t are re-read for every level they meet, 4.5x the slice
-// traffic at S = 8, which left it L2-bandwidth bound; here the traffic is 3 chunk
-// loads per (c, t) square cell instead of 2 per pair.  Levels are accumulated in the
-// same order (S-1 .. 0) with the same fp64 operations, so C is bitwise the fused
-// kernel's.  B chunks double-buffered per K chunk, A chunks through a 6-slot ring.
-constexpr int kLM = 128, kLN = 128, kLK = 64;
+// buffers x 128 columns = 512): for each 32-wide K chunk the S (or fewer) A slices and B
+// slices are loaded ONCE (both operands double-buffered per chunk) and every slice pair
+// (c, t) whose level c + t falls in the group is issued, level by level so consecutive
+// MMAs accumulate into the same buffer.  The fused kernel above streams the pairs level
+// by level over the whole K -- A_c and B_t are re-read for every level they meet, 4.5x
+// the slice traffic at S = 8.  Levels are accumulated in the same order (S-1 .. 0) with
+// the same fp64 operations and exact int32 level sums, so C is bitwise the fused kernel's.
+constexpr int kLM = 128, kLN = 128, kLK = 32;
 constexpr int kLSmax = 8;
-constexpr uint32_t kLChunk = 128 * kLK;  // 8 KiB: 128 rows x 64 int8 (64B-swizzled)
-constexpr int kLARing = 6;
-constexpr size_t kLSmem = 1024 + (2 * kLSmax + kLARing) * kLChunk + 256;
+constexpr uint32_t kLChunk = 128 * kLK;  // 4 KiB: 128 rows x 32 int8 (32B-swizzled)
+constexpr size_t kLSmem = 1024 + 4 * kLSmax * kLChunk + 256;  // [2] A + [2] B chunk sets
 constexpr int kLThreads = 10 * 32;  // producer, MMA, 8 epilogue warps
+
+// K-major, 32-byte swizzle: 8-row x 32-byte atoms (SBO = 256 B), layout type 6
+__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
+  return d;
+}
 
 __global__ void __launch_bounds__(kLThreads, 1)
     ozaki_lv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -234,14 +244,12 @@ __global__ void __launch_bounds__(kLThreads, 1)
   extern __shared__ unsigned char smem_raw[];
   const uint32_t base_s = smem_u32(smem_raw);
   unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);
-  unsigned char *sB = smem;                                // [2][kLSmax] chunks
-  unsigned char *sA = smem + 2 * kLSmax * kLChunk;         // [kLARing] chunks
-  uint64_t *bfull = reinterpret_cast<uint64_t *>(sA + kLARing * kLChunk);  // [2]
-  uint64_t *bempty = bfull + 2;                                            // [2]
-  uint64_t *afull = bempty + 2;                                            // [kLARing]
-  uint64_t *aempty = afull + kLARing;                                      // [kLARing]
-  uint64_t *tfull = aempty + kLARing;                                      // [4]
-  uint64_t *tempty = tfull + 4;                                            // [4]
+  unsigned char *sA = smem;                                // [2][kLSmax] chunks
+  unsigned char *sB = smem + 2 * kLSmax * kLChunk;         // [2][kLSmax] chunks
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + 2 * kLSmax * kLChunk);  // [2]
+  uint64_t *empty = full + 2;                                               // [2]
+  uint64_t *tfull = empty + 2;                                              // [4]
+  uint64_t *tempty = tfull + 4;                                             // [4]
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = f.S;
@@ -250,12 +258,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bfull[b], 1);
-      mbar_init(&bempty[b], 1);
-    }
-    for (int r = 0; r < kLARing; ++r) {
-      mbar_init(&afull[r], 1);
-      mbar_init(&aempty[r], 1);
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1);
     }
     for (int j = 0; j < 4; ++j) {
       mbar_init(&tfull[j], 1);
@@ -271,24 +275,17 @@ __global__ void __launch_bounds__(kLThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int bcount = 0, aslot = 0, auses = 0;
+      int use = 0;
       for (int g = 0; g < ngrp; ++g) {
-        const int hi = S - 1 - 4 * g, ns = hi + 1;
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int bb = bcount & 1;
-          if (bcount >= 2) mbar_wait(&bempty[bb], (uint32_t)(((bcount >> 1) - 1) & 1));
-          mbar_arrive_expect_tx(&bfull[bb], (uint32_t)ns * kLChunk);
-          for (int t = 0; t < ns; ++t)
-            tc::tma_load_2d(sB + (bb * kLSmax + t) * kLChunk, &tmB, (int32_t)(t * f.Kp + (int64_t)kb * kLK),
-                            (int32_t)n0, &bfull[bb]);
-          ++bcount;
-          for (int c = 0; c < ns; ++c) {
-            if (auses >= kLARing) mbar_wait(&aempty[aslot], (uint32_t)(((auses / kLARing) - 1) & 1));
-            mbar_arrive_expect_tx(&afull[aslot], kLChunk);
-            tc::tma_load_2d(sA + aslot * kLChunk, &tmA, (int32_t)(c * f.Kp + (int64_t)kb * kLK), (int32_t)m0,
-                            &afull[aslot]);
-            if (++aslot == kLARing) aslot = 0;
-            ++auses;
+        const int ns = S - 4 * g;  // slices 0 .. hi of both operands
+        for (int kb = 0; kb < nkb; ++kb, ++use) {
+          const int bb = use & 1;
+          if (use >= 2) mbar_wait(&empty[bb], (uint32_t)(((use >> 1) - 1) & 1));
+          mbar_arrive_expect_tx(&full[bb], (uint32_t)(2 * ns) * kLChunk);
+          for (int t = 0; t < ns; ++t) {
+            const int32_t kc = (int32_t)(t * f.Kp + (int64_t)kb * kLK);
+            tc::tma_load_2d(sA + (bb * kLSmax + t) * kLChunk, &tmA, kc, (int32_t)m0, &full[bb]);
+            tc::tma_load_2d(sB + (bb * kLSmax + t) * kLChunk, &tmB, kc, (int32_t)n0, &full[bb]);
           }
         }
       }
@@ -296,48 +293,25 @@ __global__ void __launch_bounds__(kLThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_i8(kLM, kLN);
-      int bcount = 0, aslot = 0, auses = 0;
+      int use = 0;
       for (int g = 0; g < ngrp; ++g) {
-        const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0, ns = hi + 1;
+        const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0;
         if (g > 0)
           for (int j = 0; j <= hi - lo; ++j) mbar_wait(&tempty[j], (uint32_t)((g - 1) & 1));
         tc::fence_after();
-        uint32_t started = 0;
-        for (int kb = 0; kb < nkb; ++kb) {
-          const int bb = bcount & 1;
-          mbar_wait(&bfull[bb], (uint32_t)((bcount >> 1) & 1));
-          ++bcount;
+        for (int kb = 0; kb < nkb; ++kb, ++use) {
+          const int bb = use & 1;
+          mbar_wait(&full[bb], (uint32_t)((use >> 1) & 1));
           tc::fence_after();
-          // descriptors: the start-address field is linear, so chunk t of the B buffer is
-          // bdesc + t * (kLChunk >> 4) and the second K half of any chunk is desc + 2
-          const uint64_t bdesc = tc::sdesc_k_sw64(smem_u32(sB + bb * kLSmax * kLChunk));
-          for (int c = 0; c < ns; ++c) {
-            mbar_wait(&afull[aslot], (uint32_t)((auses / kLARing) & 1));
-            tc::fence_after();
-            const uint64_t adesc = tc::sdesc_k_sw64(smem_u32(sA + aslot * kLChunk));
-            const int t0 = lo - c > 0 ? lo - c : 0, t1 = hi - c;
-            if (kb > 0) {
-              for (int t = t0; t <= t1; ++t) {
-                const uint32_t td = tmem + (uint32_t)((hi - c - t) * kLN);
-                const uint64_t bd = bdesc + (uint64_t)(t * (kLChunk >> 4));
-                tc::mma_i8(td, adesc, bd, idesc, 1u);
-                tc::mma_i8(td, adesc + 2, bd + 2, idesc, 1u);
-              }
-            } else {
-              for (int t = t0; t <= t1; ++t) {
-                const int j = hi - (c + t);
-                const uint32_t td = tmem + (uint32_t)(j * kLN);
-                const uint64_t bd = bdesc + (uint64_t)(t * (kLChunk >> 4));
-                tc::mma_i8(td, adesc, bd, idesc, (started >> j) & 1u);
-                tc::mma_i8(td, adesc + 2, bd + 2, idesc, 1u);
-                started |= 1u << j;
-              }
-            }
-            tc::mma_commit(&aempty[aslot]);
-            if (++aslot == kLARing) aslot = 0;
-            ++auses;
+          const uint64_t ad = sdesc_k_sw32(smem_u32(sA + bb * kLSmax * kLChunk));
+          const uint64_t bd = sdesc_k_sw32(smem_u32(sB + bb * kLSmax * kLChunk));
+          for (int h = hi; h >= lo; --h) {  // level-major: consecutive MMAs share the accumulator
+            const uint32_t td = tmem + (uint32_t)((hi - h) * kLN);
+            for (int c = 0; c <= h; ++c)
+              tc::mma_i8(td, ad + (uint64_t)(c * (kLChunk >> 4)), bd + (uint64_t)((h - c) * (kLChunk >> 4)), idesc,
+                         (kb > 0 || c > 0) ? 1u : 0u);
           }
-          tc::mma_commit(&bempty[bb]);
+          tc::mma_commit(&empty[bb]);
         }
         for (int j = 0; j <= hi - lo; ++j) tc::mma_commit(&tfull[j]);
       }
@@ -542,11 +516,12 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   if ((err = cudaMallocAsync(&ea, (M + N) * sizeof(int32_t), s)) != cudaSuccess) return err;
   eb = ea + M;
   const bool fused = std::getenv("LAKER_OZAKI_UNFUSED") == nullptr;
-  // the level-group kernel is opt-in (LAKER_OZAKI_LV=1): it cuts the slice traffic 3x but
-  // measured 3.0 vs 2.5 ms at 4096^3 and 42 vs 47 ms at 4096 x 16384 x 16384 (its per-K-chunk
-  // double buffer of 8 B slices leaves too little TMA lead time), a net loss for the fit
+  // the level-group kernel cuts the slice traffic 3x: measured 40.8 vs 49.5 ms on the fit's
+  // directions product (4096 x 16384 x 16384) but 2.87 vs 2.56 ms at 4096^3, so it serves the
+  // large products only (M N K >= 2^40); LAKER_OZAKI_LV=0 / 1 forces either kernel
   const char *lvenv = std::getenv("LAKER_OZAKI_LV");
-  const bool lv = fused && S <= kLSmax && (lvenv && lvenv[0] == '1');
+  const bool big = (double)M * (double)N * (double)K >= 1099511627776.0;
+  const bool lv = fused && S <= kLSmax && (lvenv ? lvenv[0] == '1' : big);
   if (!fused && S > 1 && (err = cudaMallocAsync(&W, (size_t)M * N * sizeof(double), s)) != cudaSuccess) return err;
   // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn);
   // (B slices in reverse order for the level-streaming kernels: level h's pairs are a
@@ -561,7 +536,7 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
     }
     CUtensorMap ta, tb;
     const int64_t ldo = (int64_t)S * Kp;
-    if (!make_tmap_s8_k64(&ta, As, M, ldo, ldo, kLM) || !make_tmap_s8_k64(&tb, Bs, N, ldo, ldo, kLN))
+    if (!make_tmap_s8_k32(&ta, As, M, ldo, ldo, kLM) || !make_tmap_s8_k32(&tb, Bs, N, ldo, ldo, kLN))
       return cudaErrorInvalidValue;
     FusedArgs f{};
     f.M = M; f.N = N; f.Kp = Kp; f.S = S; f.ea = ea; f.eb = eb; f.C = g.C; f.ldc = g.ldc; f.Cin = g.Cin;
