@@ -287,7 +287,8 @@ def run_ours(args, rank, world, local_rank):
         bytes_per_launch = 8.0 * rows * n + 16.0 * n
         kname = "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)"
     if fac:
-        prec_bytes = 8.0 * (2 * n * nr + nr * nr) + 8.0 * (3 * n + 4 * nr)
+        # sharded (pcg_dist.cu): each rank streams N_r/W rows of Q^T and M and n/W rows of Q
+        prec_bytes = 8.0 * (2 * n * nr + nr * nr) / world + 8.0 * (3 * n + 4 * nr)
         pname = "3 x gemv_dot2_kernel: z = Q^T r, w = M z, theta = a^-1/2 r + Q w (factored P)"
     elif args.precond == "learned":
         prec_bytes = (8.0 * n * (n + 1) / 2 if s1["symmetric_p"] else 8.0 * rows * n) + 16.0 * n

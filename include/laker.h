@@ -115,7 +115,8 @@ typedef struct {
                         P:239), host or device; NULL -> device Philox stream `seed` */
   uint64_t seed;
   int32_t p_layout;  /* how P = Sigma*^{-1/2} is stored and applied (LAKER_P_*):
-                        AUTO (0): FACTORED on one rank, DENSE rows when sharded */
+                        AUTO (0): FACTORED (one rank or sharded; the sharded
+                        apply gathers z = Q^T r and w = M z, N_r doubles each) */
 } laker_fit_opts;
 
 /* P = a^{-1/2} I + Q M Q^T with Q (n x N_r, orthonormal columns, the thin QR of

@@ -815,8 +815,8 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   dbg("M", Zm, nrp, nrp, nrp);
   // ---- 5. P = a^{-1/2} I + Q M Q^T with Q^T = Ut (nrp x ld), M = Zm
   const double ainv = 1.0 / std::sqrt(a);
-  const bool factored = o.p_layout == LAKER_P_FACTORED ||
-                        (o.p_layout == LAKER_P_AUTO && ctx->world == 1 && !ctx->comm);
+  // AUTO: factored (the sharded solve applies it with two N_r-vector gathers, pcg_dist.cu)
+  const bool factored = o.p_layout == LAKER_P_FACTORED || o.p_layout == LAKER_P_AUTO;
   ctx->p_factored = false;
   if (factored) {
     // keep the factors: Q^T for z = Q^T r, Q for Q w, and M;

@@ -119,7 +119,7 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
     else
       launch_gemv(w, ctx->gemv_grid, ctx->stream);
     GemvArgs t = z;
-    t.A = ctx->Qr; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fw; t.row0 = ctx->r0;
+    t.A = ctx->Qr + ctx->r0 * ldq; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fw; t.row0 = ctx->r0;
     t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
     launch_gemv(t, ctx->gemv_grid, ctx->stream);
     ctx->stats.kernel_launches += 3;

@@ -274,8 +274,13 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
   const int W = ctx->world;
   const int pk = ctx->precond_kind;
   const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
-  if (dense) LAKER_TRY(ensure_dense_p(ctx));  // a factored P is expanded once to its rows
-  if (dense && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  // factored P (SURVEY §8(f) NEXT-1 on the sharded path): with r full on every rank, rank w
+  // forms its N_r/W entries of z = Q^T r and then of w = M z (whole rows of Q^T and M, so
+  // every entry is the single-GPU Dot2 value) and all-gathers them; theta_loc = a^{-1/2}
+  // r_loc + Q_loc w.  P bytes per rank: (16 n N_r + 8 N_r^2) / W, two N_r-vector gathers.
+  const bool fac = dense && ctx->p_factored && ctx->f_nrp % W == 0;
+  if (dense && !fac) LAKER_TRY(ensure_dense_p(ctx));  // a factored P is expanded once to its rows
+  if (dense && !fac && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
   if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
   const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
   cudaStream_t s = ctx->stream;
@@ -312,14 +317,37 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
   cudaEventCreate(&ev1);
   cudaEventRecord(ev0, s);
   // init: ||y|| on the full (replicated) y; alpha = 0; r_full = y
+  laker_status err = LAKER_OK;
+  // theta_loc (-> tsend, r_loc.theta_loc pair -> tsend + nloc) = P r for the full r in rf
+  auto apply_p = [&]() {
+    GemvArgs a{};
+    a.state = st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.evict_first = true;
+    if (!fac) {
+      a.A = ctx->P; a.ld = ld; a.rows = nloc; a.ncols = n; a.x = rf; a.row0 = r0; a.y = tsend; a.lambda = 0.0;
+      a.epi = kEpiStorePair; a.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc);
+      launch_gemv(a, ctx->gemv_grid, s);
+      return;
+    }
+    const int64_t nrp = ctx->f_nrp, ldq = ctx->f_ldq, nk = nrp / W, k0 = nk * ctx->rank;
+    GemvArgs z = a;  // z[k0 .. k0+nk) = Q^T[k0.., :] r
+    z.A = ctx->Qt + k0 * ld; z.ld = ld; z.rows = nk; z.ncols = n; z.x = rf; z.row0 = k0; z.y = ctx->fz + k0;
+    z.epi = kEpiNone;
+    launch_gemv(z, ctx->gemv_grid, s);
+    if (ncclAllGather(ctx->fz + k0, ctx->fz, nk, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    GemvArgs w = z;  // w[k0 .. k0+nk) = M[k0.., :] z
+    w.A = ctx->Mf + k0 * ldq; w.ld = ldq; w.ncols = nrp; w.x = ctx->fz; w.y = ctx->fw + k0; w.evict_first = false;
+    launch_gemv(w, ctx->gemv_grid, s);
+    if (ncclAllGather(ctx->fw + k0, ctx->fw, nk, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    GemvArgs t = a;  // theta_loc = a^{-1/2} r_loc + Q[r0 .., :] w, pair r_loc.theta_loc
+    t.A = ctx->Qr + r0 * ldq; t.ld = ldq; t.rows = nloc; t.ncols = nrp; t.x = ctx->fw; t.row0 = r0; t.y = tsend;
+    t.lambda = ctx->f_ainv; t.xd = rf; t.epi = kEpiStorePair; t.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc);
+    launch_gemv(t, ctx->gemv_grid, s);
+    ctx->stats.kernel_launches += 2;
+  };
   pcg_init_kernel<<<vg, kVecThreads, 0, s>>>(n, yf, af, rf, st, ctx->partials, ctx->counters + kCtrInit);
   ctx->stats.kernel_launches++;
   if (dense) {
-    GemvArgs a{};
-    a.A = ctx->P; a.ld = ld; a.rows = nloc; a.ncols = n; a.x = rf; a.row0 = r0; a.y = tsend; a.lambda = 0.0;
-    a.state = st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.epi = kEpiStorePair;
-    a.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc); a.evict_first = true;
-    launch_gemv(a, ctx->gemv_grid, s);
+    apply_p();
     LAKER_NCCL(ctx, ncclAllGather(tsend, trecv, nloc + 2, ncclDouble, ctx->comm, s));
     dist_unpack_theta_kernel<<<vg, kVecThreads, 0, s>>>(nloc, W, trecv, thf, pf, 1, st);
     ctx->stats.kernel_launches += 2;
@@ -339,7 +367,6 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
     evs.resize(4 * chunk);
     for (auto &e : evs) cudaEventCreate(&e);
   }
-  laker_status err = LAKER_OK;
   auto record_iteration = [&](int j) {
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
     dist_operator(ctx, pf, ql, st, pq_send);
@@ -354,11 +381,7 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
     ctx->stats.kernel_launches += 2;
     if (dense) {
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
-      GemvArgs a{};
-      a.A = ctx->P; a.ld = ld; a.rows = nloc; a.ncols = n; a.x = rf; a.row0 = r0; a.y = tsend; a.lambda = 0.0;
-      a.state = st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.epi = kEpiStorePair;
-      a.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc); a.evict_first = true;
-      launch_gemv(a, ctx->gemv_grid, s);
+      apply_p();
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
       if (ncclAllGather(tsend, trecv, nloc + 2, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
       dist_unpack_theta_kernel<<<vg, kVecThreads, 0, s>>>(nloc, W, trecv, thf, pf, 0, st);

@@ -16,6 +16,8 @@ import torch.multiprocessing as mp
 
 import oracle as O
 
+P_FACTORED = 3  # test-local tag: P = a^{-1/2} I + Q M Q^T applied in factored form
+
 
 def _exact_dot(x, y):
     return sum((Fraction(float(a)) * Fraction(float(b)) for a, b in zip(x, y)), Fraction(0))
@@ -33,18 +35,36 @@ def _allgather(obj, W):
     return out
 
 
+def _factored_theta(rank, W, F, r_full, r0, r1):
+    """theta_loc = (a^{-1/2} I + Q M Q^T) r on rows [r0, r1) as pcg_dist.cu's sharded
+    factored apply does it: rank w forms z_k = Q[:, k].r for its N_r/W entries k, all-
+    gather; then w_k = M_k.z likewise; then theta_i = Dot2([a^{-1/2}, Q_i], [r_i, w])."""
+    Q, M, ainv = F
+    m = Q.shape[1]
+    nk = m // W
+    ks = range(nk * rank, nk * (rank + 1))
+    z = np.concatenate(_allgather(np.array([O.dot2(Q[:, k], r_full) for k in ks]), W))
+    w = np.concatenate(_allgather(np.array([O.dot2(M[k], z) for k in ks]), W))
+    return np.array([O.dot2(np.concatenate([[ainv], Q[i]]), np.concatenate([[r_full[i]], w]))
+                     for i in range(r0, r1)])
+
+
 def sharded_pcg(rank, W, K, lam, y, pkind, P, tol, max_iters):
     """The rank-`rank` view of the row-sharded PCG (the host logic of pcg_dist.cu)."""
     n = K.shape[0]
     r0, r1 = n // W * rank, n // W * (rank + 1)
     K_loc = K[r0:r1]
-    P_loc = None if pkind != O.P_DENSE else P[r0:r1]
+    fac = pkind == P_FACTORED
+    if fac:
+        pkind, F = O.P_DENSE, P
+    P_loc = None if pkind != O.P_DENSE or fac else P[r0:r1]
     alpha_loc = np.zeros(r1 - r0)
     r_full = y.copy()
     ynorm = float(np.sqrt(float(_exact_dot(y, y))))
     # theta^0 = P r^0 (dense: sharded GEMV + all-gather of [theta slice | partial])
     if pkind == O.P_DENSE:
-        th_loc = np.array([O.dot2(P_loc[i], r_full) for i in range(r1 - r0)])
+        th_loc = (_factored_theta(rank, W, F, r_full, r0, r1) if fac else
+                  np.array([O.dot2(P_loc[i], r_full) for i in range(r1 - r0)]))
         parts = _allgather((th_loc, _exact_dot(r_full[r0:r1], th_loc)), W)
         theta = np.concatenate([t for t, _ in parts])
         rho = float(sum(p for _, p in parts))
@@ -72,7 +92,8 @@ def sharded_pcg(rank, W, K, lam, y, pkind, P, tol, max_iters):
         if rel <= tol:
             break
         if pkind == O.P_DENSE:
-            th_loc = np.array([O.dot2(P_loc[i], r_full) for i in range(r1 - r0)])
+            th_loc = (_factored_theta(rank, W, F, r_full, r0, r1) if fac else
+                      np.array([O.dot2(P_loc[i], r_full) for i in range(r1 - r0)]))
             parts2 = _allgather((th_loc, _exact_dot(r_full[r0:r1], th_loc)), W)
             theta = np.concatenate([t for t, _ in parts2])
             rho_new = float(sum(pp for _, pp in parts2))
@@ -107,10 +128,17 @@ def _case(pkind):
     elif pkind == O.P_DENSE:
         B = np.linalg.inv(K + Pb.lam * np.eye(Pb.n) + 0.5 * np.eye(Pb.n))
         P = 0.5 * (B + B.T)
+    elif pkind == P_FACTORED:  # a^{-1/2} I + Q M Q^T, Q orthonormal n x 8, M symmetric PSD
+        r = np.random.default_rng(3)
+        Q, _ = np.linalg.qr(r.standard_normal((Pb.n, 8)))
+        B = r.standard_normal((8, 8))
+        M = 0.3 * (B @ B.T)
+        M = 0.5 * (M + M.T)
+        P = (np.ascontiguousarray(Q), M, 0.7)
     return K, Pb.lam, Pb.y, pkind, P, Pb.tol
 
 
-@pytest.mark.parametrize("pkind", [O.P_NONE, O.P_JACOBI, O.P_DENSE])
+@pytest.mark.parametrize("pkind", [O.P_NONE, O.P_JACOBI, O.P_DENSE, P_FACTORED])
 def test_two_rank_sharded_pcg_equals_oracle(pkind):
     case = _case(pkind)
     ctx = mp.get_context("spawn")
@@ -123,7 +151,10 @@ def test_two_rank_sharded_pcg_equals_oracle(pkind):
     for p in procs:
         p.join(timeout=60)
     K, lam, y, _, P, tol = case
-    ao, ro = O.pcg(K, lam, y, pkind, P, tol=tol, max_iters=200)
+    if pkind == P_FACTORED:
+        ao, ro = O.pcg_factored(K, lam, y, *P, tol=tol, max_iters=200)
+    else:
+        ao, ro = O.pcg(K, lam, y, pkind, P, tol=tol, max_iters=200)
     for r in range(2):
         alpha, iters, rel = res[r]
         assert iters == ro.iters

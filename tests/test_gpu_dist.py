@@ -20,6 +20,7 @@ def L():
 
 
 @pytest.mark.parametrize("cid,n,kind", [(1, None, "none"), (1, None, "jacobi"), (2, None, "learned"),
+                                        (2, None, "factored"), (3, 2048, "factored"),
                                         (3, 1024, "jacobi"), (1, None, "onthefly")])
 def test_collective_path_equals_single(L, cid, n, kind):
     P = make_problem(cid, n=n)
@@ -34,6 +35,10 @@ def test_collective_path_equals_single(L, cid, n, kind):
             Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
             # dense rows on both sides (AUTO picks the factored P on the single-GPU path)
             c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_DENSE)
+        elif kind == "factored":
+            # the sharded factored apply: z and w entries per rank + two gathers (pcg_dist.cu)
+            Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
+            c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_AUTO)
         a, reps, hist = c.pcg_solve(P.y, P.tol, want_history=True)
         q = c.apply_operator(a)
         res.append((a, reps[0], hist, q))
