@@ -7,8 +7,8 @@
 // host verifies bitwise symmetry on the device before selecting this path
 // (symv_check_kernel) and otherwise uses gemv.cu.
 //
-// Blocking: block-rows of 128 rows, tiles of 128 rows x 32 columns (32 KiB),
-// block-row I streams the tiles with column index jt >= 4I.  The four tiles
+// Blocking: block-rows of 128 rows, tiles of 128 rows x 64 columns (64 KiB),
+// block-row I streams the tiles with column index jt >= 2I.  The two tiles
 // over the diagonal block contribute to rows only; every other tile (I, jt)
 // contributes K_IJ x_J to its rows and K_IJ^T x_I to the rows of column
 // block jt (K_ji = K_ij).  With tiles linearised row-major over the upper
@@ -16,13 +16,15 @@
 //
 // Roles (one CTA per SM): a producer warp loads each tile with one 2-D TMA
 // (cp.async.bulk.tensor, OOB rows/columns zero-filled -> ragged n) plus the
-// 32-entry slice of x with a 1-D bulk copy into a 6-stage mbarrier ring;
-// 16 consumer warps (warp w: rows 8w .. 8w+7, column c = lane) keep one Dot2
-// pair per row for the whole block-row segment and one Dot2 pair for their
-// column per tile; a reducer warp sums the 16 warps' column pairs of each tile
-// in a fixed order and stores one pair per column to `colpart[I][j]`.  At the
-// end of a block-row segment each consumer warp reduces its 8 row pairs over
-// its 32 lanes and stores them to `rowpart`.
+// 64-entry slice of x with a 1-D bulk copy into a 3-stage mbarrier ring;
+// 16 consumer warps (warp w: rows 8w .. 8w+7, columns lane and lane + 32) keep
+// one Dot2 pair per row for the whole block-row segment and one Dot2 pair per
+// column per tile; two reducer warps sum the 16 warps' column pairs of each
+// tile in a fixed order and store one pair per column to `colpart[I][j]`.  At
+// the end of a block-row segment each consumer warp reduces its 8 row pairs
+// over its 32 lanes and stores them to `rowpart`.  (64-column tiles: 16
+// elements per thread per tile amortise the per-tile barrier / offset / hand-off
+// instructions, which at 32 columns were half of the issued instructions.)
 //
 // symv_finalize_kernel then forms, for every row i of block-row J,
 //   y_i = RN( sum_{I<J} colpart[I][i] + sum_{segments} rowpart + lambda x_i )
@@ -44,7 +46,8 @@ namespace laker {
 namespace {
 
 constexpr int kSR = 128;                 // rows per block-row
-constexpr int kSC = 32;                  // columns per tile
+constexpr int kSC = 64;                  // columns per tile
+constexpr int kCPT = kSC / 32;           // columns per consumer thread
 constexpr int kTPD = kSR / kSC;          // tiles per diagonal block
 constexpr int kRPT = 8;                  // rows per consumer thread
 constexpr int kCons = 512;               // consumer threads
@@ -53,13 +56,13 @@ constexpr int kRedWarps = 2;             // warps 16, 17: column reducers (19 wa
 constexpr int kRedWarp0 = kConsWarps;
 constexpr int kProdWarp = kConsWarps + kRedWarps;  // warp 18: TMA producer
 constexpr int kSymThreads = (kConsWarps + kRedWarps + 1) * 32;
-constexpr int kSStages = 6;
-constexpr uint32_t kTileBytes = kSR * kSC * 8;   // 32768
-constexpr uint32_t kXBytes = kSC * 8;            // 256
-constexpr size_t kStageBytes = kTileBytes + 512;  // tile + x slice (keeps 512 B alignment)
-constexpr int kRedBufs = 3;
-constexpr size_t kRedBytes = kRedBufs * kConsWarps * kSC * sizeof(dd_pair);  // [3][16 warps][32 cols]
-constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 64 * sizeof(uint64_t);
+constexpr int kSStages = 3;
+constexpr uint32_t kTileBytes = kSR * kSC * 8;   // 65536
+constexpr uint32_t kXBytes = kSC * 8;            // 512
+constexpr size_t kStageBytes = kTileBytes + kXBytes;  // tile + x slice (keeps 512 B alignment)
+constexpr int kRedBufs = 2;
+constexpr size_t kRedBytes = kRedBufs * kConsWarps * kSC * sizeof(dd_pair);  // [2][16 warps][64 cols]
+constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 16 * sizeof(uint64_t);  // + static 1 KiB <= 227 KiB
 constexpr int kFinThreads = 512;
 constexpr int kFinSub = 16;              // threads per row in the finalize kernel
 constexpr int kXParts = 32;              // CTAs of absmax_parts_kernel
@@ -80,7 +83,7 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
 // ROWOFF: the row accumulators carry offsets (at most kMaxOffTiles products each, n <=
 // 16384); otherwise they are plain Dot2 pairs (the offset-sum error grows with the
 // products per accumulator) and only the 8-product column chains use offsets
-constexpr int kMaxOffTiles = 512;
+constexpr int kMaxOffTiles = 512;  // products per row accumulator: nct kCPT
 template <bool ROWOFF>
 __global__ void __launch_bounds__(kSymThreads, 1)
     symv_dot2_kernel(const __grid_constant__ CUtensorMap tm, const SymvArgs a) {
@@ -94,7 +97,6 @@ __global__ void __launch_bounds__(kSymThreads, 1)
   uint64_t *rempty = rfull + kRedBufs;  // [kRedBufs]
   __shared__ int s_I0;
   __shared__ double s_xr[kConsWarps][kRPT];  // x at the consumer warp's 8 rows (warp-private)
-  __shared__ double s_rm[kConsWarps][kRPT];  // rowmax at those rows
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t t0 = a.T * blockIdx.x / gridDim.x;
@@ -134,10 +136,9 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         const int jt = kTPD * I + (int)(t - rbeg);
         if (!first) mbar_wait(&empty[slot], ph ^ 1u);
         unsigned char *st = smem + slot * kStageBytes;
-        mbar_arrive_expect_tx(&full[slot], kTileBytes + 2 * kXBytes);
+        mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
         tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
         bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
-        bulk_g2s(st + kTileBytes + kXBytes, a.rowmax + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
         if (++slot == kSStages) {
           slot = 0;
           ph ^= 1u;
@@ -150,9 +151,10 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 
   if (warp >= kRedWarp0) {
     // ------------------------------------------------ column reducers: warp r owns columns
-    // 16r .. 16r+15; lane l sums the pairs of warps 8q .. 8q+7 (q = l / 16) of column
-    // 16r + l % 16 in warp order, then the two q-partials are combined by one shuffle.
-    const int r = warp - kRedWarp0, q = lane >> 4, col = 16 * r + (lane & 15);
+    // 32h + 16r .. 32h + 16r + 15 (h = 0, 1); lane l sums the pairs of warps 8q .. 8q+7
+    // (q = l / 16) of its column in warp order, then the two q-partials are combined by
+    // one shuffle.
+    const int r = warp - kRedWarp0, q = lane >> 4;
     int I = I0;
     int64_t rbeg = a.toff[I], rend = a.toff[I + 1];
     int b = 0;
@@ -165,27 +167,32 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       const int jt = kTPD * I + (int)(t - rbeg);
       if (jt / kTPD == I) continue;  // diagonal-block tile: rows only
       mbar_wait(&rfull[b], rph);
-      const dd_pair *rb = red + b * kConsWarps * kSC + 8 * q * kSC + col;
-      dd_pair w[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) w[k] = rb[k * kSC];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&rempty[b]);
-      pair_add(w[0], w[1]);
-      pair_add(w[2], w[3]);
-      pair_add(w[4], w[5]);
-      pair_add(w[6], w[7]);
-      pair_add(w[0], w[2]);
-      pair_add(w[4], w[6]);
-      pair_add(w[0], w[4]);
-      dd_pair v0 = w[0];
-      {
+      for (int h = 0; h < kCPT; ++h) {
+        const dd_pair *rb = red + b * kConsWarps * kSC + 8 * q * kSC + 32 * h + 16 * r + (lane & 15);
+        dd_pair w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = rb[k * kSC];
+        if (h == kCPT - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rempty[b]);
+        }
+        pair_add(w[0], w[1]);
+        pair_add(w[2], w[3]);
+        pair_add(w[4], w[5]);
+        pair_add(w[6], w[7]);
+        pair_add(w[0], w[2]);
+        pair_add(w[4], w[6]);
+        pair_add(w[0], w[4]);
+        dd_pair v0 = w[0];
         dd_pair o;
         o.s = __shfl_down_sync(0xffffffffu, v0.s, 16);
         o.c = __shfl_down_sync(0xffffffffu, v0.c, 16);
-        if (q == 0) pair_add(v0, o);
+        if (q == 0) {
+          pair_add(v0, o);
+          a.colpart[(int64_t)I * a.ldcp + (int64_t)jt * kSC + 32 * h + 16 * r + lane] = v0;
+        }
       }
-      if (q == 0) a.colpart[(int64_t)I * a.ldcp + (int64_t)jt * kSC + col] = v0;
       if (++b == kRedBufs) {
         b = 0;
         rph ^= 1u;
@@ -196,16 +203,15 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 
   // -------------------------------------------------- consumer warps
   // Every accumulator carries a power-of-two offset C >= 2 sum |a_ij x_j| of what it will
-  // add (row: <= nct products of |a| <= rowmax_i, |x| <= xmax; column: 8 products), so
+  // add (row: <= nct kCPT products of |a| <= rowmax_i, |x| <= xmax; column: 8 products), so
   // each step is TwoProd + Fast2Sum (dot2_step_off, 7 fp64 ops instead of 10); the offset
   // is removed exactly before the pair leaves the thread.
   const int c = lane;  // column within the tile; rows 8 warp .. 8 warp + 7
   dd_pair acc[kRPT];
   double *xr = s_xr[warp];
-  double *rmr = s_rm[warp];
   double xm = 0.0;
   for (int k = 0; k < a.nxparts; ++k) xm = fmax(xm, a.xparts[k]);
-  const double mrow = 2.0 * (double)a.nct;
+  const double mrow = 2.0 * (double)a.nct * kCPT;
   int curI = -1;
   int64_t rbeg = 0, rend = 0;
   int slot = 0, b = 0;
@@ -216,6 +222,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     // reduce the 8 row pairs over the warp's 32 columns; lane k stores row k
     const int s = blockIdx.x - a.segfirst[I];
     dd_pair *dst = a.rowpart + ((int64_t)I * a.maxseg + s) * kSR + warp * kRPT;
+    const double *rmr = a.rowmax + (int64_t)I * kSR + warp * kRPT;
 #pragma unroll
     for (int k = 0; k < kRPT; ++k) {
       dd_pair v = acc[k];
@@ -235,59 +242,71 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       rbeg = a.toff[curI];
       rend = a.toff[curI + 1];
       __syncwarp();
-      if (lane < kRPT) {
-        xr[lane] = a.x[(int64_t)curI * kSR + warp * kRPT + lane];
-        rmr[lane] = a.rowmax[(int64_t)curI * kSR + warp * kRPT + lane];
-      }
+      if (lane < kRPT) xr[lane] = a.x[(int64_t)curI * kSR + warp * kRPT + lane];
       __syncwarp();
+      const double *rmr = a.rowmax + (int64_t)curI * kSR + warp * kRPT;
 #pragma unroll
       for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{ROWOFF ? pow2_above(rmr[k] * xm * mrow) : 0.0, 0.0};
     }
     const int I = curI;
     const int jt = kTPD * I + (int)(t - rbeg);
     const bool diag = jt / kTPD == I;
+    // column offsets from the column maxima (L2-resident; loaded before the data wait)
+    static_assert(kCPT == 2, "two column halves per thread");
+    const double cm0 = diag ? 0.0 : __ldg(a.rowmax + (int64_t)jt * kSC + c);
+    const double cm1 = diag ? 0.0 : __ldg(a.rowmax + (int64_t)jt * kSC + 32 + c);
+    if (!diag && !rfirst) mbar_wait(&rempty[b], rph ^ 1u);  // this tile's column-pair buffer is free
     mbar_wait(&full[slot], ph);
     const double *tile = reinterpret_cast<const double *>(smem + slot * kStageBytes);
-    const double xc = tile[kSR * kSC + c];
-    const double *tp = tile + warp * kRPT * kSC + c;
-    const double ccol = diag ? 0.0 : pow2_above(tile[kSR * kSC + kSC + c] * xm * 16.0);
-    dd_pair cacc = {ccol, 0.0};
     if (diag) {
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) {
-        if (ROWOFF)
-          dot2_step_off(acc[k], tp[k * kSC], xc);
-        else
-          dot2_step(acc[k], tp[k * kSC], xc);
+      for (int h = 0; h < kCPT; ++h) {
+        const double xc = tile[kSR * kSC + 32 * h + c];
+        const double *tp = tile + warp * kRPT * kSC + 32 * h + c;
+#pragma unroll
+        for (int k = 0; k < kRPT; ++k) {
+          if (ROWOFF)
+            dot2_step_off(acc[k], tp[k * kSC], xc);
+          else
+            dot2_step(acc[k], tp[k * kSC], xc);
+        }
       }
     } else {
       // phased so that the 8 independent row steps (and the products of the column
       // chain) are in flight together: loads, TwoProds, then the Fast2Sum chains
-      double v[kRPT], p[kRPT], pe[kRPT];
+#pragma unroll 1
+      for (int h = 0; h < kCPT; ++h) {
+        const double xc = tile[kSR * kSC + 32 * h + c];
+        const double *tp = tile + warp * kRPT * kSC + 32 * h + c;
+        const double ccol = pow2_above((h ? cm1 : cm0) * xm * 16.0);
+        dd_pair cacc = {ccol, 0.0};
+        double v[kRPT], p[kRPT], pe[kRPT];
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) v[k] = tp[k * kSC];
+        for (int k = 0; k < kRPT; ++k) v[k] = tp[k * kSC];
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) two_prod(v[k], xc, p[k], pe[k]);
+        for (int k = 0; k < kRPT; ++k) two_prod(v[k], xc, p[k], pe[k]);
 #pragma unroll
-      for (int k = 0; k < kRPT; ++k) {
-        double s, se;
-        if (ROWOFF)
-          fast_two_sum(acc[k].s, p[k], s, se);
-        else
-          two_sum(acc[k].s, p[k], s, se);
-        acc[k].s = s;
-        acc[k].c = __dadd_rn(acc[k].c, __dadd_rn(pe[k], se));
+        for (int k = 0; k < kRPT; ++k) {
+          double s, se;
+          if (ROWOFF)
+            fast_two_sum(acc[k].s, p[k], s, se);
+          else
+            two_sum(acc[k].s, p[k], s, se);
+          acc[k].s = s;
+          acc[k].c = __dadd_rn(acc[k].c, __dadd_rn(pe[k], se));
+        }
+#pragma unroll
+        for (int k = 0; k < kRPT; ++k) two_prod(v[k], xr[k], p[k], pe[k]);
+#pragma unroll
+        for (int k = 0; k < kRPT; ++k) {
+          double s, se;
+          fast_two_sum(cacc.s, p[k], s, se);
+          cacc.s = s;
+          cacc.c = __dadd_rn(cacc.c, __dadd_rn(pe[k], se));
+        }
+        cacc.s = __dsub_rn(cacc.s, ccol);
+        red[b * kConsWarps * kSC + warp * kSC + 32 * h + c] = cacc;
       }
-#pragma unroll
-      for (int k = 0; k < kRPT; ++k) two_prod(v[k], xr[k], p[k], pe[k]);
-#pragma unroll
-      for (int k = 0; k < kRPT; ++k) {
-        double s, se;
-        fast_two_sum(cacc.s, p[k], s, se);
-        cacc.s = s;
-        cacc.c = __dadd_rn(cacc.c, __dadd_rn(pe[k], se));
-      }
-      cacc.s = __dsub_rn(cacc.s, ccol);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -296,8 +315,6 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       ph ^= 1u;
     }
     if (!diag) {
-      if (!rfirst) mbar_wait(&rempty[b], rph ^ 1u);
-      red[b * kConsWarps * kSC + warp * kSC + c] = cacc;
       __syncwarp();
       if (lane == 0) mbar_arrive(&rfull[b]);
       if (++b == kRedBufs) {
@@ -658,7 +675,7 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     a.xparts = p->xparts;
     a.nxparts = kXParts;
   }
-  if (p->nct <= kMaxOffTiles)
+  if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     launch_pdl(symv_dot2_kernel<true>, dim3(p->grid), dim3(kSymThreads), kSymSmem, s, p->tm[which], a);
   else
     launch_pdl(symv_dot2_kernel<false>, dim3(p->grid), dim3(kSymThreads), kSymSmem, s, p->tm[which], a);
