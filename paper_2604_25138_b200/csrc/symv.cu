@@ -64,7 +64,6 @@ constexpr int kRedBufs = 2;
 constexpr size_t kRedBytes = kRedBufs * kConsWarps * kSC * sizeof(dd_pair);  // [2][16 warps][64 cols]
 constexpr size_t kSymSmem = kSStages * kStageBytes + kRedBytes + 16 * sizeof(uint64_t);  // + static 1 KiB <= 227 KiB
 constexpr int kFinThreads = 512;
-constexpr int kFinSub = 16;              // threads per row in the finalize kernel
 constexpr int kXParts = 32;              // CTAs of absmax_parts_kernel
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int32_t c0, int32_t c1,
@@ -329,59 +328,59 @@ __global__ void __launch_bounds__(kSymThreads, 1)
 
 // y_i = RN(sum of the partial pairs of row i in a fixed order + lambda x_i); Dot2 x.y
 // per CTA; the last CTA reduces the CTA pairs in CTA order and runs the epilogue.
-// kFinSub threads per row, each summing the partials I = sub (mod kFinSub) with all
-// its loads issued before the adds; rows grid-strided over a persistent grid.
+// 32-row groups grid-strided over a persistent grid (coalesced partial loads).
 __device__ __forceinline__ dd_pair ldcg_pair(const dd_pair *p) {
-  return dd_pair{__ldcg(&p->s), __ldcg(&p->c)};
+  const double2 v = __ldcg(reinterpret_cast<const double2 *>(p));  // pairs are 16-byte aligned
+  return dd_pair{v.x, v.y};
 }
 
 template <int BR>
 __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
   pdl_prologue();
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
-  constexpr int kRowsPerPass = kFinThreads / kFinSub;
-  constexpr int kMaxLd = 8;  // colpart loads batched per thread (nb <= kFinSub * kMaxLd handled per batch)
   __shared__ dd_pair sred[kFinThreads / 32];
+  __shared__ dd_pair spart[kFinThreads / 32][32];
   __shared__ int s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int sub = tid & (kFinSub - 1);
+  constexpr int kW = kFinThreads / 32;  // 16 warps
+  static_assert(BR % 32 == 0, "a 32-row group lies in one block-row");
   dd_pair dotp = {0.0, 0.0};
-  for (int64_t base = (int64_t)blockIdx.x * kRowsPerPass; base < a.n; base += (int64_t)gridDim.x * kRowsPerPass) {
-    const int64_t i = base + tid / kFinSub;
+  // one 32-row group per iteration: lane = row, warp w sums the column partials I = w
+  // (mod 16) of the block-rows above (each load: 32 consecutive 16-byte pairs) and the
+  // row segments q = w (mod 16); warp 0 then combines the 16 warp sums in warp order
+  for (int64_t g = blockIdx.x; g * 32 < a.n; g += gridDim.x) {
+    const int64_t i = g * 32 + lane;
     const bool valid = i < a.n;
-    const int J = valid ? (int)(i / BR) : 0, r = valid ? (int)(i % BR) : 0;
+    const int J = (int)((g * 32) / BR), r = (int)(i % BR);
+    const double xi = (warp == 0 && valid) ? a.x[i] : 0.0;  // issued before the partial loads
     dd_pair v = {0.0, 0.0};
-    // column partials of the tiles (I, .) above this row's diagonal block, I = sub (mod kFinSub)
-    for (int I0 = sub; I0 < J; I0 += kFinSub * kMaxLd) {
-      dd_pair o[kMaxLd];
-#pragma unroll
-      for (int q = 0; q < kMaxLd; ++q) {
-        const int I = I0 + q * kFinSub;
-        o[q] = I < J ? ldcg_pair(&a.colpart[(int64_t)I * a.ldcp + i]) : dd_pair{0.0, 0.0};
-      }
-#pragma unroll
-      for (int q = 0; q < kMaxLd; ++q) pair_add(v, o[q]);
-    }
-    // row partials of this block-row's segments
     if (valid) {
-      const int ns = a.nseg[J];
-      for (int q = sub; q < ns; q += kFinSub) pair_add(v, ldcg_pair(a.rowpart + ((int64_t)J * a.maxseg + q) * BR + r));
-    }
-    // combine the kFinSub sub-sums in sub order; all lanes shuffle
+      int I = warp;
+      for (; I + 3 * kW < J; I += 4 * kW) {
+        dd_pair o[4];
 #pragma unroll
-    for (int off = 1; off < kFinSub; off <<= 1) {
-      dd_pair o;
-      o.s = __shfl_down_sync(0xffffffffu, v.s, off, kFinSub);
-      o.c = __shfl_down_sync(0xffffffffu, v.c, off, kFinSub);
-      if ((sub & (2 * off - 1)) == 0) pair_add(v, o);
+        for (int q = 0; q < 4; ++q) o[q] = ldcg_pair(&a.colpart[(int64_t)(I + q * kW) * a.ldcp + i]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pair_add(v, o[q]);
+      }
+      for (; I < J; I += kW) pair_add(v, ldcg_pair(&a.colpart[(int64_t)I * a.ldcp + i]));
+      const int ns = a.nseg[J];
+      for (int q = warp; q < ns; q += kW) pair_add(v, ldcg_pair(a.rowpart + ((int64_t)J * a.maxseg + q) * BR + r));
     }
-    if (valid && sub == 0) {
-      const double xi = a.x[i];
-      if (a.lambda != 0.0) dot2_step(v, a.lambda, xi);
-      const double yv = pair_value(v);
-      a.y[i] = yv;
-      dot2_step(dotp, xi, yv);
+    spart[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0) {
+      dd_pair t = spart[0][lane];
+#pragma unroll
+      for (int w = 1; w < kW; ++w) pair_add(t, spart[w][lane]);
+      if (valid) {
+        if (a.lambda != 0.0) dot2_step(t, a.lambda, xi);
+        const double yv = pair_value(t);
+        a.y[i] = yv;
+        dot2_step(dotp, xi, yv);
+      }
     }
+    __syncthreads();
   }
   dotp = warp_reduce_pair(dotp);
   if (lane == 0) sred[warp] = dotp;
@@ -574,10 +573,10 @@ cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
     p->maxseg = std::max(p->maxseg, (int)nseg[I]);
   }
   p->ldcp = (int64_t)p->nct * tc;
-  const int64_t passes = (n + kFinThreads / kFinSub - 1) / (kFinThreads / kFinSub);
+  const int64_t groups = (n + 31) / 32;  // 32-row groups of the finalize
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  p->fin_grid = (int)std::min<int64_t>(2 * sms, passes);
+  p->fin_grid = (int)std::min<int64_t>(4 * sms, groups);
   cudaError_t e;
   if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&p->segfirst, segfirst.size() * sizeof(int32_t))) != cudaSuccess) return e;
