@@ -271,41 +271,29 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         }
       }
     } else {
-      // phased so that the 8 independent row steps (and the products of the column
-      // chain) are in flight together: loads, TwoProds, then the Fast2Sum chains
-#pragma unroll 1
-      for (int h = 0; h < kCPT; ++h) {
-        const double xc = tile[kSR * kSC + 32 * h + c];
-        const double *tp = tile + warp * kRPT * kSC + 32 * h + c;
-        const double ccol = pow2_above((h ? cm1 : cm0) * xm * 16.0);
-        dd_pair cacc = {ccol, 0.0};
-        double v[kRPT], p[kRPT], pe[kRPT];
+      // k-major over both column halves: per row k the products with x_c and x_{c+32}
+      // (in that order, as the diagonal tiles do), and two independent column chains
+      const double xc0 = tile[kSR * kSC + c], xc1 = tile[kSR * kSC + 32 + c];
+      const double *tp = tile + warp * kRPT * kSC + c;
+      const double ccol0 = pow2_above(cm0 * xm * 16.0), ccol1 = pow2_above(cm1 * xm * 16.0);
+      dd_pair c0 = {ccol0, 0.0}, c1 = {ccol1, 0.0};
 #pragma unroll
-        for (int k = 0; k < kRPT; ++k) v[k] = tp[k * kSC];
-#pragma unroll
-        for (int k = 0; k < kRPT; ++k) two_prod(v[k], xc, p[k], pe[k]);
-#pragma unroll
-        for (int k = 0; k < kRPT; ++k) {
-          double s, se;
-          if (ROWOFF)
-            fast_two_sum(acc[k].s, p[k], s, se);
-          else
-            two_sum(acc[k].s, p[k], s, se);
-          acc[k].s = s;
-          acc[k].c = __dadd_rn(acc[k].c, __dadd_rn(pe[k], se));
+      for (int k = 0; k < kRPT; ++k) {
+        const double v0 = tp[k * kSC], v1 = tp[k * kSC + 32];
+        if (ROWOFF) {
+          dot2_step_off(acc[k], v0, xc0);
+          dot2_step_off(acc[k], v1, xc1);
+        } else {
+          dot2_step(acc[k], v0, xc0);
+          dot2_step(acc[k], v1, xc1);
         }
-#pragma unroll
-        for (int k = 0; k < kRPT; ++k) two_prod(v[k], xr[k], p[k], pe[k]);
-#pragma unroll
-        for (int k = 0; k < kRPT; ++k) {
-          double s, se;
-          fast_two_sum(cacc.s, p[k], s, se);
-          cacc.s = s;
-          cacc.c = __dadd_rn(cacc.c, __dadd_rn(pe[k], se));
-        }
-        cacc.s = __dsub_rn(cacc.s, ccol);
-        red[b * kConsWarps * kSC + warp * kSC + 32 * h + c] = cacc;
+        dot2_step_off(c0, v0, xr[k]);
+        dot2_step_off(c1, v1, xr[k]);
       }
+      c0.s = __dsub_rn(c0.s, ccol0);
+      c1.s = __dsub_rn(c1.s, ccol1);
+      red[b * kConsWarps * kSC + warp * kSC + c] = c0;
+      red[b * kConsWarps * kSC + warp * kSC + 32 + c] = c1;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
