@@ -17,7 +17,7 @@
 // Roles (one CTA per SM): a producer warp loads each tile with one 2-D TMA
 // (cp.async.bulk.tensor, OOB rows/columns zero-filled -> ragged n) plus the
 // 64-entry slice of x with a 1-D bulk copy into a 3-stage mbarrier ring;
-// 16 consumer warps (warp w: rows 8w .. 8w+7, columns lane and lane + 32) keep
+// 16 consumer warps (warp w: rows 8w .. 8w+7, columns 2 lane and 2 lane + 1) keep
 // one Dot2 pair per row for the whole block-row segment and one Dot2 pair per
 // column per tile; two reducer warps sum the 16 warps' column pairs of each
 // tile in a fixed order and store one pair per column to `colpart[I][j]`.  At
@@ -252,16 +252,16 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     const bool diag = jt / kTPD == I;
     // column offsets from the column maxima (L2-resident; loaded before the data wait)
     static_assert(kCPT == 2, "two column halves per thread");
-    const double cm0 = diag ? 0.0 : __ldg(a.rowmax + (int64_t)jt * kSC + c);
-    const double cm1 = diag ? 0.0 : __ldg(a.rowmax + (int64_t)jt * kSC + 32 + c);
+    // this thread's columns are 2c and 2c + 1 (16-byte loads of the tile, x and maxima)
+    const double2 cm = diag ? double2{0.0, 0.0} : __ldg(reinterpret_cast<const double2 *>(a.rowmax + (int64_t)jt * kSC) + c);
     if (!diag && !rfirst) mbar_wait(&rempty[b], rph ^ 1u);  // this tile's column-pair buffer is free
     mbar_wait(&full[slot], ph);
     const double *tile = reinterpret_cast<const double *>(smem + slot * kStageBytes);
     if (diag) {
 #pragma unroll
       for (int h = 0; h < kCPT; ++h) {
-        const double xc = tile[kSR * kSC + 32 * h + c];
-        const double *tp = tile + warp * kRPT * kSC + 32 * h + c;
+        const double xc = tile[kSR * kSC + 2 * c + h];
+        const double *tp = tile + warp * kRPT * kSC + 2 * c + h;
 #pragma unroll
         for (int k = 0; k < kRPT; ++k) {
           if (ROWOFF)
@@ -273,13 +273,15 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     } else {
       // k-major over both column halves: per row k the products with x_c and x_{c+32}
       // (in that order, as the diagonal tiles do), and two independent column chains
-      const double xc0 = tile[kSR * kSC + c], xc1 = tile[kSR * kSC + 32 + c];
-      const double *tp = tile + warp * kRPT * kSC + c;
-      const double ccol0 = pow2_above(cm0 * xm * 16.0), ccol1 = pow2_above(cm1 * xm * 16.0);
+      const double2 xcv = reinterpret_cast<const double2 *>(tile + kSR * kSC)[c];
+      const double xc0 = xcv.x, xc1 = xcv.y;
+      const double *tp = tile + warp * kRPT * kSC + 2 * c;
+      const double ccol0 = pow2_above(cm.x * xm * 16.0), ccol1 = pow2_above(cm.y * xm * 16.0);
       dd_pair c0 = {ccol0, 0.0}, c1 = {ccol1, 0.0};
 #pragma unroll
       for (int k = 0; k < kRPT; ++k) {
-        const double v0 = tp[k * kSC], v1 = tp[k * kSC + 32];
+        const double2 vv = *reinterpret_cast<const double2 *>(tp + k * kSC);
+        const double v0 = vv.x, v1 = vv.y;
         if (ROWOFF) {
           dot2_step_off(acc[k], v0, xc0);
           dot2_step_off(acc[k], v1, xc1);
@@ -292,8 +294,8 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       }
       c0.s = __dsub_rn(c0.s, ccol0);
       c1.s = __dsub_rn(c1.s, ccol1);
-      red[b * kConsWarps * kSC + warp * kSC + c] = c0;
-      red[b * kConsWarps * kSC + warp * kSC + 32 + c] = c1;
+      red[b * kConsWarps * kSC + warp * kSC + 2 * c] = c0;
+      red[b * kConsWarps * kSC + warp * kSC + 2 * c + 1] = c1;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
