@@ -188,7 +188,7 @@ ORC_API int64_t orc_jacobi_diag(int64_t n, int32_t d, const double *E, double sc
 /* P = ainv I + Q M Q^T: Q n x m row-major, M m x m row-major (O4').
    z_k = RN(sum_i Q_ik r_i), w_k = RN(sum_j M_kj z_j),
    theta_i = RN(ainv r_i + sum_k Q_ik w_k), each a Dot2 in index order. */
-typedef struct { int64_t m; const double *Q, *M; double ainv; } orc_factored;
+typedef struct { int64_t m; const double *Q, *M; double ainv; const double *QM; } orc_factored;
 
 static void factored_apply(int64_t n, const orc_factored *F, const double *r, double *theta) {
   const int64_t m = F->m;
@@ -196,6 +196,22 @@ static void factored_apply(int64_t n, const orc_factored *F, const double *r, do
   double *w = malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
 #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < m; ++k) z[k] = dot2(n, F->Q + k, m, r, 1);
+  if (F->QM) {
+    /* QM form: P r = ainv r + (Q M)(Q^T r) -- the same product associated as
+       Q (M z) -> (Q M) z with the n x m product QM given (R21):
+       theta_i = Dot2([ainv, QM_i.], [r_i, z]). */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      dot2_t A = {0.0, 0.0};
+      dot2_add(&A, F->ainv, r[i]);
+      const double *q = F->QM + i * m;
+      for (int64_t k = 0; k < m; ++k) dot2_add(&A, q[k], z[k]);
+      theta[i] = dot2_result(A);
+    }
+    free(z);
+    free(w);
+    return;
+  }
 #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < m; ++k) w[k] = dot2(m, F->M + k * m, 1, z, 1);
 #pragma omp parallel for schedule(static)
@@ -212,7 +228,14 @@ static void factored_apply(int64_t n, const orc_factored *F, const double *r, do
 
 ORC_API void orc_factored_apply(int64_t n, int64_t m, const double *Q, const double *M, double ainv,
                                 const double *r, double *theta) {
-  orc_factored F = {m, Q, M, ainv};
+  orc_factored F = {m, Q, M, ainv, NULL};
+  factored_apply(n, &F, r, theta);
+}
+
+/* theta = ainv r + QM (Q^T r) (QM = Q M, n x m row-major; R21). */
+ORC_API void orc_factored_qm_apply(int64_t n, int64_t m, const double *Q, const double *QM, double ainv,
+                                   const double *r, double *theta) {
+  orc_factored F = {m, Q, NULL, ainv, QM};
   factored_apply(n, &F, r, theta);
 }
 
@@ -315,7 +338,15 @@ ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, 
 ORC_API int orc_pcg_factored(int64_t n, const double *K, double lambda, const double *y, int64_t m,
                              const double *Q, const double *M, double ainv, double tol, int32_t max_iters,
                              double *alpha, orc_pcg_report *rep, double *history) {
-  orc_factored F = {m, Q, M, ainv};
+  orc_factored F = {m, Q, M, ainv, NULL};
+  return pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
+}
+
+/* PCG with the factored P applied in QM form (orc_factored_qm_apply). */
+ORC_API int orc_pcg_factored_qm(int64_t n, const double *K, double lambda, const double *y, int64_t m,
+                                const double *Q, const double *QM, double ainv, double tol, int32_t max_iters,
+                                double *alpha, orc_pcg_report *rep, double *history) {
+  orc_factored F = {m, Q, NULL, ainv, QM};
   return pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
 }
 

@@ -35,7 +35,7 @@ import scipy.linalg as sla
 
 __all__ = [
     "lib", "exp_cr", "dot2", "assemble", "assemble_rows", "cross_kernel", "predict",
-    "apply", "dense_apply", "factored_apply", "jacobi_diag", "pcg", "pcg_factored", "PcgReport",
+    "apply", "dense_apply", "factored_apply", "factored_qm_apply", "pcg_factored_qm", "jacobi_diag", "pcg", "pcg_factored", "PcgReport",
     "P_NONE", "P_JACOBI", "P_DENSE", "factors", "TERM_RESIDUAL_TOL", "TERM_MAX_ITERS", "TERM_ZERO_RHS", "TERM_BREAKDOWN",
     "TERM_INDEFINITE", "rho_schedule", "nr_schedule", "directions", "cccp_step_literal",
     "cccp_fit_literal",
@@ -68,6 +68,9 @@ def _load():
     L.orc_factored_apply.argtypes = [i64, i64, D, D, dbl, D, D]; L.orc_factored_apply.restype = None
     L.orc_pcg_factored.argtypes = [i64, D, dbl, D, i64, D, D, dbl, dbl, i32, D, ctypes.c_void_p, D]
     L.orc_pcg_factored.restype = ctypes.c_int
+    L.orc_factored_qm_apply.argtypes = [i64, i64, D, D, dbl, D, D]; L.orc_factored_qm_apply.restype = None
+    L.orc_pcg_factored_qm.argtypes = [i64, D, dbl, D, i64, D, D, dbl, dbl, i32, D, ctypes.c_void_p, D]
+    L.orc_pcg_factored_qm.restype = ctypes.c_int
     L.orc_num_threads.argtypes = []; L.orc_num_threads.restype = ctypes.c_int
     return L
 
@@ -167,6 +170,17 @@ def factored_apply(Q, M, ainv: float, r) -> np.ndarray:
     return th
 
 
+def factored_qm_apply(Q, QM, ainv: float, r) -> np.ndarray:
+    """theta = P r with P = ainv I + Q M Q^T applied as ainv r + QM (Q^T r), QM = Q M given
+    (the same product associated (Q M) z instead of Q (M z); R21): z = Q^T r and
+    theta_i = ainv r_i + QM_i. z, each entry one Dot2."""
+    Q, QM, r = _c(Q), _c(QM), _c(r)
+    n, m = Q.shape
+    th = np.empty(n)
+    lib.orc_factored_qm_apply(n, m, _p(Q), _p(QM), float(ainv), _p(r), _p(th))
+    return th
+
+
 def jacobi_diag(E, scale: float, lam: float) -> np.ndarray:
     """P_J = diag(lambda I + G)^{-1} (P:727, P:757-758)."""
     E = _c(E)
@@ -223,6 +237,21 @@ def pcg_factored(K, lam: float, y, Q, M, ainv: float, tol: float = 1e-10,
     rep = _CReport()
     lib.orc_pcg_factored(n, _p(K), float(lam), _p(y), Q.shape[1], _p(Q), _p(M), float(ainv), float(tol),
                          max_iters, _p(alpha), ctypes.byref(rep), _p(hist))
+    return alpha, PcgReport(rep.iters, rep.termination, rep.rel_residual, rep.true_rel_residual,
+                            hist[: rep.iters].copy())
+
+
+def pcg_factored_qm(K, lam: float, y, Q, QM, ainv: float, tol: float = 1e-10,
+                    max_iters: Optional[int] = None):
+    """`pcg` with the factored preconditioner in the QM form of `factored_qm_apply`."""
+    K, y, Q, QM = _c(K), _c(y), _c(Q), _c(QM)
+    n = K.shape[0]
+    max_iters = 10 * n if max_iters is None else int(max_iters)
+    alpha = np.empty(n)
+    hist = np.zeros(max(max_iters, 1))
+    rep = _CReport()
+    lib.orc_pcg_factored_qm(n, _p(K), float(lam), _p(y), Q.shape[1], _p(Q), _p(QM), float(ainv), float(tol),
+                            max_iters, _p(alpha), ctypes.byref(rep), _p(hist))
     return alpha, PcgReport(rep.iters, rep.termination, rep.rel_residual, rep.true_rel_residual,
                             hist[: rep.iters].copy())
 

@@ -83,3 +83,52 @@ def test_pcg_factored_matches_dense_and_cholesky():
     a0, r0 = O.pcg_factored(K, P.lam, P.y, np.zeros((n, 1)), np.zeros((1, 1)), 1.0, tol=P.tol)
     a1, r1 = O.pcg(K, P.lam, P.y, O.P_NONE, None, tol=P.tol)
     assert r0.iters == r1.iters and (a0 == a1).all()
+
+
+def _exact_factored_qm(Q, QM, ainv, r):
+    n, m = Q.shape
+    F = lambda x: Fraction(float(x))  # noqa: E731
+    z = [sum(F(Q[i, k]) * F(r[i]) for i in range(n)) for k in range(m)]
+    return [F(ainv) * F(r[i]) + sum(F(QM[i, k]) * z[k] for k in range(m)) for i in range(n)]
+
+
+def test_factored_qm_apply_exact_dyadic():
+    """QM form (R21): theta = a^{-1/2} r + QM (Q^T r).  Dyadic inputs make
+    every Dot2 exact: theta must equal the rational result; a QM used transposed, a
+    Q^T r taken over the wrong index or a dropped a^{-1/2} r term fails."""
+    r = np.random.default_rng(2)
+    n, m = 9, 4
+    Q = r.integers(-4, 5, (n, m)) / 8.0
+    QM = r.integers(-3, 4, (n, m)).astype(float)
+    x = r.integers(-8, 9, n) / 4.0
+    th = O.factored_qm_apply(Q, QM, 0.5, x)
+    assert all(Fraction(float(t)) == e for t, e in zip(th, _exact_factored_qm(Q, QM, 0.5, x)))
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (50, 7), (300, 64)])
+def test_factored_qm_apply_is_P_times_r(n, m):
+    """With QM = Q M the QM form is the same operator a^{-1/2} I + Q M Q^T (dense
+    numpy product as the independent reference), and M = 0 gives a^{-1/2} r exactly."""
+    r = np.random.default_rng(3 * n + m)
+    Q, _ = np.linalg.qr(r.standard_normal((n, m)))
+    M = r.standard_normal((m, m))
+    M = M + M.T
+    x = r.standard_normal(n)
+    P = 0.7 * np.eye(n) + Q @ M @ Q.T
+    th = O.factored_qm_apply(Q, Q @ M, 0.7, x)
+    assert np.abs(th - P @ x).max() <= 1e-13 * np.abs(P).sum(axis=1).max() * np.abs(x).max()
+    assert (O.factored_qm_apply(Q, np.zeros((n, m)), 0.7, x) == 0.7 * x).all()
+
+
+def test_pcg_factored_qm_solves():
+    P = make_problem(1)
+    K, _ = O.assemble(P.E, P.scale)
+    Z = make_directions(1, P.n, P.n_dirs)
+    _, _, st = O.cccp_fit_structured(K, P.lam, Z)
+    Q, M, ainv = O.factors(st)
+    aq, rq = O.pcg_factored_qm(K, P.lam, P.y, Q, Q @ M, ainv, tol=P.tol)
+    af, rf = O.pcg_factored(K, P.lam, P.y, Q, M, ainv, tol=P.tol)
+    assert rq.termination == O.TERM_RESIDUAL_TOL
+    assert abs(rq.iters - rf.iters) <= 25  # R15(iii): a different rounding of the same P
+    ref = O.reference_solve(K, P.lam, P.y)
+    assert np.linalg.norm(aq - ref) / np.linalg.norm(ref) <= 1e-6
