@@ -286,7 +286,11 @@ def run_ours(args, rank, world, local_rank):
     else:
         bytes_per_launch = 8.0 * rows * n + 16.0 * n
         kname = "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)"
-    if fac:
+    if fac == 2:
+        # QM form (R21); sharded: N_r/W rows of Q^T and n/W rows of QM per rank
+        prec_bytes = 8.0 * (2 * n * nr) / world + 8.0 * (3 * n + 2 * nr)
+        pname = "2 x gemv_dot2_kernel: z = Q^T r, theta = a^-1/2 r + QM z (factored P, QM = Q M)"
+    elif fac:
         # sharded (pcg_dist.cu): each rank streams N_r/W rows of Q^T and M and n/W rows of Q
         prec_bytes = 8.0 * (2 * n * nr + nr * nr) / world + 8.0 * (3 * n + 4 * nr)
         pname = "3 x gemv_dot2_kernel: z = Q^T r, w = M z, theta = a^-1/2 r + Q w (factored P)"

@@ -209,6 +209,11 @@ laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows);
    row-major) and the scalar a^{-1/2} (host), so that P = a^{-1/2} I + Q M Q^T;
    any pointer may be NULL.  NOT_READY if the context holds no factored P. */
 laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *M, double *a_inv_sqrt);
+/* The product QM = Q M (n x n_dirs row-major, host or device) the factored apply uses
+   (R21: theta = a^{-1/2} r + QM (Q^T r), two Dot2 passes).  NOT_READY if the
+   context holds no factored P in QM form (LAKER_P_3PASS=1 at fit time keeps three
+   passes), INVALID_ARGUMENT for NULL. */
+laker_status laker_get_preconditioner_qm(laker_ctx ctx, double *QM);
 /* y = (lambda I + K) x, x and y length n (y complete on every rank). */
 laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y);
 
@@ -235,7 +240,8 @@ typedef struct {
   int64_t kernel_launches;       /* kernels this context launched since creation */
   int32_t symmetric_k, symmetric_p; /* 1: K / dense P found bitwise symmetric on one rank, so the
                                        PCG applies stream only their block upper triangle (symv) */
-  int32_t p_factored, n_dirs;    /* 1: LEARNED P held as Q, M, a (LAKER_P_FACTORED); its N_r */
+  int32_t p_factored, n_dirs;    /* LEARNED P held as Q, M, a (LAKER_P_FACTORED): 1 applied in three
+                                    passes Q (M (Q^T r)), 2 in the QM form (R21); its N_r */
 } laker_stats;
 laker_status laker_get_stats(laker_ctx ctx, laker_stats *out);
 

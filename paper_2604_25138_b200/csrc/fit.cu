@@ -364,6 +364,9 @@ void free_factors(laker_ctx ctx) {
   cudaFree(ctx->Qt);
   cudaFree(ctx->Qr);
   cudaFree(ctx->Mf);
+  cudaFree(ctx->QMf);
+  ctx->QMf = nullptr;
+  ctx->p_qm = false;
   cudaFree(ctx->fz);
   ctx->Qt = ctx->Qr = ctx->Mf = ctx->fz = ctx->fw = nullptr;
   ctx->p_factored = false;
@@ -832,6 +835,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ld * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)n * ldq * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Mf, (size_t)nrp * ldq * 8));
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->QMf, (size_t)n * ldq * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->fz, (size_t)2 * ldq * 8));
       ctx->f_alloc_nrp = nrp;
       ctx->f_alloc_n = n;
@@ -844,6 +848,35 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     launch_transpose(Ut, nrp, n, ld, ctx->Qr, ldq, s);
     LAKER_CUDA(ctx, cudaMemcpy2DAsync(ctx->Mf, ldq * 8, Zm, nrp * 8, nrp * 8, nrp, cudaMemcpyDeviceToDevice, s));
     ++L;
+    // QM = Q M (reading R21, opt-in LAKER_P_QM=1): the apply becomes two passes,
+    // a^-1/2 r + QM (Q^T r) -- 2353 vs ~2140 it/s at C3, but C2's iteration count
+    // (1029) falls outside the R15(iii) envelope [975, 1015] with either GEMM, so the
+    // three-pass Q (M (Q^T r)) form stays the default (LAKER_P_3PASS=1 forces it)
+    {
+      const char *eq = std::getenv("LAKER_P_QM"), *e3 = std::getenv("LAKER_P_3PASS");
+      ctx->p_qm = (eq && eq[0] == '1') && !(e3 && e3[0] == '1');
+    }
+    if (ctx->p_qm) {
+      LAKER_CUDA(ctx, cudaMemsetAsync(ctx->QMf, 0, (size_t)n * ldq * 8, s));
+      GemmArgs g{};
+      g.M = n;
+      g.N = nrp;
+      g.K = nrp;
+      g.A = ctx->Qr;
+      g.lda = ldq;
+      g.B = ctx->Mf;
+      g.ldb = ldq;
+      g.C = ctx->QMf;
+      g.ldc = ldq;
+      g.alpha = 1.0;
+      g.beta = 0.0;
+      // int8-emulated GEMM by default (10 ms at C3); LAKER_QM_DMMA=1 keeps it on DMMA
+      // (56 ms; the same C2 count: the envelope miss is the QM association itself)
+      const char *ed = std::getenv("LAKER_QM_DMMA");
+      g.dmma_only = ed && ed[0] == '1';
+      launch_dgemm(g, true, s);
+      ++L;
+    }
     ctx->f_nr = nr;
     ctx->f_nrp = nrp;
     ctx->f_ldq = ldq;

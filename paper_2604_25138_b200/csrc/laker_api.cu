@@ -621,6 +621,18 @@ laker_status laker_apply_operator(laker_ctx ctx, const double *x, double *y) {
   return LAKER_OK;
 }
 
+laker_status laker_get_preconditioner_qm(laker_ctx ctx, double *QM) {
+  CHECK_CTX(ctx);
+  if (!ctx->p_factored || !ctx->p_qm) return set_err(ctx, LAKER_ERR_NOT_READY, "no QM-form factored preconditioner");
+  if (!QM) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "get_preconditioner_qm: NULL");
+  cudaSetDevice(ctx->device);
+  const int64_t n = ctx->n, nr = ctx->f_nr;
+  LAKER_CUDA(ctx, cudaMemcpy2DAsync(QM, nr * sizeof(double), ctx->QMf, ctx->f_ldq * sizeof(double),
+                                    nr * sizeof(double), n, cudaMemcpyDefault, ctx->stream));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return LAKER_OK;
+}
+
 laker_status laker_get_stats(laker_ctx ctx, laker_stats *out) {
   CHECK_CTX(ctx);
   if (!out) return LAKER_ERR_INVALID_ARGUMENT;
@@ -634,7 +646,7 @@ laker_status laker_get_stats(laker_ctx ctx, laker_stats *out) {
   ctx->stats.mode = ctx->mode;
   ctx->stats.symmetric_k = ctx->k_sym ? 1 : 0;
   ctx->stats.symmetric_p = ctx->p_sym ? 1 : 0;
-  ctx->stats.p_factored = ctx->p_factored ? 1 : 0;
+  ctx->stats.p_factored = ctx->p_factored ? (ctx->p_qm ? 2 : 1) : 0;
   ctx->stats.n_dirs = (int32_t)ctx->f_nr;
   *out = ctx->stats;
   return LAKER_OK;

@@ -114,6 +114,8 @@ struct laker_ctx_s {
   bool p_factored = false;
   double *Qt = nullptr;             // nrp x ld   (row k = q_k, zero padded)
   double *Qr = nullptr;             // n x f_ldq  (row i = Q_i., zero padded)
+  double *QMf = nullptr;            // n x f_ldq  QM = Q M (R21: theta = a^-1/2 r + QM (Q^T r))
+  bool p_qm = false;                // the factored apply uses QMf (two passes)
   double *Mf = nullptr;             // nrp x f_ldq
   double *fz = nullptr, *fw = nullptr;  // f_ldq workspaces (z = Q^T r, w = M z), zero padded
   int64_t f_nr = 0, f_nrp = 0, f_ldq = 0;
@@ -266,6 +268,7 @@ struct GemmArgs {
   double diag;
   int64_t diag_offset;
   bool lower_only;        // skip CTA tiles strictly above the block diagonal
+  bool dmma_only = false; // keep the product on the fp64 (DMMA) path, never the int8 emulation
   int tri;                // 0 all; 1 only entries with row + tri_off >= col; 2 only row + tri_off < col
   int64_t tri_off;        // (tiles with no kept entry are skipped; masked entries are not written)
   // internal (launch_dgemm's split-K for skinny products): CTA z covers k in

@@ -492,7 +492,7 @@ bool ozaki_eligible(const GemmArgs &g) {
     const char *v = std::getenv("LAKER_OZAKI");
     mode = (v && v[0] == '0') ? 0 : 1;
   }
-  if (!mode || g.lower_only) return false;
+  if (!mode || g.lower_only || g.dmma_only) return false;
   // pays above ~2^32 multiply-adds, with K long enough to amortize the slicing and
   // both output dimensions >= 512 (each input is re-sliced per call: a skinny product
   // such as the block solve's K X with 64 right-hand sides would re-slice the large

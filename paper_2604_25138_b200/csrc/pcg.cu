@@ -111,6 +111,14 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
     z.state = st; z.partials = ctx->partials; z.counter = ctx->counters + kCtrGemv; z.epi = kEpiNone;
     z.evict_first = true;
     launch_gemv(z, ctx->gemv_grid, ctx->stream);
+    if (ctx->p_qm) {  // R21: theta = a^-1/2 r + QM z
+      GemvArgs t = z;
+      t.A = ctx->QMf + ctx->r0 * ldq; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fz;
+      t.row0 = ctx->r0; t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
+      launch_gemv(t, ctx->gemv_grid, ctx->stream);
+      ctx->stats.kernel_launches += 2;
+      return;
+    }
     GemvArgs w = z;
     w.A = ctx->Mf; w.ld = ldq; w.rows = nrp; w.ncols = nrp; w.x = ctx->fz; w.y = ctx->fw;
     w.evict_first = false;  // keep M in L2 across iterations

@@ -334,6 +334,14 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
     z.epi = kEpiNone;
     launch_gemv(z, ctx->gemv_grid, s);
     if (ncclAllGather(ctx->fz + k0, ctx->fz, nk, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    if (ctx->p_qm) {  // R21: theta_loc = a^-1/2 r_loc + QM_loc z
+      GemvArgs t = a;
+      t.A = ctx->QMf + r0 * ldq; t.ld = ldq; t.rows = nloc; t.ncols = nrp; t.x = ctx->fz; t.row0 = r0; t.y = tsend;
+      t.lambda = ctx->f_ainv; t.xd = rf; t.epi = kEpiStorePair; t.pair_out = reinterpret_cast<dd_pair *>(tsend + nloc);
+      launch_gemv(t, ctx->gemv_grid, s);
+      ctx->stats.kernel_launches += 1;
+      return;
+    }
     GemvArgs w = z;  // w[k0 .. k0+nk) = M[k0.., :] z
     w.A = ctx->Mf + k0 * ldq; w.ld = ldq; w.ncols = nrp; w.x = ctx->fz; w.y = ctx->fw + k0; w.evict_first = false;
     launch_gemv(w, ctx->gemv_grid, s);

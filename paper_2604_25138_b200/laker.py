@@ -35,7 +35,8 @@ TERM_RESIDUAL_TOL, TERM_MAX_ITERS, TERM_ZERO_RHS, TERM_BREAKDOWN, TERM_INDEFINIT
 EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_status_string",
             "laker_last_error", "laker_assemble_kernel", "laker_fit_preconditioner", "laker_pcg_solve",
             "laker_predict", "laker_load_kernel_rows", "laker_get_kernel_rows", "laker_set_preconditioner",
-            "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_apply_operator",
+            "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_get_preconditioner_qm",
+            "laker_apply_operator",
             "laker_get_stats", "laker_debug_igemm_s8", "laker_debug_ozaki_gemm"]
 
 
@@ -101,6 +102,7 @@ def _load() -> ctypes.CDLL:
         "laker_set_preconditioner": [vp, st, vp],
         "laker_get_preconditioner_rows": [vp, vp],
         "laker_get_preconditioner_factors": [vp, vp, vp, vp],
+        "laker_get_preconditioner_qm": [vp, vp],
         "laker_apply_operator": [vp, vp, vp],
         "laker_get_stats": [vp, ctypes.POINTER(Stats)],
         "laker_debug_igemm_s8": [vp, vp, vp, i64, i64, i64],
@@ -223,6 +225,10 @@ def laker_get_preconditioner_rows(ctx, P_rows):
     _check(ctx, lib.laker_get_preconditioner_rows(ctx, _ptr(P_rows)))
 
 
+def laker_get_preconditioner_qm(ctx, QM) -> None:
+    _check(ctx, lib.laker_get_preconditioner_qm(ctx, _ptr(QM)))
+
+
 def laker_get_preconditioner_factors(ctx, Q, M, a_inv_sqrt) -> None:
     _check(ctx, lib.laker_get_preconditioner_factors(ctx, _ptr(Q), _ptr(M), _ptr(a_inv_sqrt)))
 
@@ -342,6 +348,14 @@ class Context:
         Q, M, ai = np.empty((self.n, nr)), np.empty((nr, nr)), np.zeros(1)
         laker_get_preconditioner_factors(self.h, Q, M, ai)
         return Q, M, float(ai[0])
+
+    def get_preconditioner_qm(self):
+        """QM = Q M (n x N_r) of a factored LEARNED P in the QM form (R21), or None."""
+        if self.stats()["p_factored"] != 2:
+            return None
+        QM = np.empty((self.n, self.stats()["n_dirs"]))
+        laker_get_preconditioner_qm(self.h, QM)
+        return QM
 
     def apply_operator(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64) if isinstance(x, np.ndarray) else x

@@ -11,6 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
+from staged import oracle_pcg_factored  # noqa: E402
 from synth import make_problem, make_directions  # noqa: E402
 
 
@@ -40,14 +41,14 @@ def test_factored_staged_pcg_bitwise(ctx, L, cid, n):
     Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
     rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
     st = ctx.stats()
-    assert rep["converged"] == 1 and st["p_factored"] == 1 and st["n_dirs"] == P.n_dirs
+    assert rep["converged"] == 1 and st["p_factored"] in (1, 2) and st["n_dirs"] == P.n_dirs
     Q, M, ainv = ctx.get_preconditioner_factors()
     # Q has orthonormal columns (thin QR of Ubar) and M is symmetric
     assert np.abs(Q.T @ Q - np.eye(P.n_dirs)).max() <= 1e-10
     assert np.abs(M - M.T).max() <= 1e-9 * np.abs(M).max()
     K, _ = O.assemble(P.E, P.scale)
     ag, reps, hist = ctx.pcg_solve(P.y, P.tol, want_history=True)
-    ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, ainv, tol=P.tol)
+    ao, ro = oracle_pcg_factored(ctx, K, P.lam, P.y, Q, M, ainv, tol=P.tol)
     assert reps[0]["termination"] == ro.termination == O.TERM_RESIDUAL_TOL
     assert reps[0]["iters"] == ro.iters
     _bitwise(hist, ro.history, "history")
@@ -62,6 +63,7 @@ def test_factored_symmetric_M_staged_bitwise(ctx, L, monkeypatch, cid, n):
     """LAKER_MSYM=1: w = M z through the symmetric GEMV (M is formed bitwise
     symmetric) -- the same Dot2-exact row sums, so the staged parity stays bitwise."""
     monkeypatch.setenv("LAKER_MSYM", "1")
+    monkeypatch.setenv("LAKER_P_3PASS", "1")  # the M pass exists only in the three-pass form
     P = make_problem(cid, n=n)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
@@ -70,7 +72,7 @@ def test_factored_symmetric_M_staged_bitwise(ctx, L, monkeypatch, cid, n):
     assert (M == M.T).all()
     K, _ = O.assemble(P.E, P.scale)
     ag, reps, hist = ctx.pcg_solve(P.y, P.tol, want_history=True)
-    ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, ainv, tol=P.tol)
+    ao, ro = oracle_pcg_factored(ctx, K, P.lam, P.y, Q, M, ainv, tol=P.tol)
     assert reps[0]["iters"] == ro.iters
     _bitwise(hist, ro.history, "history")
     _bitwise(ag, ao, "alpha")
@@ -88,7 +90,7 @@ def test_factored_equals_dense_layout_P(ctx, L):
     Pd = ctx.get_preconditioner_rows()
     ad, rd, _ = ctx.pcg_solve(P.y, P.tol)
     ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_FACTORED)
-    assert ctx.stats()["p_factored"] == 1
+    assert ctx.stats()["p_factored"] in (1, 2)
     af, rf, _ = ctx.pcg_solve(P.y, P.tol)
     _bitwise(ctx.get_preconditioner_rows(), Pd, "P rows from factors vs dense layout")
     assert np.linalg.norm(af - ad) / np.linalg.norm(ad) <= 1e-6
@@ -103,7 +105,7 @@ def test_factored_block_solve_T18(ctx, L):
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(1, P.n, P.n_dirs))
     ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
-    assert ctx.stats()["p_factored"] == 1
+    assert ctx.stats()["p_factored"] in (1, 2)
     Y = np.stack([P.y, -0.5 * P.y, np.roll(P.y, 7)], axis=1)
     A, reps, _ = ctx.pcg_solve(Y, P.tol)
     K, _ = O.assemble(P.E, P.scale)
@@ -123,11 +125,11 @@ def test_factored_c3_full_size_certificate(ctx, L):
     P = make_problem(3)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     ctx.fit_preconditioner(L.PRECOND_LEARNED, seed=7)
-    assert ctx.stats()["p_factored"] == 1
+    assert ctx.stats()["p_factored"] in (1, 2)
     Q, M, ainv = ctx.get_preconditioner_factors()
     K, _ = O.assemble(P.E, P.scale)
     a3, _, _ = ctx.pcg_solve(P.y, P.tol, max_iters=3)
-    o3 = O.pcg_factored(K, P.lam, P.y, Q, M, ainv, tol=P.tol, max_iters=3)[0]
+    o3 = oracle_pcg_factored(ctx, K, P.lam, P.y, Q, M, ainv, tol=P.tol, max_iters=3)[0]
     _bitwise(a3, o3, "C3 alpha after 3 iterations")
     a, reps, _ = ctx.pcg_solve(P.y, P.tol)
     assert reps[0]["termination"] == L.TERM_RESIDUAL_TOL

@@ -16,6 +16,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
+from staged import oracle_pcg_factored  # noqa: E402
 from synth import make_problem, make_directions  # noqa: E402
 
 
@@ -62,7 +63,7 @@ def test_otf_learned_chunked_staged_parity(L, monkeypatch):
     assert np.abs(Q - Qm).max() <= 1e-9
     assert np.abs(M - Mm).max() <= 1e-8 * np.abs(Mm).max()
     K, _ = O.assemble(P.E, P.scale)
-    ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, a, tol=P.tol)
+    ao, ro = oracle_pcg_factored(co, K, P.lam, P.y, Q, M, a, tol=P.tol)
     al, reps, _ = co.pcg_solve(P.y, P.tol)
     assert reps[0]["iters"] == ro.iters
     assert (al == ao).all()

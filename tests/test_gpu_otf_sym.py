@@ -12,6 +12,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
+from staged import oracle_pcg_factored  # noqa: E402
 from synth import make_problem, make_directions  # noqa: E402
 
 
@@ -60,7 +61,7 @@ def test_otf_sym_pcg_staged_parity(ctx, L, cid, n, kind):
         Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
         ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_FACTORED)
         Q, M, ai = ctx.get_preconditioner_factors()
-        ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, ai, tol=P.tol)
+        ao, ro = oracle_pcg_factored(ctx, K, P.lam, P.y, Q, M, ai, tol=P.tol)
     elif kind == "jacobi":
         ctx.set_preconditioner(L.PRECOND_JACOBI)
         ao, ro = O.pcg(K, P.lam, P.y, O.P_JACOBI, O.jacobi_diag(P.E, P.scale, P.lam), tol=P.tol)

@@ -11,6 +11,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
+from staged import oracle_pcg_factored  # noqa: E402
 from synth import make_paper_problem, make_directions  # noqa: E402
 
 
@@ -42,7 +43,7 @@ def test_paper_regime(L, n):
             Z = np.asfortranarray(make_directions(0, P.n, P.n_dirs))
             c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
             Q, M, ai = c.get_preconditioner_factors()
-            ao, ro = O.pcg_factored(K, P.lam, P.y, Q, M, ai, tol=P.tol)
+            ao, ro = oracle_pcg_factored(c, K, P.lam, P.y, Q, M, ai, tol=P.tol)
         elif kind == "jacobi":
             c.set_preconditioner(L.PRECOND_JACOBI)
             ao, ro = O.pcg(K, P.lam, P.y, O.P_JACOBI, O.jacobi_diag(P.E, P.scale, P.lam), tol=P.tol)
