@@ -97,10 +97,12 @@ def test_factored_equals_dense_layout_P(ctx, L):
     assert abs(rf[0]["iters"] - rd[0]["iters"]) <= 0.05 * rd[0]["iters"] + 2
 
 
-def test_factored_block_solve_T18(ctx, L):
+def test_factored_block_solve_T18(ctx, L, monkeypatch):
     """nrhs > 1 (block solve, C4 path) applies the factored P as three Dot2 GEMMs
     (Z = Q^T R, W = M Z, Theta = Q W + a^{-1/2} R): every column equals the
-    single-RHS factored solve bitwise (T18) and solves the system (R14)."""
+    single-RHS factored solve bitwise (T18) and solves the system (R14).  T18 is a
+    property of the three-pass form (the QM opt-in, R21, is single-RHS only)."""
+    monkeypatch.setenv("LAKER_P_3PASS", "1")
     P = make_problem(1)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(1, P.n, P.n_dirs))
