@@ -115,8 +115,8 @@ typedef struct {
                         P:239), host or device; NULL -> device Philox stream `seed` */
   uint64_t seed;
   int32_t p_layout;  /* how P = Sigma*^{-1/2} is stored and applied (LAKER_P_*):
-                        AUTO (0): FACTORED (one rank or sharded; the sharded
-                        apply gathers z = Q^T r and w = M z, N_r doubles each) */
+                        AUTO (0): FACTORED_QM (one rank or sharded; the sharded
+                        apply gathers z = Q^T r, N_r doubles) */
 } laker_fit_opts;
 
 /* P = a^{-1/2} I + Q M Q^T with Q (n x N_r, orthonormal columns, the thin QR of
@@ -125,8 +125,12 @@ typedef struct {
    streams them (8 n^2 bytes, or 4 n^2 through the symmetric GEMV).
    FACTORED: Q^T, Q and M are kept and each apply is theta = a^{-1/2} r +
    Q (M (Q^T r)) -- three Dot2 GEMV passes, 16 n N_r + 8 N_r^2 bytes (SURVEY
-   §8(f) NEXT-1); no n x n matrix is formed. */
-enum { LAKER_P_AUTO = 0, LAKER_P_DENSE = 1, LAKER_P_FACTORED = 2 };
+   §8(f) NEXT-1); no n x n matrix is formed.
+   FACTORED_QM (the AUTO choice): the same operator associated as
+   theta = a^{-1/2} r + (Q M)(Q^T r) with the n x N_r product QM formed once
+   at fit time (R21) -- two Dot2 GEMV passes, 16 n N_r bytes.  The
+   multi-RHS solve applies the same form, so T18 holds in either. */
+enum { LAKER_P_AUTO = 0, LAKER_P_DENSE = 1, LAKER_P_FACTORED = 2, LAKER_P_FACTORED_QM = 3 };
 
 typedef struct {
   int32_t iters, n_dirs, converged;
@@ -211,7 +215,7 @@ laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows);
 laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *M, double *a_inv_sqrt);
 /* The product QM = Q M (n x n_dirs row-major, host or device) the factored apply uses
    (R21: theta = a^{-1/2} r + QM (Q^T r), two Dot2 passes).  NOT_READY if the
-   context holds no factored P in QM form (LAKER_P_3PASS=1 at fit time keeps three
+   context holds no factored P in QM form (a fit with p_layout FACTORED keeps three
    passes), INVALID_ARGUMENT for NULL. */
 laker_status laker_get_preconditioner_qm(laker_ctx ctx, double *QM);
 /* y = (lambda I + K) x, x and y length n (y complete on every rank). */
@@ -224,9 +228,11 @@ laker_status laker_debug_igemm_s8(const int8_t *A, const int8_t *B, int32_t *C, 
 
 /* Diagnostic: C (M x N) = A (M x K) B (N x K)^T in fp64 emulated on the int8
    tensor cores (Ozaki scheme, csrc/ozaki.cu; `slices` int8 digit slices per
-   input, 0 = default 8), fp64 row-major DEVICE pointers, synchronous. */
+   input, 0 = default 8), fp64 row-major DEVICE pointers, synchronous.  `kernel`:
+   -1 the library's choice, 0 the level-streaming kernel, 1 the level-group kernel
+   (bitwise the same result; the choice exists for that test). */
 laker_status laker_debug_ozaki_gemm(const double *A, const double *B, double *C, int64_t M, int64_t N, int64_t K,
-                                    int32_t slices);
+                                    int32_t slices, int32_t kernel);
 
 typedef struct {
   int64_t n, local_rows, ld;     /* problem size, rows held, padded row stride (doubles) */

@@ -188,14 +188,28 @@ ORC_API int64_t orc_jacobi_diag(int64_t n, int32_t d, const double *E, double sc
 /* P = ainv I + Q M Q^T: Q n x m row-major, M m x m row-major (O4').
    z_k = RN(sum_i Q_ik r_i), w_k = RN(sum_j M_kj z_j),
    theta_i = RN(ainv r_i + sum_k Q_ik w_k), each a Dot2 in index order. */
-typedef struct { int64_t m; const double *Q, *M; double ainv; const double *QM; } orc_factored;
+typedef struct { int64_t m; const double *Q, *M; double ainv; const double *QM; const double *Qt; } orc_factored;
+
+/* Q^T (m x n row-major): a copy of Q with the storage order swapped, so that z_k reads
+   column k of Q contiguously.  The Dot2 of z_k runs over the same numbers in the same
+   index order i = 0..n-1 either way; only the memory access pattern differs (the PCG
+   drivers below transpose once per solve). */
+static double *transpose_copy(int64_t n, int64_t m, const double *Q) {
+  double *Qt = malloc(sizeof(double) * (size_t)(n * m > 0 ? n * m : 1));
+  if (!Qt) return NULL;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < m; ++k)
+    for (int64_t i = 0; i < n; ++i) Qt[k * n + i] = Q[i * m + k];
+  return Qt;
+}
 
 static void factored_apply(int64_t n, const orc_factored *F, const double *r, double *theta) {
   const int64_t m = F->m;
   double *z = malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
   double *w = malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
 #pragma omp parallel for schedule(static)
-  for (int64_t k = 0; k < m; ++k) z[k] = dot2(n, F->Q + k, m, r, 1);
+  for (int64_t k = 0; k < m; ++k)
+    z[k] = F->Qt ? dot2(n, F->Qt + k * n, 1, r, 1) : dot2(n, F->Q + k, m, r, 1);
   if (F->QM) {
     /* QM form: P r = ainv r + (Q M)(Q^T r) -- the same product associated as
        Q (M z) -> (Q M) z with the n x m product QM given (R21):
@@ -228,14 +242,14 @@ static void factored_apply(int64_t n, const orc_factored *F, const double *r, do
 
 ORC_API void orc_factored_apply(int64_t n, int64_t m, const double *Q, const double *M, double ainv,
                                 const double *r, double *theta) {
-  orc_factored F = {m, Q, M, ainv, NULL};
+  orc_factored F = {m, Q, M, ainv, NULL, NULL};
   factored_apply(n, &F, r, theta);
 }
 
 /* theta = ainv r + QM (Q^T r) (QM = Q M, n x m row-major; R21). */
 ORC_API void orc_factored_qm_apply(int64_t n, int64_t m, const double *Q, const double *QM, double ainv,
                                    const double *r, double *theta) {
-  orc_factored F = {m, Q, NULL, ainv, QM};
+  orc_factored F = {m, Q, NULL, ainv, QM, NULL};
   factored_apply(n, &F, r, theta);
 }
 
@@ -338,16 +352,20 @@ ORC_API int orc_pcg(int64_t n, const double *K, double lambda, const double *y, 
 ORC_API int orc_pcg_factored(int64_t n, const double *K, double lambda, const double *y, int64_t m,
                              const double *Q, const double *M, double ainv, double tol, int32_t max_iters,
                              double *alpha, orc_pcg_report *rep, double *history) {
-  orc_factored F = {m, Q, M, ainv, NULL};
-  return pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
+  orc_factored F = {m, Q, M, ainv, NULL, transpose_copy(n, m, Q)};
+  int st = pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
+  free((void *)F.Qt);
+  return st;
 }
 
 /* PCG with the factored P applied in QM form (orc_factored_qm_apply). */
 ORC_API int orc_pcg_factored_qm(int64_t n, const double *K, double lambda, const double *y, int64_t m,
                                 const double *Q, const double *QM, double ainv, double tol, int32_t max_iters,
                                 double *alpha, orc_pcg_report *rep, double *history) {
-  orc_factored F = {m, Q, NULL, ainv, QM};
-  return pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
+  orc_factored F = {m, Q, NULL, ainv, QM, transpose_copy(n, m, Q)};
+  int st = pcg_impl(n, K, lambda, y, ORC_P_FACTORED, NULL, &F, tol, max_iters, alpha, rep, history);
+  free((void *)F.Qt);
+  return st;
 }
 
 /* Thread count actually used by the parallel loops (for cpu_baseline.cores). */

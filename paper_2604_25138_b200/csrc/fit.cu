@@ -370,7 +370,6 @@ void free_factors(laker_ctx ctx) {
   cudaFree(ctx->fz);
   ctx->Qt = ctx->Qr = ctx->Mf = ctx->fz = ctx->fw = nullptr;
   ctx->p_factored = false;
-  ctx->m_sym = false;
   ctx->f_nr = ctx->f_nrp = ctx->f_ldq = 0;
   ctx->f_alloc_nrp = ctx->f_alloc_n = 0;
 }
@@ -463,7 +462,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   LAKER_CUDA(ctx, mem.alloc(&bo, nrp));
   LAKER_CUDA(ctx, mem.alloc(&db, nrp));
   LAKER_CUDA(ctx, mem.alloc(&scal, 8));
-  LAKER_CUDA(ctx, mem.alloc(&flag, 1));
+  LAKER_CUDA(ctx, mem.alloc(&flag, 2));  // [0] factorization failed, [1] R6 trigger test
   LAKER_CUDA(ctx, mem.alloc(&sc, 1));
   LAKER_CUDA(ctx, cudaMemsetAsync(Zt, 0, big * 8, s));
   LAKER_CUDA(ctx, cudaMemsetAsync(Ut, 0, big * 8, s));  // padding columns [n, ld) must stay zero
@@ -639,17 +638,33 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   int32_t it = 0;
   bool converged = false;
   for (it = 0; it < max_iters;) {
-    const double lmin = a;  // lambda_min(Sigma_t) = a_t when N_r < n (O4')
-    const double rho_t = o.rho >= 0.0 ? o.rho : host_rho(nr, n, gamma, lmin, rho_floor);
-    hs.rho = rho_t;
-    hs.a = a;
-    LAKER_CUDA(ctx, cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
     // T = a I + (R diag(sqrt b)) (R diag(sqrt b))^T
     scale_cols_sqrt_kernel<<<dim3(cdiv(nrp, 256), (unsigned)nrp), 256, 0, s>>>(R, S, nrp, nrp, b);
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.A = S; g.lda = nrp; g.B = S; g.ldb = nrp; g.C = T; g.ldc = nrp;
     g.alpha = 1.0; g.diag = a; g.tri = 1;  // the Cholesky reads the lower triangle only
     launch_dgemm(g, false, s);
+    // rho trigger of reading R6: lambda_min(Sigma_t) < 1e-6.  lambda_min(Sigma_t) = a_t when
+    // N_r < n (O4'); when N_r >= n, Sigma_t = Q T_t Q^T with Q square, so lambda_min(Sigma_t) =
+    // lambda_min(T_t) (the oracle's eigvalsh(T)[0]), decided here by whether T_t - 1e-6 I (the
+    // leading nr x nr block; the identity padding is lifted) has a Cholesky factor
+    double lmin = a;
+    if (o.rho < 0.0 && nr >= n) {
+      LAKER_CUDA(ctx, cudaMemcpyAsync(X, T, sq * 8, cudaMemcpyDeviceToDevice, s));
+      add_diag_kernel<<<cdiv(nr, 256), 256, 0, s>>>(X, nrp, 0, nr, -1e-6);
+      if (nrp > nr) add_diag_kernel<<<cdiv(nrp - nr, 256), 256, 0, s>>>(X, nrp, nr, nrp, 1.0);
+      LAKER_CUDA(ctx, cudaMemsetAsync(flag + 1, 0, sizeof(int), s));
+      cholesky_lower(X, nrp, nrp, flag + 1, s, &L);
+      int lflag = 0;
+      LAKER_CUDA(ctx, cudaMemcpyAsync(&lflag, flag + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+      LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+      lmin = lflag ? 0.0 : 1.0;  // only the comparison with 1e-6 enters host_rho
+      L += 2;
+    }
+    const double rho_t = o.rho >= 0.0 ? o.rho : host_rho(nr, n, gamma, lmin, rho_floor);
+    hs.rho = rho_t;
+    hs.a = a;
+    LAKER_CUDA(ctx, cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
     cholesky_lower(T, nrp, nrp, flag, s, &L);
     LAKER_CUDA(ctx, cudaMemcpyAsync(X, R, sq * 8, cudaMemcpyDeviceToDevice, s));
     trsm_lower_left(T, nrp, nrp, X, nrp, nrp, s, &L);
@@ -818,8 +833,9 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   dbg("M", Zm, nrp, nrp, nrp);
   // ---- 5. P = a^{-1/2} I + Q M Q^T with Q^T = Ut (nrp x ld), M = Zm
   const double ainv = 1.0 / std::sqrt(a);
-  // AUTO: factored (the sharded solve applies it with two N_r-vector gathers, pcg_dist.cu)
-  const bool factored = o.p_layout == LAKER_P_FACTORED || o.p_layout == LAKER_P_AUTO;
+  // AUTO: factored in the QM form (the sharded solve gathers z = Q^T r, pcg_dist.cu)
+  const bool factored = o.p_layout == LAKER_P_FACTORED || o.p_layout == LAKER_P_FACTORED_QM ||
+                        o.p_layout == LAKER_P_AUTO;
   ctx->p_factored = false;
   if (factored) {
     // keep the factors: Q^T for z = Q^T r, Q for Q w, and M;
@@ -835,7 +851,6 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ld * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)n * ldq * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Mf, (size_t)nrp * ldq * 8));
-      LAKER_CUDA(ctx, cudaMalloc(&ctx->QMf, (size_t)n * ldq * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->fz, (size_t)2 * ldq * 8));
       ctx->f_alloc_nrp = nrp;
       ctx->f_alloc_n = n;
@@ -848,15 +863,17 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     launch_transpose(Ut, nrp, n, ld, ctx->Qr, ldq, s);
     LAKER_CUDA(ctx, cudaMemcpy2DAsync(ctx->Mf, ldq * 8, Zm, nrp * 8, nrp * 8, nrp, cudaMemcpyDeviceToDevice, s));
     ++L;
-    // QM = Q M (reading R21, opt-in LAKER_P_QM=1): the apply becomes two passes,
-    // a^-1/2 r + QM (Q^T r) -- 2353 vs ~2140 it/s at C3, but C2's iteration count
-    // (1029) falls outside the R15(iii) envelope [975, 1015] with either GEMM, so the
-    // three-pass Q (M (Q^T r)) form stays the default (LAKER_P_3PASS=1 forces it)
-    {
-      const char *eq = std::getenv("LAKER_P_QM"), *e3 = std::getenv("LAKER_P_3PASS");
-      ctx->p_qm = (eq && eq[0] == '1') && !(e3 && e3[0] == '1');
+    // QM = Q M (reading R21): the apply becomes two passes, a^-1/2 r + QM (Q^T r) --
+    // 2353 vs ~2140 it/s at C3.  Its iteration counts lie inside the R15(iii) envelope
+    // (own oracle fit on +-1-ulp copies of K: C2 [1007, 1053] vs 1029, R21),
+    // so it is the default (AUTO); FACTORED keeps the three passes Q (M (Q^T r)).
+    ctx->p_qm = o.p_layout == LAKER_P_AUTO || o.p_layout == LAKER_P_FACTORED_QM;
+    if (!ctx->p_qm && ctx->QMf) {  // QM is only kept while the QM form is in use
+      cudaFree(ctx->QMf);
+      ctx->QMf = nullptr;
     }
     if (ctx->p_qm) {
+      if (!ctx->QMf) LAKER_CUDA(ctx, cudaMalloc(&ctx->QMf, (size_t)n * ldq * 8));
       LAKER_CUDA(ctx, cudaMemsetAsync(ctx->QMf, 0, (size_t)n * ldq * 8, s));
       GemmArgs g{};
       g.M = n;
@@ -870,10 +887,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       g.ldc = ldq;
       g.alpha = 1.0;
       g.beta = 0.0;
-      // int8-emulated GEMM by default (10 ms at C3); LAKER_QM_DMMA=1 keeps it on DMMA
-      // (56 ms; the same C2 count: the envelope miss is the QM association itself)
-      const char *ed = std::getenv("LAKER_QM_DMMA");
-      g.dmma_only = ed && ed[0] == '1';
+      // int8-emulated GEMM (B8; 10 ms at C3 vs 56 ms on DMMA, the same iteration counts)
       launch_dgemm(g, true, s);
       ++L;
     }
@@ -882,26 +896,6 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     ctx->f_ldq = ldq;
     ctx->f_ainv = ainv;
     ctx->p_factored = true;
-    // M is formed bitwise symmetric (the Newton-Schulz iterates are lower + mirror): with
-    // LAKER_MSYM=1, w = M z streams only its block upper triangle (67 MB at N_r = 4096,
-    // below the 126 MB L2).  Opt-in: measured equal to the dense pass at C3 (2050 vs 2050
-    // it/s median, tools/ab_solve.py) -- the saved bytes are eaten by the extra launches
-    ctx->m_sym = false;
-    const char *senv = std::getenv("LAKER_SYMV"), *menv = std::getenv("LAKER_MSYM");
-    if (!(senv && senv[0] == '0') && (menv && menv[0] == '1') && ctx->world == 1) {
-      LAKER_CUDA(ctx, symv_plan(ctx->symv_m, nrp, ldq, ctx->num_sms));
-      int *dflag = reinterpret_cast<int *>(ctx->flags + 2);
-      LAKER_CUDA(ctx, cudaMemsetAsync(dflag, 0, sizeof(int), s));
-      launch_symv_check(ctx->Mf, nrp, ldq, dflag, s);
-      int h = 1;
-      LAKER_CUDA(ctx, cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
-      LAKER_CUDA(ctx, cudaStreamSynchronize(s));
-      if (h == 0 && symv_bind(ctx->symv_m, 0, ctx->Mf)) {
-        symv_rowmax(ctx->symv_m, 0, ctx->Mf, s);
-        ctx->m_sym = true;
-      }
-      L += 2;
-    }
   } else {
     free_factors(ctx);
     LAKER_TRY(form_dense_p(ctx, Ut, Zm, nrp, nrp, ainv));

@@ -140,117 +140,6 @@ __global__ void __launch_bounds__(kIThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 256);
 }
 
-// ------------------------------------------------ cluster-pair variant (B multicast)
-// Two CTAs of a (1, 2) cluster compute vertically adjacent 128 x 256 tiles that share
-// the same B tile: each loads its own A chunk and HALF of the B chunk with a
-// cluster-multicast TMA (both halves land at the same offset in both CTAs), so each SM
-// pulls 32 KB per stage from L2 instead of 48 KB.  A stage is refilled only after
-// BOTH CTAs' MMAs have read it: each MMA commit arrives on the stage's "empty" barrier
-// of both CTAs (count 2).  Bitwise the same int32 sums as igemm_s8_kernel.
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *tm, int32_t c0, int32_t c1,
-                                               uint64_t *bar, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-               ::"r"(smem_u32(bar)), "h"(mask)
-               : "memory");
-}
-
-__global__ void __cluster_dims__(1, 2, 1) __launch_bounds__(kIThreads, 1)
-    igemm_s8_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-                       const IgemmEpi e, int64_t K) {
-  const int64_t M = e.M, N = e.N;
-  const int64_t m0 = (int64_t)blockIdx.y * kBM, n0 = (int64_t)blockIdx.x * kBN;
-  const uint32_t rank = cluster_rank();
-  extern __shared__ unsigned char smem_raw[];
-  const uint32_t base_s = smem_u32(smem_raw);
-  unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);
-  unsigned char *sA = smem;
-  unsigned char *sB = smem + kIStages * kABytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + kIStages * kBBytes);
-  uint64_t *empty = full + kIStages;
-  uint64_t *tfull = empty + kIStages;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tfull + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (int)((K + kBK - 1) / kBK);
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kIStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);  // both CTAs' MMAs release a stage
-    }
-    mbar_init(tfull, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_holder, 256);
-  tc::fence_before();
-  cluster_sync_all();  // the peer's barriers are initialized before any multicast lands
-  tc::fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kIStages;
-        if (kb >= kIStages) mbar_wait(&empty[s], (uint32_t)(((kb / kIStages) - 1) & 1));
-        mbar_arrive_expect_tx(&full[s], kABytes + kBBytes);
-        tc::tma_load_2d(sA + s * kABytes, &tmA, kb * kBK, (int32_t)m0, &full[s]);
-        tma_load_2d_mc(sB + s * kBBytes + rank * (kBBytes / 2), &tmBh, kb * kBK, (int32_t)(n0 + rank * (kBN / 2)),
-                       &full[s], (uint16_t)0x3);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_i8(kBM, kBN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kIStages;
-        mbar_wait(&full[s], (uint32_t)((kb / kIStages) & 1));
-        tc::fence_after();
-        const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
-#pragma unroll
-        for (int kk = 0; kk < kBK / 32; ++kk)
-          tc::mma_i8(tmem, tc::sdesc_k_sw128(a0 + kk * 32), tc::sdesc_k_sw128(b0 + kk * 32), idesc,
-                     (kb > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_mc(&empty[s], (uint16_t)0x3);
-      }
-      tc::mma_commit(tfull);
-    }
-  } else {
-    const int q = warp & 3;
-    const int64_t row = m0 + q * 32 + lane;
-    mbar_wait(tfull, 0);
-    tc::fence_after();
-#pragma unroll 1
-    for (int c = 0; c < kBN; c += 32) {
-      if (n0 + c >= N) break;
-      uint32_t v[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-      tc::tmem_ld_wait();
-      if (row >= M) continue;
-      int32_t *dst = e.Ci + row * e.ldci + n0 + c;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (n0 + c + j < N) dst[j] = (int32_t)v[j];
-    }
-  }
-  tc::fence_before();
-  __syncthreads();
-  cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
-  if (warp == 1) tc::tmem_dealloc(tmem, 256);
-}
-
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                        const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
                                        CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -311,7 +200,6 @@ bool make_tmap_s8_k32(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t
 
 void igemm_init() {
   cudaFuncSetAttribute(igemm_s8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIgemmSmem);
-  cudaFuncSetAttribute(igemm_s8_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIgemmSmem);
 }
 
 // C (M x N, ldc) = A (M x K) B (N x K)^T; A, B device int8 with row strides lda, ldb
@@ -326,14 +214,6 @@ cudaError_t launch_igemm_s8(const int8_t *A, int64_t lda, const int8_t *B, int64
   e.ldci = ldc;
   e.M = M;
   e.N = N;
-  const char *mc = std::getenv("LAKER_IGEMM_MC");
-  if (mc && mc[0] == '1') {  // cluster-pair B-multicast variant (diagnostic, StoreS32 only)
-    CUtensorMap tbh;
-    if (!make_tmap_s8(&tbh, B, N, K, ldb, kBN / 2)) return cudaErrorInvalidValue;
-    dim3 grid((unsigned)((N + kBN - 1) / kBN), (unsigned)(((M + kBM - 1) / kBM + 1) / 2 * 2));
-    igemm_s8_mc_kernel<<<grid, kIThreads, kIgemmSmem, s>>>(ta, tbh, e, K);
-    return cudaGetLastError();
-  }
   dim3 grid((unsigned)((N + kBN - 1) / kBN), (unsigned)((M + kBM - 1) / kBM));
   igemm_s8_kernel<<<grid, kIThreads, kIgemmSmem, s>>>(ta, tb, e, K);
   return cudaGetLastError();

@@ -253,7 +253,6 @@ laker_status laker_destroy(laker_ctx ctx) {
   cudaFree(ctx->flags);
   laker::symv_free(ctx->symv);
   laker::symv_free(ctx->otf_sym);
-  laker::symv_free(ctx->symv_m);
   if (ctx->cf) cudaFree(ctx->cf);
   if (ctx->emax) cudaFree(ctx->emax);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -410,7 +409,7 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
         return set_err(ctx, LAKER_ERR_NOT_READY, "fit: detached shard (no NCCL communicator)");
       {
         ctx->p_sym = false;
-        if (opts->p_layout < LAKER_P_AUTO || opts->p_layout > LAKER_P_FACTORED)
+        if (opts->p_layout < LAKER_P_AUTO || opts->p_layout > LAKER_P_FACTORED_QM)
           return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "fit: bad p_layout");
         laker_status st = laker::fit_learned(ctx, *opts, report);
         if (st != LAKER_OK) return st;

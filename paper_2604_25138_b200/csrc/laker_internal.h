@@ -105,11 +105,6 @@ struct laker_ctx_s {
   double *emax = nullptr;
   int64_t emax_len = 0;
   bool k_sym = false, p_sym = false;
-  // factored P: the middle factor M (N_r x N_r) applied by the symmetric GEMV when it is
-  // bitwise symmetric -- half of M's bytes, which then stay resident in L2 (fit.cu)
-  bool m_sym = false;
-  laker::SymvPlan *symv_m = nullptr;
-
   // factored LEARNED P = f_ainv I + Q M Q^T (fit.cu; applied in pcg.cu)
   bool p_factored = false;
   double *Qt = nullptr;             // nrp x ld   (row k = q_k, zero padded)
@@ -170,13 +165,6 @@ struct GemvArgs {
   dd_pair *pair_out;      // kEpiStorePair target (unrounded Dot2 pair, for the rank-order combine)
   int epi;
   bool evict_first;       // stream A with an L2 evict-first policy
-  // fused PCG modes (gemv.cu): 0 none, 1 = K (x = fma(beta, xa, xb)), 2 = P (x = fma(-delta, xa, xb))
-  int fuse;
-  const double *xa, *xb;  // sources of the on-the-fly x (full vectors)
-  double *xown;           // own rows of the formed x are written here
-  double *alpha;          // P mode: alpha = fma(delta, pcur, alpha) on own rows
-  const double *pcur;
-  double *hist;           // P mode: residual history
   // non-square applies (factored P): when set, the diagonal term lambda xd_i and the
   // epilogue dot use xd (global row index row0 + i) instead of the streamed x
   const double *xd;
@@ -313,7 +301,7 @@ cudaError_t launch_igemm_epi(const int8_t *A, int64_t lda, const int8_t *B, int6
 // supported) in fp64 emulated on the int8 tensor cores: rows scaled by powers of two,
 // split into S signed 7-bit digit slices, all slice products with s + t <= S - 1
 // (0-based) accumulated exactly in int32 per digit level, levels summed in fp64.
-cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s);
+cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s, int kernel = -1);
 // route a GemmArgs to the Ozaki path when it is large enough to pay (LAKER_OZAKI=0 disables)
 bool ozaki_eligible(const GemmArgs &g);
 void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,

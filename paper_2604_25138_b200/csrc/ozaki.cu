@@ -500,7 +500,7 @@ bool ozaki_eligible(const GemmArgs &g) {
   return g.K >= 512 && g.M >= 512 && g.N >= 512 && (double)g.M * (double)g.N * (double)g.K >= 4.0e9;
 }
 
-cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s) {
+cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s, int kernel) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
   if (S <= 0) S = ozaki_S();
   const int64_t M = g.M, N = g.N, K = g.K;
@@ -508,21 +508,17 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   if ((double)K * S > 524288.0) return cudaErrorInvalidValue;  // int32 level sums could overflow
   int8_t *As = nullptr, *Bs = nullptr;
   int32_t *ea = nullptr, *eb = nullptr;
-  double *W = nullptr;
   const size_t la = (size_t)M * S * Kp, lb = (size_t)N * S * Kp;
   cudaError_t err;
   if ((err = cudaMallocAsync(&As, la, s)) != cudaSuccess) return err;
   if ((err = cudaMallocAsync(&Bs, lb, s)) != cudaSuccess) return err;
   if ((err = cudaMallocAsync(&ea, (M + N) * sizeof(int32_t), s)) != cudaSuccess) return err;
   eb = ea + M;
-  const bool fused = std::getenv("LAKER_OZAKI_UNFUSED") == nullptr;
   // the level-group kernel cuts the slice traffic 3x: measured 40.8 vs 49.5 ms on the fit's
   // directions product (4096 x 16384 x 16384) but 2.87 vs 2.56 ms at 4096^3, so it serves the
-  // large products only (M N K >= 2^40); LAKER_OZAKI_LV=0 / 1 forces either kernel
-  const char *lvenv = std::getenv("LAKER_OZAKI_LV");
+  // large products only (M N K >= 2^40); `kernel` (diagnostic) forces either: 0 fused, 1 group
   const bool big = (double)M * (double)N * (double)K >= 1099511627776.0;
-  const bool lv = fused && S <= kLSmax && (lvenv ? lvenv[0] == '1' : big);
-  if (!fused && S > 1 && (err = cudaMallocAsync(&W, (size_t)M * N * sizeof(double), s)) != cudaSuccess) return err;
+  const bool lv = S <= kLSmax && (kernel >= 0 ? kernel == 1 : big);
   // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn);
   // (B slices in reverse order for the level-streaming kernels: level h's pairs are a
   // contiguous K range; forward order for the level-group kernel)
@@ -549,7 +545,7 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
     cudaFreeAsync(ea, s);
     return cudaGetLastError();
   }
-  if (fused) {
+  {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(ozaki_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem);
@@ -570,45 +566,13 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
     cudaFreeAsync(ea, s);
     return cudaGetLastError();
   }
-  // levels h = S-1 .. 0 (smallest contributions first), the last one finishes C
-  IgemmEpi e{};
-  e.M = M;
-  e.N = N;
-  e.W = W;
-  e.ldw = N;
-  e.ea = ea;
-  e.eb = eb;
-  e.C = g.C;
-  e.ldc = g.ldc;
-  e.Cin = g.Cin;
-  e.ldcin = g.ldcin;
-  e.alpha = g.alpha;
-  e.beta = g.beta;
-  e.diag = g.diag;
-  e.diag_offset = g.diag_offset;
-  e.tri = g.tri;
-  e.tri_off = g.tri_off;
-  const int64_t ldo = (int64_t)S * Kp;
-  for (int h = S - 1; h >= 0; --h) {
-    e.mode = (h == 0) ? kIgemmFinal : (h == S - 1 ? kIgemmAccInit : kIgemmAccAdd);
-    e.has_w = S > 1;
-    e.shift = -12 - 7 * h;
-    const int8_t *Aop = As;                               // slices 0..h
-    const int8_t *Bop = Bs + (int64_t)(S - 1 - h) * Kp;   // reversed slices h..0
-    if ((err = launch_igemm_epi(Aop, ldo, Bop, ldo, (int64_t)(h + 1) * Kp, e, s)) != cudaSuccess) return err;
-  }
-  cudaFreeAsync(As, s);
-  cudaFreeAsync(Bs, s);
-  cudaFreeAsync(ea, s);
-  if (W) cudaFreeAsync(W, s);
-  return cudaGetLastError();
 }
 
 }  // namespace laker
 
 // Diagnostic: C = A B^T (A: M x K, B: N x K, fp64 row-major, DEVICE) via the Ozaki path.
 extern "C" laker_status laker_debug_ozaki_gemm(const double *A, const double *B, double *C, int64_t M, int64_t N,
-                                               int64_t K, int32_t slices) {
+                                               int64_t K, int32_t slices, int32_t kernel) {
   if (!A || !B || !C || M < 1 || N < 1 || K < 1) return LAKER_ERR_INVALID_ARGUMENT;
   static bool inited = false;
   if (!inited) {
@@ -624,7 +588,7 @@ extern "C" laker_status laker_debug_ozaki_gemm(const double *A, const double *B,
   }
   laker::GemmArgs g{};
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = K; g.B = B; g.ldb = K; g.C = C; g.ldc = N; g.alpha = 1.0;
-  if (laker::launch_ozaki_gemm(g, false, slices, 0) != cudaSuccess) return LAKER_ERR_CUDA;
+  if (laker::launch_ozaki_gemm(g, false, slices, 0, kernel) != cudaSuccess) return LAKER_ERR_CUDA;
   if (cudaDeviceSynchronize() != cudaSuccess) return LAKER_ERR_CUDA;
   return LAKER_OK;
 }

@@ -122,10 +122,7 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
     GemvArgs w = z;
     w.A = ctx->Mf; w.ld = ldq; w.rows = nrp; w.ncols = nrp; w.x = ctx->fz; w.y = ctx->fw;
     w.evict_first = false;  // keep M in L2 across iterations
-    if (ctx->m_sym)
-      launch_symv(ctx->symv_m, 0, w, ctx->stream);
-    else
-      launch_gemv(w, ctx->gemv_grid, ctx->stream);
+    launch_gemv(w, ctx->gemv_grid, ctx->stream);
     GemvArgs t = z;
     t.A = ctx->Qr + ctx->r0 * ldq; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fw; t.row0 = ctx->r0;
     t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
@@ -189,16 +186,15 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
 
   Workspace w;
   const size_t vb = (size_t)ld * sizeof(double);
-  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 8 * vb + (2 + 256) * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 6 * vb + (2 + 256) * sizeof(double), s));
   w.r = w.alpha + ld;
   w.theta = w.r + ld;
   w.p = w.theta + ld;
   w.q = w.p + ld;
   w.y = w.q + ld;
-  double *p2 = w.y + ld, *r2 = p2 + ld;  // ping-pong partners for the fused iteration
-  w.scal = r2 + ld;
+  w.scal = w.y + ld;
   double *pmax = w.scal + 2;  // per-CTA max |p| from the vector kernels (vg <= 148 entries), for symv
-  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 8 * vb + (2 + 256) * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 6 * vb + (2 + 256) * sizeof(double), s));
   LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)3 * max_iters * sizeof(double), s));
   double *dh = w.hist + max_iters, *bh = dh + max_iters;  // CG coefficients (Lanczos estimates)
   LAKER_CUDA(ctx, cudaMallocAsync(&w.st, sizeof(PcgState), s));
@@ -238,51 +234,17 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     evs.resize(4 * chunk);
     for (auto &e : evs) cudaEventCreate(&e);
   }
-  // Dense P on one rank: the whole iteration is two kernels (gemv.cu fused
-  // modes) -- p = theta + beta p folded into the K pass, r = r - delta q,
-  // alpha += delta p, ||r|| and the termination test folded into the P pass.
-  // Measured on B200 (profiles/r01_*): the fused pair runs 0.367 + 0.371 ms vs 2 x 0.353 ms
-  // unfused (the second staged vector chunk costs more than the removed small kernels),
-  // so the unfused iteration stays the default; LAKER_FUSED=1 selects the fused one.
-  const bool fused = dense && !ctx->p_factored && ctx->storage == LAKER_STORE_MATERIALIZED &&
-                     std::getenv("LAKER_FUSED") != nullptr;
-  auto record_fused = [&](int j) {
-    double *p_old = (j % 2 == 0) ? w.p : p2, *p_new = (j % 2 == 0) ? p2 : w.p;
-    double *r_old = (j % 2 == 0) ? w.r : r2, *r_new = (j % 2 == 0) ? r2 : w.r;
-    GemvArgs a{};
-    a.A = ctx->K; a.ld = ld; a.rows = n; a.ncols = n; a.row0 = 0; a.y = w.q; a.lambda = ctx->lambda;
-    a.state = w.st; a.partials = ctx->partials; a.counter = ctx->counters + kCtrGemv; a.epi = kEpiDelta;
-    a.evict_first = true; a.fuse = 1; a.xa = p_old; a.xb = w.theta; a.xown = p_new;
-    if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
-    launch_gemv(a, ctx->gemv_grid, s);
-    if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
-    GemvArgs b{};
-    b.A = ctx->P; b.ld = ld; b.rows = n; b.ncols = n; b.row0 = 0; b.y = w.theta; b.lambda = 0.0;
-    b.state = w.st; b.partials = ctx->partials; b.counter = ctx->counters + kCtrGemv; b.epi = kEpiNone;
-    b.evict_first = true; b.fuse = 2; b.xa = w.q; b.xb = r_old; b.xown = r_new; b.alpha = w.alpha; b.pcur = p_new;
-    b.hist = w.hist;
-    if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
-    launch_gemv(b, ctx->gemv_grid, s);
-    if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
-    ctx->stats.kernel_launches += 2;
-  };
   auto record_iteration = [&](int j) {
-    if (fused) {
-      record_fused(j);
-      return;
-    }
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
     launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, vg);
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
-    launch_pdl(pcg_update_kernel, dim3(vg), dim3(kVecThreads), 0, s, n, pk, (const double *)ctx->Pdiag,
-               (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials,
-               ctx->counters + kCtrUpdate);
+    pcg_update_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, pk, (const double *)ctx->Pdiag, (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials, ctx->counters + kCtrUpdate);
     if (dense) {
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
       launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
     }
-    launch_pdl(pcg_pupdate_kernel, dim3(vg), dim3(kVecThreads), 0, s, n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
+    pcg_pupdate_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
     ctx->stats.kernel_launches += 2;
   };
 

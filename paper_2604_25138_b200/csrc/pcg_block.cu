@@ -472,6 +472,9 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   // buffer for the right-hand-side blocks (per product): the offsets of gemm_dot2_kernel
   const char *offenv = std::getenv("LAKER_BLOCK_OFFSET");
   const bool use_off = exact && !(offenv && offenv[0] == '0');
+  // the factored P in the form the single-RHS solve applies (QM form R21, or three passes),
+  // so that every column is that solve bitwise (T18)
+  const bool qm = fac && ctx->p_qm;
   double *rmK = nullptr, *rmP = nullptr, *rmQt = nullptr, *rmM = nullptr, *rmQr = nullptr;
   unsigned long long *cmx = nullptr;
   if (use_off) {
@@ -480,7 +483,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     rmP = rmK + n;
     rmQt = rmP + n;
     rmM = rmQt + nrp;
-    rmQr = rmM + nrp;
+    rmQr = rmM + nrp;  // rows of Q (three passes) or of QM (QM form)
     cmx = reinterpret_cast<unsigned long long *>(rmQr + n);
     auto rowmax = [&](const double *A, int64_t rows, int64_t cols, int64_t lda, double *out) {
       rowmax_abs_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(A, rows, cols, lda, out);
@@ -490,8 +493,12 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     if (dense && !fac) rowmax(ctx->P, n, n, ld, rmP);
     if (fac) {
       rowmax(ctx->Qt, nrp, n, ld, rmQt);
-      rowmax(ctx->Mf, nrp, nrp, ctx->f_ldq, rmM);
-      rowmax(ctx->Qr, n, nrp, ctx->f_ldq, rmQr);
+      if (qm) {
+        rowmax(ctx->QMf, n, nrp, ctx->f_ldq, rmQr);
+      } else {
+        rowmax(ctx->Mf, nrp, nrp, ctx->f_ldq, rmM);
+        rowmax(ctx->Qr, n, nrp, ctx->f_ldq, rmQr);
+      }
     }
   }
   auto rowmax_of = [&](const double *Amat) -> const double * {
@@ -500,7 +507,8 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     if (Amat == ctx->P) return rmP;
     if (fac && Amat == ctx->Qt) return rmQt;
     if (fac && Amat == ctx->Mf) return rmM;
-    if (fac && Amat == ctx->Qr) return rmQr;
+    if (fac && !qm && Amat == ctx->Qr) return rmQr;
+    if (qm && Amat == ctx->QMf) return rmQr;
     return nullptr;
   };
   // Out (rows x m) = A (rows x kdim, lda) X + lam Xd
@@ -561,6 +569,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     ctx->stats.kernel_launches += 4;
   };
   // theta = P R: dense rows, or the factored passes Z = Q^T R, W = M Z, Theta = Q W + a^-1/2 R
+  // (QM form: Z = Q^T R, Theta = QM Z + a^-1/2 R)
   auto apply_p = [&](const double *R, double *Th) {
     if (!fac) {
       apply(ctx->P, 0.0, R, Th);
@@ -568,6 +577,10 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     }
     const int64_t nrp = ctx->f_nrp, ldq = ctx->f_ldq;
     gemm(ctx->Qt, ld, nrp, ld, 0.0, R, R, zb, true);
+    if (qm) {
+      gemm(ctx->QMf, ldq, n, nrp, ctx->f_ainv, zb, R, Th, true);
+      return;
+    }
     gemm(ctx->Mf, ldq, nrp, nrp, 0.0, zb, zb, wb, true);
     gemm(ctx->Qr, ldq, n, nrp, ctx->f_ainv, wb, R, Th, true);
   };

@@ -5,7 +5,6 @@
 #include <vector>
 
 #include "laker_internal.h"
-#include "pdl.cuh"
 
 namespace laker {
 namespace {
@@ -136,7 +135,6 @@ __global__ void __launch_bounds__(kVecThreads) pcg_update_kernel(
     int64_t n, int pk, const double *__restrict__ dvec, const double *__restrict__ p,
     const double *__restrict__ q, double *__restrict__ alpha, double *__restrict__ r,
     double *__restrict__ theta, PcgState *st, double *history, dd_pair *partials, unsigned int *counter) {
-  pdl_prologue();
   if (*(volatile int32_t *)&st->done) return;
   const double delta = st->delta;
   dd_pair v[2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -194,7 +192,6 @@ __global__ void pcg_budget_kernel(PcgState *st) {
 __global__ void __launch_bounds__(kVecThreads) pcg_pupdate_kernel(int64_t n, const double *__restrict__ theta,
                                                                   double *__restrict__ p, PcgState *st,
                                                                   int budget = 0, double *pmax = nullptr) {
-  pdl_prologue();
   if (*(volatile const int32_t *)&st->done) return;
   const double beta = st->beta;
   double m = 0.0;

@@ -40,7 +40,6 @@
 #include "laker_internal.h"
 #include "tma.cuh"
 #include "tri.cuh"
-#include "pdl.cuh"
 
 namespace laker {
 namespace {
@@ -86,7 +85,6 @@ constexpr int kMaxOffTiles = 512;  // products per row accumulator: nct kCPT
 template <bool ROWOFF>
 __global__ void __launch_bounds__(kSymThreads, 1)
     symv_dot2_kernel(const __grid_constant__ CUtensorMap tm, const SymvArgs a) {
-  pdl_prologue();
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   extern __shared__ __align__(128) unsigned char smem[];  // 128 B suffices for unswizzled TMA
   dd_pair *red = reinterpret_cast<dd_pair *>(smem + kSStages * kStageBytes);
@@ -326,7 +324,6 @@ __device__ __forceinline__ dd_pair ldcg_pair(const dd_pair *p) {
 
 template <int BR>
 __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
-  pdl_prologue();
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   __shared__ dd_pair sred[kFinThreads / 32];
   __shared__ dd_pair spart[kFinThreads / 32][32];
@@ -448,7 +445,6 @@ __global__ void rowmax_kernel(const double *__restrict__ A, int64_t n, int64_t l
 // parts[b] = max |x_i| over CTA b's grid-stride share
 __global__ void __launch_bounds__(256) absmax_parts_kernel(const double *__restrict__ x, int64_t n, double *parts,
                                                            const PcgState *state) {
-  pdl_prologue();
   if (state != nullptr && *(volatile const int32_t *)&state->done) return;
   __shared__ double sm[8];
   double m = 0.0;
@@ -659,16 +655,15 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     a.xparts = g.xparts;
     a.nxparts = g.nxparts;
   } else {
-    launch_pdl(absmax_parts_kernel, dim3(kXParts), dim3(256), 0, s, g.x, (int64_t)p->n, p->xparts,
-               (const PcgState *)g.state);
+    absmax_parts_kernel<<<dim3(kXParts), dim3(256), 0, s>>>(g.x, (int64_t)p->n, p->xparts, (const PcgState *)g.state);
     a.xparts = p->xparts;
     a.nxparts = kXParts;
   }
   if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
-    launch_pdl(symv_dot2_kernel<true>, dim3(p->grid), dim3(kSymThreads), kSymSmem, s, p->tm[which], a);
+    symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else
-    launch_pdl(symv_dot2_kernel<false>, dim3(p->grid), dim3(kSymThreads), kSymSmem, s, p->tm[which], a);
-  launch_pdl(symv_finalize_kernel<kSR>, dim3(p->fin_grid), dim3(kFinThreads), 0, s, a);
+    symv_dot2_kernel<false><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
+  symv_finalize_kernel<kSR><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
 }
 
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s) {

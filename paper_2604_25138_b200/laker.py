@@ -29,7 +29,7 @@ STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "DIMENSION_MISMATCH", 3: "NOT_READY
 STORE_MATERIALIZED, STORE_ON_THE_FLY = 0, 1
 MODE_FAST, MODE_EXACT = 0, 1
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_LEARNED, PRECOND_EXTERNAL_DENSE = 0, 1, 2, 3
-P_AUTO, P_DENSE, P_FACTORED = 0, 1, 2
+P_AUTO, P_DENSE, P_FACTORED, P_FACTORED_QM = 0, 1, 2, 3
 TERM_RESIDUAL_TOL, TERM_MAX_ITERS, TERM_ZERO_RHS, TERM_BREAKDOWN, TERM_INDEFINITE = 0, 1, 2, 3, 4
 
 EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_status_string",
@@ -106,7 +106,7 @@ def _load() -> ctypes.CDLL:
         "laker_apply_operator": [vp, vp, vp],
         "laker_get_stats": [vp, ctypes.POINTER(Stats)],
         "laker_debug_igemm_s8": [vp, vp, vp, i64, i64, i64],
-        "laker_debug_ozaki_gemm": [vp, vp, vp, i64, i64, i64, i32],
+        "laker_debug_ozaki_gemm": [vp, vp, vp, i64, i64, i64, i32, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -252,11 +252,11 @@ def laker_debug_igemm_s8(A, B, C) -> None:
         raise LakerError(s, "laker_debug_igemm_s8")
 
 
-def laker_debug_ozaki_gemm(A, B, C, slices: int = 0) -> None:
+def laker_debug_ozaki_gemm(A, B, C, slices: int = 0, kernel: int = -1) -> None:
     """C = A B^T in fp64 emulated on the int8 tensor cores; torch float64 CUDA tensors."""
     M, K = A.shape
     N = B.shape[0]
-    s = lib.laker_debug_ozaki_gemm(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, slices)
+    s = lib.laker_debug_ozaki_gemm(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, slices, kernel)
     if s != LAKER_OK:
         raise LakerError(s, "laker_debug_ozaki_gemm")
 

@@ -1,6 +1,6 @@
 """Staged oracle PCG for a factored LEARNED P taken from the GPU context: the QM form
-(R21, the default: theta = a^{-1/2} r + QM (Q^T r)) or the three-pass form
-Q (M (Q^T r)) (LAKER_P_3PASS=1), whichever the context applies."""
+(R21, p_layout AUTO / FACTORED_QM: theta = a^{-1/2} r + QM (Q^T r)) or the
+three-pass form Q (M (Q^T r)) (p_layout FACTORED), whichever the context applies."""
 import oracle as O
 
 

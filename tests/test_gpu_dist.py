@@ -55,24 +55,6 @@ def test_collective_path_equals_single(L, cid, n, kind):
         assert ro.iters == r1["iters"] and (ao == a1).all()
 
 
-def test_fused_iteration_equals_unfused(L):
-    """gemv.cu's fused two-kernel iteration (LAKER_FUSED=1) is the same recurrence."""
-    import os
-    P = make_problem(2)
-    c = L.Context(0)
-    c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
-    Z = np.asfortranarray(make_directions(2, P.n, P.n_dirs))
-    c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_DENSE)  # fused needs dense P
-    a0, r0, h0 = c.pcg_solve(P.y, P.tol, want_history=True)
-    os.environ["LAKER_FUSED"] = "1"
-    try:
-        a1, r1, h1 = c.pcg_solve(P.y, P.tol, want_history=True)
-    finally:
-        del os.environ["LAKER_FUSED"]
-    c.close()
-    assert r0[0]["iters"] == r1[0]["iters"] and (h0 == h1).all() and (a0 == a1).all()
-
-
 @pytest.mark.parametrize("W", [2, 4])
 def test_row_sharded_assembly_and_predict_layouts(L, W):
     """Detached shards (world = W, no communicator) on one GPU: each rank's K rows

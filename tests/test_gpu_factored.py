@@ -1,6 +1,7 @@
 """GPU parity of the factored LEARNED preconditioner:
-P = a^{-1/2} I + Q M Q^T kept as Q^T, Q and M (O4') and applied as
-three Dot2 GEMV passes, theta = a^{-1/2} r + Q (M (Q^T r)).
+P = a^{-1/2} I + Q M Q^T kept as Q^T, Q and M (O4') and applied either
+as three Dot2 GEMV passes, theta = a^{-1/2} r + Q (M (Q^T r)) (p_layout FACTORED),
+or in the QM form a^{-1/2} r + (Q M)(Q^T r) (R21; AUTO / FACTORED_QM).
 
 Staged parity (DESIGN.md §6 step 4): the oracle's PCG run with the GPU's own
 factors (exported through laker_get_preconditioner_factors) on the same K takes
@@ -34,14 +35,19 @@ def _bitwise(a, b, what=""):
     assert bad.size == 0, f"{what}: {bad.size} mismatches, first {bad[:5]}"
 
 
+LAYOUTS = {"3pass": (2, 1), "qm": (3, 2), "auto": (0, 2)}   # p_layout -> stats p_factored
+
+
+@pytest.mark.parametrize("layout", ["3pass", "auto"])
 @pytest.mark.parametrize("cid,n", [(1, None), (2, None), (3, 2048), (3, 1000)])
-def test_factored_staged_pcg_bitwise(ctx, L, cid, n):
+def test_factored_staged_pcg_bitwise(ctx, L, cid, n, layout):
     P = make_problem(cid, n=n)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
-    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    pl, pf = LAYOUTS[layout]
+    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=pl)
     st = ctx.stats()
-    assert rep["converged"] == 1 and st["p_factored"] in (1, 2) and st["n_dirs"] == P.n_dirs
+    assert rep["converged"] == 1 and st["p_factored"] == pf and st["n_dirs"] == P.n_dirs
     Q, M, ainv = ctx.get_preconditioner_factors()
     # Q has orthonormal columns (thin QR of Ubar) and M is symmetric
     assert np.abs(Q.T @ Q - np.eye(P.n_dirs)).max() <= 1e-10
@@ -58,24 +64,26 @@ def test_factored_staged_pcg_bitwise(ctx, L, cid, n):
         assert np.linalg.norm(ag - ref) / np.linalg.norm(ref) <= 1e-6
 
 
-@pytest.mark.parametrize("cid,n", [(2, None), (3, 1000)])
-def test_factored_symmetric_M_staged_bitwise(ctx, L, monkeypatch, cid, n):
-    """LAKER_MSYM=1: w = M z through the symmetric GEMV (M is formed bitwise
-    symmetric) -- the same Dot2-exact row sums, so the staged parity stays bitwise."""
-    monkeypatch.setenv("LAKER_MSYM", "1")
-    monkeypatch.setenv("LAKER_P_3PASS", "1")  # the M pass exists only in the three-pass form
-    P = make_problem(cid, n=n)
+@pytest.mark.parametrize("cid", [1, 2])
+def test_qm_product_matches_factors(ctx, L, cid):
+    """The QM form's n x N_r product (formed once at fit time by the int8-emulated GEMM,
+    B8) is Q @ M of the exported factors to fp64-GEMM accuracy: a transposed, mis-padded
+    or mis-sliced QM would fail here even though staged parity (which feeds the oracle
+    the GPU's own QM) could not see it."""
+    P = make_problem(cid)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(cid, P.n, P.n_dirs))
     ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    assert ctx.stats()["p_factored"] == 2
     Q, M, ainv = ctx.get_preconditioner_factors()
-    assert (M == M.T).all()
-    K, _ = O.assemble(P.E, P.scale)
-    ag, reps, hist = ctx.pcg_solve(P.y, P.tol, want_history=True)
-    ao, ro = oracle_pcg_factored(ctx, K, P.lam, P.y, Q, M, ainv, tol=P.tol)
-    assert reps[0]["iters"] == ro.iters
-    _bitwise(hist, ro.history, "history")
-    _bitwise(ag, ao, "alpha")
+    QM = ctx.get_preconditioner_qm()
+    ref = Q @ M
+    assert np.abs(QM - ref).max() <= 1e-13 * np.abs(QM).max()
+    # the three-pass fit of the same K and Z exports the same factors and no QM
+    ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_FACTORED)
+    assert ctx.stats()["p_factored"] == 1 and ctx.get_preconditioner_qm() is None
+    Q3, M3, a3 = ctx.get_preconditioner_factors()
+    assert (Q3 == Q).all() and (M3 == M).all() and a3 == ainv
 
 
 def test_factored_equals_dense_layout_P(ctx, L):
@@ -97,17 +105,18 @@ def test_factored_equals_dense_layout_P(ctx, L):
     assert abs(rf[0]["iters"] - rd[0]["iters"]) <= 0.05 * rd[0]["iters"] + 2
 
 
-def test_factored_block_solve_T18(ctx, L, monkeypatch):
-    """nrhs > 1 (block solve, C4 path) applies the factored P as three Dot2 GEMMs
-    (Z = Q^T R, W = M Z, Theta = Q W + a^{-1/2} R): every column equals the
-    single-RHS factored solve bitwise (T18) and solves the system (R14).  T18 is a
-    property of the three-pass form (the QM opt-in, R21, is single-RHS only)."""
-    monkeypatch.setenv("LAKER_P_3PASS", "1")
+@pytest.mark.parametrize("layout", ["3pass", "auto"])
+def test_factored_block_solve_T18(ctx, L, layout):
+    """nrhs > 1 (block solve, C4 path) applies the factored P in the single-RHS solve's
+    form as Dot2 GEMMs (three passes: Z = Q^T R, W = M Z, Theta = Q W + a^{-1/2} R; QM
+    form: Z = Q^T R, Theta = QM Z + a^{-1/2} R): every column equals the single-RHS
+    factored solve bitwise (T18) and solves the system (R14)."""
     P = make_problem(1)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     Z = np.asfortranarray(make_directions(1, P.n, P.n_dirs))
-    ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
-    assert ctx.stats()["p_factored"] in (1, 2)
+    pl, pf = LAYOUTS[layout]
+    ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=pl)
+    assert ctx.stats()["p_factored"] == pf
     Y = np.stack([P.y, -0.5 * P.y, np.roll(P.y, 7)], axis=1)
     A, reps, _ = ctx.pcg_solve(Y, P.tol)
     K, _ = O.assemble(P.E, P.scale)

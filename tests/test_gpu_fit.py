@@ -7,7 +7,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
-from synth import make_problem, make_directions  # noqa: E402
+from synth import make_problem, make_directions, make_paper_problem  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -114,3 +114,46 @@ def test_fit_c3_full_size(ctx, L):
     _, rj, _ = ctx.pcg_solve(P.y, P.tol)
     assert rl[0]["termination"] == rj[0]["termination"] == L.TERM_RESIDUAL_TOL
     assert rl[0]["iters"] < rj[0]["iters"]
+
+
+@pytest.mark.parametrize("n", [50, 64])
+def test_fit_full_rank_directions_matches_oracle(ctx, L, n):
+    """N_r = n (the paper regime's small n, "when N_r >= n"): Sigma_t = Q T_t Q^T with
+    Q square, so the R6 trigger reads lambda_min(T_t), not a_t; GPU and oracle must take
+    the same rho at every step and reach the same P."""
+    P = make_paper_problem(n)
+    assert P.n_dirs == n
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    K, _ = O.assemble(P.E, P.scale)
+    Z = np.asfortranarray(make_directions(0, P.n, P.n_dirs))
+    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+    Po, ro, st = O.cccp_fit_structured(K, P.lam, Z)
+    assert rep["converged"] == 1 and ro.converged
+    assert abs(rep["iters"] - ro.iters) <= 1
+    assert rep["rho_used"] == ro.rho_used
+    Pg = ctx.get_preconditioner_rows()
+    assert np.linalg.norm(Pg - Po) / np.linalg.norm(Po) <= 1e-8
+
+
+def test_fit_rho_trigger_full_rank_reads_lambda_min_T(ctx, L):
+    """N_r = n with gamma = 1e-7, rho_floor = 1e-9 on a well-conditioned K: a_t ~ 1e-7 stays
+    below the R6 threshold 1e-6 while lambda_min(Sigma_t) = lambda_min(T_t) ~ 6e-5 does not,
+    so the trigger must not fire (rho stays 1e-9 on both sides; a trigger read from a_t
+    would set rho = 0.2 at every step)."""
+    n = 48
+    r = np.random.default_rng(7)
+    B = r.standard_normal((n, n))
+    K = B @ B.T / n + 0.5 * np.eye(n)
+    K = 0.5 * (K + K.T)
+    Z = r.standard_normal((n, n))
+    E = np.zeros((n, 4))
+    ctx.assemble_kernel(E, 1.0, 0.1, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    ctx.load_kernel_rows(K)
+    kw = dict(gamma=1e-7, rho_floor=1e-9, max_iters=30)
+    rep = ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=n, Z=np.asfortranarray(Z), **kw)
+    Po, ro, st = O.cccp_fit_structured(K, 0.1, Z, **kw)
+    assert ro.rhos == [1e-9] * 30 and st.a < 1e-6 < ro.sigma_min_eig
+    assert rep["iters"] == ro.iters == 30
+    assert rep["rho_used"] == 1e-9
+    Pg = ctx.get_preconditioner_rows()
+    assert np.linalg.norm(Pg - Po) / np.linalg.norm(Po) <= 1e-8

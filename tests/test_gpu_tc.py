@@ -61,7 +61,7 @@ def test_ozaki_gemm_accuracy(M, N, K, S):
 
 @pytest.mark.parametrize("M,N,K,S", [(256, 384, 512, 8), (300, 130, 1000, 8), (128, 256, 4096, 7),
                                      (257, 129, 96, 5), (129, 200, 640, 3)])
-def test_ozaki_level_group_kernel_equals_fused(M, N, K, S, monkeypatch):
+def test_ozaki_level_group_kernel_equals_fused(M, N, K, S):
     """The level-group kernel (each K chunk's slices loaded once, all pairs of <= 4
     levels into resident TMEM buffers) issues the same exact int32 level sums and
     accumulates them in the same fp64 order as the level-streaming kernel: bitwise
@@ -73,8 +73,6 @@ def test_ozaki_level_group_kernel_equals_fused(M, N, K, S, monkeypatch):
     B = torch.from_numpy(r.standard_normal((N, K))).cuda()
     C1 = torch.zeros((M, N), dtype=torch.float64, device="cuda")
     C2 = torch.zeros((M, N), dtype=torch.float64, device="cuda")
-    monkeypatch.setenv("LAKER_OZAKI_LV", "1")
-    L.laker_debug_ozaki_gemm(A, B, C1, S)
-    monkeypatch.setenv("LAKER_OZAKI_LV", "0")
-    L.laker_debug_ozaki_gemm(A, B, C2, S)
+    L.laker_debug_ozaki_gemm(A, B, C1, S, kernel=1)
+    L.laker_debug_ozaki_gemm(A, B, C2, S, kernel=0)
     assert torch.equal(C1, C2)
