@@ -130,6 +130,7 @@ def cpu_baseline_sample(prob, iters: int = 48):
     dense P (identity stored densely -- the same per-iteration work, two Dot2
     GEMVs over n^2 entries, as the learned P), `iters` iterations; K assembled
     by the oracle beforehand (its time reported separately)."""
+    _oracle_threads()
     import oracle as O
     t0 = time.perf_counter()
     K, _ = O.assemble(prob.E, prob.scale)
@@ -146,10 +147,18 @@ def cpu_baseline_sample(prob, iters: int = 48):
             "seconds": dt, "assembly_s": t_asm}
 
 
+def _oracle_threads():
+    """torchrun sets OMP_NUM_THREADS=1 per rank; the oracle (rank 0 only) uses the host's
+    cores.  Must run before the oracle library is loaded."""
+    if "oracle" not in sys.modules:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle, as it stands, on the host cores."""
     if rank != 0:
         return
+    _oracle_threads()
     from synth import make_problem
     import oracle as O
     prob = make_problem(3)
@@ -346,7 +355,19 @@ def main():
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` launches its own N ranks (one process per GPU) the way
+        # the driver does, and returns their exit status
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

@@ -211,10 +211,13 @@ laker_status laker_set_preconditioner(laker_ctx ctx, int kind, const double *dat
 laker_status laker_get_preconditioner_rows(laker_ctx ctx, double *P_rows);
 /* LEARNED P in factored form: Q (n x n_dirs row-major), M (n_dirs x n_dirs
    row-major) and the scalar a^{-1/2} (host), so that P = a^{-1/2} I + Q M Q^T;
-   any pointer may be NULL.  NOT_READY if the context holds no factored P. */
+   any pointer may be NULL.  NOT_READY if the context holds no factored P.  A
+   row-sharded context keeps only its part of the factors: Q is then its rows
+   [r n/W, (r+1) n/W) (n/W x n_dirs); M is whole. */
 laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *M, double *a_inv_sqrt);
 /* The product QM = Q M (n x n_dirs row-major, host or device) the factored apply uses
-   (R21: theta = a^{-1/2} r + QM (Q^T r), two Dot2 passes).  NOT_READY if the
+   (R21: theta = a^{-1/2} r + QM (Q^T r), two Dot2 passes; a row-sharded
+   context: its n/W rows).  NOT_READY if the
    context holds no factored P in QM form (a fit with p_layout FACTORED keeps three
    passes), INVALID_ARGUMENT for NULL. */
 laker_status laker_get_preconditioner_qm(laker_ctx ctx, double *QM);
@@ -233,6 +236,26 @@ laker_status laker_debug_igemm_s8(const int8_t *A, const int8_t *B, int32_t *C, 
    (bitwise the same result; the choice exists for that test). */
 laker_status laker_debug_ozaki_gemm(const double *A, const double *B, double *C, int64_t M, int64_t N, int64_t K,
                                     int32_t slices, int32_t kernel);
+
+/* Test hooks of the row-sharded symmetric K apply (pcg_dist.cu, symv.cu).
+   laker_debug_dist_tiles (host only, no GPU): the tile lists rank `rank` of `world`
+   streams for an n x n symmetric matrix in br x tc tiles -- counts[0..2] = local
+   block-rows L, tiles T, column tiles; toff [L+1], jt [T], cr_lo / cr_hi [n/tc] (any
+   output NULL to query the counts).  INVALID_ARGUMENT unless n/world is a multiple of br
+   (2 br for even world > 1).
+   laker_debug_dist_symv_partials: on a context whose K uses the sharded symmetric apply
+   (EXACT assembly, n/W % 256 == 0; a detached shard works), x (n) -> pairs (2 n: the
+   unrounded (s, c) pair of this rank's partial sum of every row); rowmax (n: max_j |K_ij|
+   of all rows) replaces the all-gathered row maxima a detached shard cannot form (NULL:
+   keep).  laker_debug_dist_symv_combine: own (2 n/W: this rank's pairs of its rows) and
+   recv (2 (W/2) n/W: the pairs of its rows from ranks w-1, ..., w-W/2) -> q_loc (n/W) =
+   the rows of (lambda I + K) x, and pq_pair (2, may be NULL) = the unrounded x_loc.q_loc.
+   All vectors host or device, synchronous. */
+laker_status laker_debug_dist_tiles(int64_t n, int32_t br, int32_t tc, int32_t rank, int32_t world, int64_t *counts,
+                                    int64_t *toff, int32_t *jt, int32_t *cr_lo, int32_t *cr_hi);
+laker_status laker_debug_dist_symv_partials(laker_ctx ctx, const double *x, const double *rowmax, double *pairs);
+laker_status laker_debug_dist_symv_combine(laker_ctx ctx, const double *x, const double *own, const double *recv,
+                                           double *q_loc, double *pq_pair);
 
 typedef struct {
   int64_t n, local_rows, ld;     /* problem size, rows held, padded row stride (doubles) */

@@ -370,6 +370,7 @@ void free_factors(laker_ctx ctx) {
   cudaFree(ctx->fz);
   ctx->Qt = ctx->Qr = ctx->Mf = ctx->fz = ctx->fw = nullptr;
   ctx->p_factored = false;
+  ctx->f_local = false;
   ctx->f_nr = ctx->f_nrp = ctx->f_ldq = 0;
   ctx->f_alloc_nrp = ctx->f_alloc_n = 0;
 }
@@ -416,6 +417,8 @@ laker_status form_dense_p(laker_ctx ctx, const double *Ut, const double *Mm, int
 
 laker_status ensure_dense_p(laker_ctx ctx) {
   if (ctx->P || !ctx->p_factored) return LAKER_OK;
+  if (ctx->f_local && ctx->world > 1)
+    return set_err(ctx, LAKER_ERR_NOT_READY, "dense P rows: the sharded context keeps only its part of the factors");
   LAKER_TRY(form_dense_p(ctx, ctx->Qt, ctx->Mf, ctx->f_ldq, ctx->f_nrp, ctx->f_ainv));
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return LAKER_OK;
@@ -846,21 +849,34 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       ctx->P = nullptr;
     }
     const int64_t ldq = (nrp + 255) / 256 * 256;  // gemv streams whole 256-column chunks
+    // row-sharded context: every rank keeps only its own part -- Q^T's
+    // columns [r0, r1) (nrp x ldl), Q's and QM's rows [r0, r1) -- so a P apply streams
+    // 16 (n/W) N_r bytes per rank; M (N_r^2) is kept whole.  One rank: all of it.
+    const bool loc = ctx->comm != nullptr || ctx->world > 1;
+    const int64_t r0 = loc ? ctx->r0 : 0, nloc = loc ? ctx->r1 - ctx->r0 : n;
+    const int64_t ldl = loc ? padded_ld(nloc) : ld;
     if (!(ctx->Qt && ctx->f_alloc_nrp == nrp && ctx->f_alloc_n == n)) {
       free_factors(ctx);
-      LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ld * 8));
-      LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)n * ldq * 8));
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->Qt, (size_t)nrp * ldl * 8));
+      LAKER_CUDA(ctx, cudaMalloc(&ctx->Qr, (size_t)nloc * ldq * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->Mf, (size_t)nrp * ldq * 8));
       LAKER_CUDA(ctx, cudaMalloc(&ctx->fz, (size_t)2 * ldq * 8));
       ctx->f_alloc_nrp = nrp;
       ctx->f_alloc_n = n;
     }
+    ctx->f_local = loc;
+    ctx->f_ldl = ldl;
     ctx->fw = ctx->fz + ldq;
-    LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Qr, 0, (size_t)n * ldq * 8, s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Qr, 0, (size_t)nloc * ldq * 8, s));
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Mf, 0, (size_t)nrp * ldq * 8, s));
     LAKER_CUDA(ctx, cudaMemsetAsync(ctx->fz, 0, (size_t)2 * ldq * 8, s));
-    LAKER_CUDA(ctx, cudaMemcpyAsync(ctx->Qt, Ut, (size_t)nrp * ld * 8, cudaMemcpyDeviceToDevice, s));
-    launch_transpose(Ut, nrp, n, ld, ctx->Qr, ldq, s);
+    if (loc) {
+      LAKER_CUDA(ctx, cudaMemsetAsync(ctx->Qt, 0, (size_t)nrp * ldl * 8, s));
+      LAKER_CUDA(ctx, cudaMemcpy2DAsync(ctx->Qt, ldl * 8, Ut + r0, ld * 8, nloc * 8, nrp, cudaMemcpyDeviceToDevice, s));
+    } else {
+      LAKER_CUDA(ctx, cudaMemcpyAsync(ctx->Qt, Ut, (size_t)nrp * ld * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    launch_transpose(Ut + r0, nrp, nloc, ld, ctx->Qr, ldq, s);
     LAKER_CUDA(ctx, cudaMemcpy2DAsync(ctx->Mf, ldq * 8, Zm, nrp * 8, nrp * 8, nrp, cudaMemcpyDeviceToDevice, s));
     ++L;
     // QM = Q M (reading R21): the apply becomes two passes, a^-1/2 r + QM (Q^T r) --
@@ -873,10 +889,10 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       ctx->QMf = nullptr;
     }
     if (ctx->p_qm) {
-      if (!ctx->QMf) LAKER_CUDA(ctx, cudaMalloc(&ctx->QMf, (size_t)n * ldq * 8));
-      LAKER_CUDA(ctx, cudaMemsetAsync(ctx->QMf, 0, (size_t)n * ldq * 8, s));
+      if (!ctx->QMf) LAKER_CUDA(ctx, cudaMalloc(&ctx->QMf, (size_t)nloc * ldq * 8));
+      LAKER_CUDA(ctx, cudaMemsetAsync(ctx->QMf, 0, (size_t)nloc * ldq * 8, s));
       GemmArgs g{};
-      g.M = n;
+      g.M = nloc;
       g.N = nrp;
       g.K = nrp;
       g.A = ctx->Qr;

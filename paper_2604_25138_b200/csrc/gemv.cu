@@ -227,9 +227,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
           const int64_t gi = a.row0 + rb + R;
           const double xi = a.xd != nullptr ? a.xd[gi] : xrow[R];
           if (a.lambda != 0.0) dot2_step(t, a.lambda, xi);  // the lambda x_i term of the row
-          const double yv = pair_value(t);
-          a.y[rb + R] = yv;
-          dot2_step(part, xi, yv);
+          if (a.ypair != nullptr) {
+            a.ypair[rb + R] = t;  // unrounded row pair (sharded partial sums, pcg_dist.cu)
+          } else {
+            const double yv = pair_value(t);
+            a.y[rb + R] = yv;
+            dot2_step(part, xi, yv);
+          }
         }
       }
     }

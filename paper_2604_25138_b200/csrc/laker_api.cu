@@ -22,16 +22,35 @@ laker_status cuda_err(laker_ctx ctx, cudaError_t e, const char *what) {
   return set_err(ctx, e == cudaErrorMemoryAllocation ? LAKER_ERR_OUT_OF_MEMORY : LAKER_ERR_CUDA, m);
 }
 
-// The symmetric GEMV (symv.cu) is selected for K (which = 0) or P (which = 1)
-// only on a single rank, for a materialized matrix that a device check finds
-// bitwise symmetric.  LAKER_SYMV=0 disables it (A/B measurements).
-laker_status refresh_symmetry(laker_ctx ctx, int which) {
+// The symmetric GEMV (symv.cu) is selected for K (which = 0) or P (which = 1) on a
+// single rank for a materialized matrix that a device check finds bitwise symmetric.
+// Row-sharded (world > 1), where no rank sees the whole matrix, it is selected for K
+// only when the rows are symmetric by construction (EXACT assembly: K_ij and K_ji are
+// the same correctly rounded operations, assemble.cu) and n / W is a multiple of 256;
+// each rank then streams its tiles of tri_plan_dist and the row maxima of all n rows
+// are all-gathered.  LAKER_SYMV=0 disables it (A/B measurements).
+laker_status refresh_symmetry(laker_ctx ctx, int which, bool symmetric_rows) {
   bool &flag = which == 0 ? ctx->k_sym : ctx->p_sym;
   flag = false;
   const double *A = which == 0 ? ctx->K : ctx->P;
-  if (!A || ctx->world != 1 || ctx->storage != LAKER_STORE_MATERIALIZED) return LAKER_OK;
+  if (!A || ctx->storage != LAKER_STORE_MATERIALIZED) return LAKER_OK;
   const char *env = std::getenv("LAKER_SYMV");
   if (env && env[0] == '0') return LAKER_OK;
+  if (ctx->world > 1 || ctx->comm) {
+    const int64_t nloc = ctx->n / ctx->world;
+    if (which != 0 || !symmetric_rows || nloc % 256 != 0) return LAKER_OK;
+    LAKER_CUDA(ctx, symv_plan(ctx->symv, ctx->n, ctx->ld, ctx->num_sms, ctx->rank, ctx->world, true));
+    if (!symv_bind(ctx->symv, 0, A)) return LAKER_OK;
+    symv_rowmax(ctx->symv, 0, A, ctx->stream);
+    ctx->stats.kernel_launches++;
+    if (ctx->comm) {
+      double *rm = symv_rowmax_ptr(ctx->symv, 0);
+      LAKER_NCCL(ctx, ncclAllGather(rm + ctx->r0, rm, nloc, ncclDouble, ctx->comm, ctx->stream));
+    }
+    LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    flag = true;
+    return LAKER_OK;
+  }
   LAKER_CUDA(ctx, symv_plan(ctx->symv, ctx->n, ctx->ld, ctx->num_sms));
   int *dflag = reinterpret_cast<int *>(ctx->flags + 2);
   LAKER_CUDA(ctx, cudaMemsetAsync(dflag, 0, sizeof(int), ctx->stream));
@@ -381,7 +400,7 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
   ctx->assembled = true;
   LAKER_CUDA(ctx, laker::otf_sym_prepare(ctx));
   if (hf[1] > 0) return set_err(ctx, LAKER_ERR_OVERFLOW, "scale*<e_i,e_j> exceeded ln(DBL_MAX)");
-  LAKER_TRY(laker::refresh_symmetry(ctx, 0));
+  LAKER_TRY(laker::refresh_symmetry(ctx, 0, mode == LAKER_MODE_EXACT));
   return LAKER_OK;
 }
 
@@ -519,7 +538,7 @@ laker_status laker_load_kernel_rows(laker_ctx ctx, const double *K_rows) {
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   free_dev(ctx, ctx->Pdiag);  // Jacobi diagonal derived from E no longer matches
   if (ctx->precond_kind == LAKER_PRECOND_JACOBI) ctx->precond_kind = LAKER_PRECOND_NONE;
-  return laker::refresh_symmetry(ctx, 0);
+  return laker::refresh_symmetry(ctx, 0, false);
 }
 
 laker_status laker_get_kernel_rows(laker_ctx ctx, double *K_rows) {
@@ -590,7 +609,7 @@ laker_status laker_get_preconditioner_factors(laker_ctx ctx, double *Q, double *
   CHECK_CTX(ctx);
   if (!ctx->p_factored) return set_err(ctx, LAKER_ERR_NOT_READY, "no factored preconditioner");
   cudaSetDevice(ctx->device);
-  const int64_t n = ctx->n, nr = ctx->f_nr;
+  const int64_t n = ctx->f_local ? ctx->r1 - ctx->r0 : ctx->n, nr = ctx->f_nr;  // sharded: own rows of Q
   if (Q)
     LAKER_CUDA(ctx, cudaMemcpy2DAsync(Q, nr * sizeof(double), ctx->Qr, ctx->f_ldq * sizeof(double),
                                       nr * sizeof(double), n, cudaMemcpyDefault, ctx->stream));
@@ -625,7 +644,7 @@ laker_status laker_get_preconditioner_qm(laker_ctx ctx, double *QM) {
   if (!ctx->p_factored || !ctx->p_qm) return set_err(ctx, LAKER_ERR_NOT_READY, "no QM-form factored preconditioner");
   if (!QM) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "get_preconditioner_qm: NULL");
   cudaSetDevice(ctx->device);
-  const int64_t n = ctx->n, nr = ctx->f_nr;
+  const int64_t n = ctx->f_local ? ctx->r1 - ctx->r0 : ctx->n, nr = ctx->f_nr;  // sharded: own rows of QM
   LAKER_CUDA(ctx, cudaMemcpy2DAsync(QM, nr * sizeof(double), ctx->QMf, ctx->f_ldq * sizeof(double),
                                     nr * sizeof(double), n, cudaMemcpyDefault, ctx->stream));
   LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -107,9 +107,13 @@ struct laker_ctx_s {
   bool k_sym = false, p_sym = false;
   // factored LEARNED P = f_ainv I + Q M Q^T (fit.cu; applied in pcg.cu)
   bool p_factored = false;
+  // one rank: Qt = nrp x ld (row k = q_k), Qr / QMf = n x f_ldq; sharded (f_local): Qt holds
+  // the columns [r0, r1) (nrp x f_ldl), Qr / QMf the rows [r0, r1); M is always whole
   double *Qt = nullptr;             // nrp x ld   (row k = q_k, zero padded)
   double *Qr = nullptr;             // n x f_ldq  (row i = Q_i., zero padded)
   double *QMf = nullptr;            // n x f_ldq  QM = Q M (R21: theta = a^-1/2 r + QM (Q^T r))
+  bool f_local = false;
+  int64_t f_ldl = 0;
   bool p_qm = false;                // the factored apply uses QMf (two passes)
   double *Mf = nullptr;             // nrp x f_ldq
   double *fz = nullptr, *fw = nullptr;  // f_ldq workspaces (z = Q^T r, w = M z), zero padded
@@ -172,6 +176,8 @@ struct GemvArgs {
   // null -> launch_symv computes them
   const double *xparts;
   int nxparts;
+  // symv on a row-sharded plan: the unrounded pair of every row i < n (pcg_dist.cu)
+  dd_pair *ypair;
 };
 void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
 void gemv_init();
@@ -181,7 +187,12 @@ size_t gemv_smem_bytes();
 // ----------------------------------------------------------------- symv.cu
 // Symmetric Dot2 GEMV over the block upper triangle (half the bytes of gemv.cu),
 // same outputs and epilogues, bitwise equal rows.  which = 0 (K) / 1 (P).
-cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms);
+// world > 1: the row-sharded plan of rank `rank` (tri_plan_dist); the matrix holds the
+// rank's n / W rows and launch_symv writes GemvArgs::ypair instead of y
+cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms, int rank = 0, int world = 1,
+                      bool dist = false);
+bool tri_is_dist(const SymvPlan *p);
+double *symv_rowmax_ptr(SymvPlan *p, int which);
 void symv_free(SymvPlan *&p);
 bool symv_bind(SymvPlan *p, int which, const double *A);
 void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s);
@@ -195,7 +206,9 @@ bool launch_operator_otf_sym(laker_ctx ctx, const double *p, double *q, PcgState
                              cudaStream_t s);
 size_t symv_smem_bytes();
 // set ctx->k_sym / p_sym: bitwise-symmetry check of the (whole, single-rank) matrix
-laker_status refresh_symmetry(laker_ctx ctx, int which);
+// symmetric_rows: the rows are bitwise symmetric by construction (sharded contexts
+// cannot check it)
+laker_status refresh_symmetry(laker_ctx ctx, int which, bool symmetric_rows = false);
 
 // -------------------------------------------------------------- assemble.cu
 // emax: max_k |e_ik| per row of E (launch_rowabsmax), the offsets of the compensated dots
@@ -375,6 +388,13 @@ laker_status apply_operator_dist(laker_ctx ctx, const double *x, double *y);
 // nrhs independent recurrences sharing GEMM-shaped applies (multi-RHS, C4).
 laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *alpha,
                              const laker_solve_opts &o, laker_solve_report *reps, double *history);
+// the row-sharded version (ctx->comm): K / P / vectors by row blocks, rank-order combines
+laker_status pcg_solve_block_dist(laker_ctx ctx, int32_t m, const double *Y, double *alpha,
+                                  const laker_solve_opts &o, laker_solve_report *reps, double *history);
+// wait for an event / the stream while watching the communicator for asynchronous NCCL
+// errors (on one: ncclCommAbort, ctx->comm = null, LAKER_ERR_NCCL) -- pcg_dist.cu
+laker_status dist_wait(laker_ctx ctx, cudaEvent_t ev);
+laker_status dist_sync(laker_ctx ctx, cudaStream_t s);
 laker_status nccl_err(laker_ctx ctx, ncclResult_t r, const char *what);
 
 #define LAKER_NCCL(ctx, call)                                        \

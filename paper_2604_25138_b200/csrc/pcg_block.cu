@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict
                                                         const int32_t *__restrict__ all_done,
                                                         const double *__restrict__ Xd,
                                                         const double *__restrict__ rmax,
-                                                        const double *__restrict__ cmax) {
+                                                        const double *__restrict__ cmax,
+                                                        dd_pair *__restrict__ Qpair = nullptr) {
   if (all_done && *(volatile const int32_t *)all_done) return;
   __shared__ double As[kBR][kBK + 1];
   __shared__ __align__(16) double Xs[kBK][kBM];
@@ -165,7 +166,10 @@ __global__ void __launch_bounds__(256) gemm_dot2_kernel(const double *__restrict
           v = tot[a][b];
         }
         if (lambda != 0.0) dot2_step(v, lambda, Xd[(row0 + R0 + tr + a) * ldx + C0 + tc + b]);
-        Q[(R0 + tr + a) * ldq + C0 + tc + b] = pair_value(v);
+        if (Qpair)  // unrounded entry (row-sharded partial products, pcg_solve_block_dist)
+          Qpair[(R0 + tr + a) * ldq + C0 + tc + b] = v;
+        else
+          Q[(R0 + tr + a) * ldq + C0 + tc + b] = pair_value(v);
       }
 }
 
@@ -183,6 +187,9 @@ struct BlockArgs {
   double *true_rel;    // [m]
   dd_pair *partials;   // [grid][m][2]
   unsigned int *counter;
+  int64_t ldy;         // column stride of Y (n; the row-sharded solve passes Y + r0)
+  double *pair_out;    // row-sharded: the last block stores the unrounded column pairs
+                       // [m][2] here instead of running the column epilogue
 };
 
 __device__ void column_epilogue(const BlockArgs &a, int col, dd_pair t0, dd_pair t1);
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(256) block_col_kernel(const BlockArgs a) {
       const int64_t e = i * a.ldv + c;
       switch (a.mode) {
         case kColInit: {  // alpha = 0, r = y, ||y||^2; theta^0 = P r (none/jacobi), p = theta, rho
-          const double yi = a.Y[i + c * a.n];
+          const double yi = a.Y[i + c * a.ldy];
           a.alpha[e] = 0.0;
           a.r[e] = yi;
           dot2_step(v0, yi, yi);
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(256) block_col_kernel(const BlockArgs a) {
           dot2_step(v0, a.r[e], a.theta[e]);
           break;
         case kColTrue: {
-          const double t = __dsub_rn(a.Y[i + c * a.n], a.q[e]);
+          const double t = __dsub_rn(a.Y[i + c * a.ldy], a.q[e]);
           dot2_step(v0, t, t);
           break;
         }
@@ -307,10 +314,19 @@ __global__ void __launch_bounds__(256) block_col_kernel(const BlockArgs a) {
         pair_add(s0, red[g * m + threadIdx.x][0]);
         pair_add(s1, red[g * m + threadIdx.x][1]);
       }
-      column_epilogue(a, threadIdx.x, s0, s1);
+      if (a.pair_out) {
+        double *o = a.pair_out + 4 * threadIdx.x;
+        o[0] = s0.s; o[1] = s0.c; o[2] = s1.s; o[3] = s1.c;
+      } else {
+        column_epilogue(a, threadIdx.x, s0, s1);
+      }
     }
   }
   __syncthreads();
+  if (last && threadIdx.x == 0 && a.pair_out) {
+    *a.counter = 0u;
+    return;
+  }
   if (last && threadIdx.x == 0) {
     int all = 1;
     for (int k = 0; k < (int)m; ++k) all &= a.st[k].done != 0;
@@ -398,6 +414,48 @@ __device__ void column_epilogue(const BlockArgs &a, int col, dd_pair t0, dd_pair
   }
 }
 
+// Row-sharded block solve: the W gathered [m][2] column pairs -> summed in rank order,
+// then the column epilogue of `a.mode` (identical on every rank), then all_done.
+__global__ void block_combine_kernel(const BlockArgs a, const double *__restrict__ recv, int W) {
+  if (a.mode != kColTrue && a.mode != kColInit && *(volatile int32_t *)a.all_done) return;
+  const int c = threadIdx.x;
+  if (c < a.m) {
+    dd_pair t0 = {0.0, 0.0}, t1 = {0.0, 0.0};
+    for (int w = 0; w < W; ++w) {
+      const double *o = recv + (int64_t)w * 4 * a.m + 4 * c;
+      pair_add(t0, dd_pair{o[0], o[1]});
+      pair_add(t1, dd_pair{o[2], o[3]});
+    }
+    column_epilogue(a, c, t0, t1);
+  }
+  __syncthreads();
+  if (c == 0) {
+    int all = 1;
+    for (int k = 0; k < (int)a.m; ++k) all &= a.st[k].done != 0;
+    *a.all_done = all;
+  }
+}
+
+// Z (nrp x ldz) = the rank-order sum of the W gathered partial products (EXACT: unrounded
+// pairs, rounded once; FAST: fp64 values summed in rank order)
+__global__ void block_zcombine_kernel(int64_t rows, int64_t m, int64_t ldz, const double *__restrict__ recv, int W,
+                                      int pairs, double *__restrict__ Z, const int32_t *all_done) {
+  if (*(volatile const int32_t *)all_done) return;
+  const int64_t per = rows * ldz * (pairs ? 2 : 1);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * ldz; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e % ldz >= m) continue;
+    if (pairs) {
+      dd_pair t = {0.0, 0.0};
+      for (int w = 0; w < W; ++w) pair_add(t, dd_pair{recv[w * per + 2 * e], recv[w * per + 2 * e + 1]});
+      Z[e] = pair_value(t);
+    } else {
+      double t = recv[e];
+      for (int w = 1; w < W; ++w) t = __dadd_rn(t, recv[w * per + e]);
+      Z[e] = t;
+    }
+  }
+}
+
 // p = theta + beta p for active columns; p = theta at init (dense)
 __global__ void block_pupdate_kernel(int64_t n, int64_t m, int64_t ldv, const double *__restrict__ theta,
                                      double *__restrict__ p, const PcgState *st, int init,
@@ -415,7 +473,8 @@ __global__ void block_pupdate_kernel(int64_t n, int64_t m, int64_t ldv, const do
 
 laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *alpha_out,
                              const laker_solve_opts &o, laker_solve_report *reps, double *history) {
-  if (ctx->world != 1 || ctx->comm) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS: single rank only in this version");
+  if (ctx->comm) return pcg_solve_block_dist(ctx, m, Y, alpha_out, o, reps, history);
+  if (ctx->world != 1) return set_err(ctx, LAKER_ERR_NOT_READY, "multi-RHS: detached shard (no NCCL communicator)");
   if (ctx->storage != LAKER_STORE_MATERIALIZED) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS needs MATERIALIZED");
   if (m > 256) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS: nrhs <= 256");
   const int64_t n = ctx->n, ld = ctx->ld;
@@ -460,7 +519,7 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   BlockArgs ba{};
   ba.n = n; ba.m = m; ba.ldv = mp; ba.pk = pk; ba.Y = Y; ba.alpha = al; ba.r = rr; ba.theta = th; ba.p = pp;
   ba.q = qq; ba.dvec = ctx->Pdiag; ba.st = st; ba.hist = hist; ba.all_done = all_done; ba.true_rel = trel;
-  ba.partials = parts; ba.counter = ctx->counters + kCtrMisc;
+  ba.partials = parts; ba.counter = ctx->counters + kCtrMisc; ba.ldy = n;
   auto col = [&](int mode) {
     BlockArgs b = ba;
     b.mode = mode;
@@ -677,6 +736,242 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   oz_slices_free(sXn, s);
   oz_slices_free(sXr, s);
   if (mxb) cudaFreeAsync(mxb, s);
+  cudaFreeAsync(st, s);
+  cudaFreeAsync(hist, s);
+  cudaFreeAsync(trel, s);
+  cudaFreeAsync(all_done, s);
+  cudaFreeAsync(parts, s);
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  if (worst == LAKER_TERM_BREAKDOWN) return set_err(ctx, LAKER_ERR_BREAKDOWN_ZERO_CURVATURE, "p.(lambda I + K)p <= 0");
+  if (worst == LAKER_TERM_INDEFINITE) return set_err(ctx, LAKER_ERR_INDEFINITE_PRECONDITIONER, "r.theta <= 0");
+  return LAKER_OK;
+}
+
+}  // namespace laker
+
+namespace laker {
+
+// Row-sharded multi-RHS PCG (C4 on W GPUs): rank w holds rows [r0, r1) of
+// K (full rows), of alpha, R, Q, Theta, and its part of the factored P (fit.cu: Q^T's
+// columns, QM's / Q's rows); P (the search directions) is kept whole on every rank.
+// Every column reduction is a per-rank unrounded Dot2 pair, all-gathered and summed in
+// rank order (block_combine_kernel), so every rank takes identical per-column decisions;
+// the factored P's N_r x m product Z = Q^T R is formed from the W partial products the
+// same way (block_zcombine_kernel).  Per iteration and rank: K_loc X (8 n^2 / W bytes),
+// Z_loc = Q^T_loc R_loc and Theta_loc = QM_loc Z + a^-1/2 R_loc (16 n N_r / W bytes).
+// Exchanges: the column pairs of p.q, ||r||^2 (+ r.theta), r.theta (4 m doubles each),
+// the partial Z (2 N_r m doubles, EXACT) and the Theta rows (n m / W doubles).
+laker_status pcg_solve_block_dist(laker_ctx ctx, int32_t m, const double *Y, double *alpha_out,
+                                  const laker_solve_opts &o, laker_solve_report *reps, double *history) {
+  if (ctx->storage != LAKER_STORE_MATERIALIZED) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS needs MATERIALIZED");
+  if (m > 256) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS: nrhs <= 256");
+  const int W = ctx->world;
+  const int64_t n = ctx->n, ld = ctx->ld, r0 = ctx->r0, nloc = ctx->r1 - ctx->r0;
+  const int pk = ctx->precond_kind;
+  const bool dense = (pk == LAKER_PRECOND_LEARNED || pk == LAKER_PRECOND_EXTERNAL_DENSE);
+  const bool fac = dense && ctx->p_factored && ctx->f_local;
+  if (dense && !fac && !ctx->P) return set_err(ctx, LAKER_ERR_NOT_READY, "dense preconditioner not set");
+  if (pk == LAKER_PRECOND_JACOBI && !ctx->Pdiag) return set_err(ctx, LAKER_ERR_NOT_READY, "Jacobi diagonal not set");
+  const bool qm = fac && ctx->p_qm;
+  const int32_t max_iters = o.max_iters > 0 ? o.max_iters : (int32_t)std::min<int64_t>(10 * n, 1 << 30);
+  const int64_t mp = (m + 1) / 2 * 2;
+  const bool exact = ctx->mode == LAKER_MODE_EXACT;
+  const int64_t nrp = fac ? ctx->f_nrp : 0, ldq = fac ? ctx->f_ldq : 0;
+  cudaStream_t s = ctx->stream;
+  // local n/W x mp blocks: alpha, R, Theta_loc, Q; whole ld x mp: P, Theta; exchanges
+  const size_t lb = (size_t)nloc * mp, fb = (size_t)ld * mp;
+  const size_t zb = fac ? (size_t)nrp * mp : 0, zp = exact ? 2 * zb : zb;
+  const size_t cs = 4 * (size_t)m;
+  const size_t total = 4 * lb + 2 * fb + 2 * zb + (1 + W) * zp + (1 + W) * cs + 8;
+  double *base = nullptr;
+  LAKER_CUDA(ctx, cudaMallocAsync(&base, total * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(base, 0, total * sizeof(double), s));
+  double *al = base, *rr = al + lb, *thl = rr + lb, *qq = thl + lb, *pp = qq + lb, *thf = pp + fb;
+  double *Zb = thf + fb, *Wb = Zb + zb, *zsend = Wb + zb, *zrecv = zsend + zp, *csend = zrecv + W * zp,
+         *crecv = csend + cs;
+  PcgState *st = nullptr;
+  double *hist = nullptr, *trel = nullptr;
+  int32_t *all_done = nullptr;
+  dd_pair *parts = nullptr;
+  const int cg = (int)std::min<int64_t>(2 * ctx->num_sms, (nloc + 63) / 64);
+  LAKER_CUDA(ctx, cudaMallocAsync(&st, m * sizeof(PcgState), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&hist, (size_t)max_iters * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&trel, m * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&all_done, sizeof(int32_t), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&parts, (size_t)cg * m * 2 * sizeof(dd_pair), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(all_done, 0, sizeof(int32_t), s));
+  std::vector<PcgState> h0(m);
+  for (auto &x : h0) {
+    x = PcgState{};
+    x.tol = o.tol;
+    x.max_iters = max_iters;
+  }
+  LAKER_CUDA(ctx, cudaMemcpyAsync(st, h0.data(), m * sizeof(PcgState), cudaMemcpyHostToDevice, s));
+  laker_status err = LAKER_OK;
+
+  BlockArgs ba{};
+  ba.n = nloc; ba.m = m; ba.ldv = mp; ba.pk = pk; ba.Y = Y + r0; ba.ldy = n; ba.alpha = al; ba.r = rr;
+  ba.theta = thl; ba.p = pp + (size_t)r0 * mp; ba.q = qq; ba.dvec = ctx->Pdiag ? ctx->Pdiag + r0 : nullptr;
+  ba.st = st; ba.hist = hist; ba.all_done = all_done; ba.true_rel = trel; ba.partials = parts;
+  ba.counter = ctx->counters + kCtrMisc; ba.pair_out = csend;
+  // a column reduction on the local rows, its W pair blocks gathered and combined in rank order
+  auto col = [&](int mode) {
+    BlockArgs b = ba;
+    b.mode = mode;
+    block_col_kernel<<<cg, 256, 0, s>>>(b);
+    if (ncclAllGather(csend, crecv, cs, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    block_combine_kernel<<<1, 256, 0, s>>>(b, crecv, W);
+    ctx->stats.kernel_launches += 2;
+  };
+  // EXACT offsets: row maxima of the local matrices, column maxima of each right-hand block
+  double *rmK = nullptr, *rmQt = nullptr, *rmQ = nullptr, *rmM = nullptr;
+  unsigned long long *cmx = nullptr;
+  if (exact) {
+    LAKER_CUDA(ctx, cudaMallocAsync(&rmK, (size_t)(2 * nloc + 2 * nrp + 256) * sizeof(double), s));
+    rmQt = rmK + nloc;
+    rmQ = rmQt + nrp;
+    rmM = rmQ + nloc;
+    cmx = reinterpret_cast<unsigned long long *>(rmM + nrp);
+    auto rowmax = [&](const double *A, int64_t rows, int64_t cols, int64_t lda, double *out) {
+      rowmax_abs_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(A, rows, cols, lda, out);
+      ctx->stats.kernel_launches++;
+    };
+    rowmax(ctx->K, nloc, n, ld, rmK);
+    if (fac) {
+      rowmax(ctx->Qt, nrp, nloc, ctx->f_ldl, rmQt);
+      rowmax(qm ? ctx->QMf : ctx->Qr, nloc, nrp, ldq, rmQ);
+      if (!qm) rowmax(ctx->Mf, nrp, nrp, ldq, rmM);
+    }
+  }
+  // Out (rows x m) = A (rows x kdim) X + lam Xd[row0 ..] -- EXACT compensated (pair output
+  // when Op != null) or the DMMA GEMM (FAST)
+  auto gemm = [&](const double *A, int64_t lda, int64_t rows, int64_t kdim, double lam, const double *X,
+                  const double *Xd, int64_t row0, double *Out, const double *rmx, dd_pair *Op) {
+    if (exact) {
+      cudaMemsetAsync(cmx, 0, 256 * sizeof(unsigned long long), s);
+      colmax_abs_kernel<<<dim3((unsigned)std::min<int64_t>(2 * ctx->num_sms, (kdim + 3) / 4), (unsigned)((m + 63) / 64)),
+                          256, 0, s>>>(X, kdim, m, mp, cmx, all_done);
+      dim3 grid((unsigned)((rows + kBR - 1) / kBR), (unsigned)((m + kBM - 1) / kBM));
+      gemm_dot2_kernel<true><<<grid, 256, 0, s>>>(A, lda, rows, kdim, X, mp, m, Out, mp, lam, row0, all_done, Xd, rmx,
+                                                  reinterpret_cast<const double *>(cmx), Op);
+      ctx->stats.kernel_launches += 2;
+    } else {
+      GemmArgs g{};
+      g.M = rows; g.N = mp; g.K = kdim; g.A = A; g.lda = lda; g.B = X; g.ldb = mp; g.C = Out; g.ldc = mp;
+      g.alpha = 1.0; g.beta = lam; g.Cin = Xd ? Xd + row0 * mp : nullptr; g.ldcin = mp;
+      launch_dgemm(g, true, s);
+      ctx->stats.kernel_launches++;
+    }
+  };
+  // Theta_loc = P R_loc (factored, from the local R); Theta gathered whole afterwards
+  auto apply_p = [&]() {
+    gemm(ctx->Qt, ctx->f_ldl, nrp, nloc, 0.0, rr, nullptr, 0, zsend, rmQt,
+         exact ? reinterpret_cast<dd_pair *>(zsend) : nullptr);
+    if (ncclAllGather(zsend, zrecv, zp, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+    block_zcombine_kernel<<<2 * ctx->num_sms, 256, 0, s>>>(nrp, m, mp, zrecv, W, exact ? 1 : 0, Zb, all_done);
+    ctx->stats.kernel_launches++;
+    if (qm) {
+      gemm(ctx->QMf, ldq, nloc, nrp, ctx->f_ainv, Zb, rr, 0, thl, rmQ, nullptr);
+    } else {
+      gemm(ctx->Mf, ldq, nrp, nrp, 0.0, Zb, nullptr, 0, Wb, rmM, nullptr);
+      gemm(ctx->Qr, ldq, nloc, nrp, ctx->f_ainv, Wb, rr, 0, thl, rmQ, nullptr);
+    }
+  };
+  auto gather_theta = [&]() {  // Theta_loc (nloc x mp) -> rows [r0, r1) of Theta on every rank
+    if (ncclAllGather(thl, thf, lb, ncclDouble, ctx->comm, s) != ncclSuccess) err = LAKER_ERR_NCCL;
+  };
+  const int vg = 2 * ctx->num_sms;
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  cudaEventRecord(ev0, s);
+  col(kColInit);
+  if (dense) {
+    if (!fac) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "sharded multi-RHS: dense P rows not supported");
+    apply_p();
+    col(kColBeta);  // initial rho = r.theta
+  }
+  gather_theta();
+  block_pupdate_kernel<<<vg, 256, 0, s>>>(n, m, mp, thf, pp, st, 1, all_done);
+  ctx->stats.kernel_launches++;
+  LAKER_CUDA(ctx, cudaGetLastError());
+  const int chunk = 4;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const int64_t before = ctx->stats.kernel_launches;
+  LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int j = 0; j < chunk; ++j) {
+    gemm(ctx->K, ld, nloc, n, ctx->lambda, pp, pp, r0, qq, rmK, nullptr);
+    col(kColDelta);
+    col(kColUpdate);
+    if (dense) {
+      apply_p();
+      col(kColBeta);
+    }
+    gather_theta();
+    block_pupdate_kernel<<<vg, 256, 0, s>>>(n, m, mp, thf, pp, st, 0, all_done);
+    ctx->stats.kernel_launches++;
+  }
+  LAKER_CUDA(ctx, cudaStreamEndCapture(s, &graph));
+  if (err != LAKER_OK) return set_err(ctx, err, "sharded multi-RHS: NCCL call failed during capture");
+  const int64_t per_chunk = ctx->stats.kernel_launches - before;
+  ctx->stats.kernel_launches = before;
+  LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec, graph, 0));
+  int32_t *hd = nullptr;
+  LAKER_CUDA(ctx, cudaMallocHost(&hd, sizeof(int32_t)));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hd, all_done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  LAKER_TRY(dist_sync(ctx, s));
+  while (!*hd) {
+    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
+    ctx->stats.kernel_launches += per_chunk;
+    LAKER_CUDA(ctx, cudaMemcpyAsync(hd, all_done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    LAKER_TRY(dist_sync(ctx, s));
+  }
+  cudaEventRecord(ev1, s);
+  // true residuals on the local rows (combined), alpha gathered (column-major n x m out)
+  LAKER_NCCL(ctx, ncclAllGather(al, thf, lb, ncclDouble, ctx->comm, s));   // alpha rows of every rank -> thf
+  LAKER_CUDA(ctx, cudaMemsetAsync(all_done, 0, sizeof(int32_t), s));
+  gemm(ctx->K, ld, nloc, n, ctx->lambda, thf, thf, r0, qq, rmK, nullptr);
+  {
+    BlockArgs b = ba;
+    b.mode = kColTrue;
+    block_col_kernel<<<cg, 256, 0, s>>>(b);
+    LAKER_NCCL(ctx, ncclAllGather(csend, crecv, cs, ncclDouble, ctx->comm, s));
+    block_combine_kernel<<<1, 256, 0, s>>>(b, crecv, W);
+    ctx->stats.kernel_launches += 2;
+  }
+  for (int32_t c = 0; c < m; ++c)
+    LAKER_CUDA(ctx, cudaMemcpy2DAsync(alpha_out + (size_t)c * n, sizeof(double), thf + c, mp * sizeof(double),
+                                      sizeof(double), n, cudaMemcpyDeviceToDevice, s));
+  std::vector<PcgState> hs(m);
+  std::vector<double> htr(m);
+  LAKER_CUDA(ctx, cudaMemcpyAsync(hs.data(), st, m * sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(htr.data(), trel, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_TRY(dist_sync(ctx, s));
+  if (history && hs[0].iters > 0)
+    LAKER_CUDA(ctx, cudaMemcpyAsync(history, hist, (size_t)hs[0].iters * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  ctx->stats.solve_ms = ms;
+  int worst = LAKER_TERM_RESIDUAL_TOL;
+  for (int32_t c = 0; c < m; ++c) {
+    if (reps) {
+      reps[c].iters = hs[c].iters;
+      reps[c].termination = hs[c].term;
+      reps[c].rel_residual = hs[c].iters > 0 ? hs[c].rel : (hs[c].term == LAKER_TERM_ZERO_RHS ? 0.0 : 1.0);
+      reps[c].true_rel_residual = htr[c];
+      reps[c].seconds = ms * 1e-3;
+    }
+    if (hs[c].term == LAKER_TERM_BREAKDOWN || hs[c].term == LAKER_TERM_INDEFINITE) worst = hs[c].term;
+  }
+  cudaFreeHost(hd);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaGraphExecDestroy(gexec);
+  cudaGraphDestroy(graph);
+  cudaFreeAsync(base, s);
+  if (rmK) cudaFreeAsync(rmK, s);
   cudaFreeAsync(st, s);
   cudaFreeAsync(hist, s);
   cudaFreeAsync(trel, s);

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
           rbeg = rend;
           rend = a.toff[++I + 1];
         }
-        const int jt = kTPD * I + (int)(t - rbeg);
+        const int jt = a.jt_of ? a.jt_of[t] : kTPD * I + (int)(t - rbeg);
         if (!first) mbar_wait(&empty[slot], ph ^ 1u);
         unsigned char *st = smem + slot * kStageBytes;
         mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         rbeg = rend;
         rend = a.toff[++I + 1];
       }
-      const int jt = kTPD * I + (int)(t - rbeg);
-      if (jt / kTPD == I) continue;  // diagonal-block tile: rows only
+      const int jt = a.jt_of ? a.jt_of[t] : kTPD * I + (int)(t - rbeg);
+      if (jt / kTPD == I + a.I0) continue;  // diagonal-block tile: rows only
       mbar_wait(&rfull[b], rph);
 #pragma unroll
       for (int h = 0; h < kCPT; ++h) {
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kSymThreads, 1)
     // reduce the 8 row pairs over the warp's 32 columns; lane k stores row k
     const int s = blockIdx.x - a.segfirst[I];
     dd_pair *dst = a.rowpart + ((int64_t)I * a.maxseg + s) * kSR + warp * kRPT;
-    const double *rmr = a.rowmax + (int64_t)I * kSR + warp * kRPT;
+    const double *rmr = a.rowmax + (int64_t)(I + a.I0) * kSR + warp * kRPT;
 #pragma unroll
     for (int k = 0; k < kRPT; ++k) {
       dd_pair v = acc[k];
@@ -239,15 +239,15 @@ __global__ void __launch_bounds__(kSymThreads, 1)
       rbeg = a.toff[curI];
       rend = a.toff[curI + 1];
       __syncwarp();
-      if (lane < kRPT) xr[lane] = a.x[(int64_t)curI * kSR + warp * kRPT + lane];
+      if (lane < kRPT) xr[lane] = a.x[(int64_t)(curI + a.I0) * kSR + warp * kRPT + lane];
       __syncwarp();
-      const double *rmr = a.rowmax + (int64_t)curI * kSR + warp * kRPT;
+      const double *rmr = a.rowmax + (int64_t)(curI + a.I0) * kSR + warp * kRPT;
 #pragma unroll
       for (int k = 0; k < kRPT; ++k) acc[k] = dd_pair{ROWOFF ? pow2_above(rmr[k] * xm * mrow) : 0.0, 0.0};
     }
     const int I = curI;
-    const int jt = kTPD * I + (int)(t - rbeg);
-    const bool diag = jt / kTPD == I;
+    const int jt = a.jt_of ? a.jt_of[t] : kTPD * I + (int)(t - rbeg);
+    const bool diag = jt / kTPD == I + a.I0;
     // column offsets from the column maxima (L2-resident; loaded before the data wait)
     static_assert(kCPT == 2, "two column halves per thread");
     // this thread's columns are 2c and 2c + 1 (16-byte loads of the tile, x and maxima)
@@ -430,11 +430,58 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
   }
 }
 
-// rm[i] = max_j |A_ij| (one warp per row)
-__global__ void rowmax_kernel(const double *__restrict__ A, int64_t n, int64_t ld, double *__restrict__ rm) {
+// Row-sharded finalize (tri_plan_dist): for every row i < n the unrounded pair of this
+// rank's partials -- the column partials of the local block-rows [cr_lo, cr_hi) of i's
+// column tile and, for the rank's own rows, the row segments -- summed in the order of
+// symv_finalize_kernel (warp w: block-rows cr_lo + w (mod 16), then segments w (mod 16);
+// warps combined in order), so at W = 1 the pair is the one that kernel rounds.
+template <int BR, int TC>
+__global__ void __launch_bounds__(kFinThreads) tri_finalize_dist_kernel(const SymvArgs a) {
+  if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
+  __shared__ dd_pair spart[kFinThreads / 32][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kW = kFinThreads / 32;
+  static_assert(BR % 32 == 0 && TC % 32 == 0, "a 32-row group lies in one block-row and one column tile");
+  for (int64_t g = blockIdx.x; g * 32 < a.n; g += gridDim.x) {
+    const int64_t i = g * 32 + lane;
+    const bool valid = i < a.n;
+    const int jt = (int)((g * 32) / TC);
+    dd_pair v = {0.0, 0.0};
+    if (valid) {
+      const int hi = a.cr_hi[jt];
+      int I = a.cr_lo[jt] + warp;
+      for (; I + 3 * kW < hi; I += 4 * kW) {
+        dd_pair o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = ldcg_pair(&a.colpart[(int64_t)(I + q * kW) * a.ldcp + i]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pair_add(v, o[q]);
+      }
+      for (; I < hi; I += kW) pair_add(v, ldcg_pair(&a.colpart[(int64_t)I * a.ldcp + i]));
+      if (i >= a.own0 && i < a.own1) {
+        const int J = (int)((i - a.own0) / BR), r = (int)((i - a.own0) % BR);
+        const int ns = a.nseg[J];
+        for (int q = warp; q < ns; q += kW) pair_add(v, ldcg_pair(a.rowpart + ((int64_t)J * a.maxseg + q) * BR + r));
+      }
+    }
+    spart[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && valid) {
+      dd_pair t = spart[0][lane];
+#pragma unroll
+      for (int w = 1; w < kW; ++w) pair_add(t, spart[w][lane]);
+      a.ypair[i] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// rm[i] = max_j |A_ij| over the `rows` rows of A (n columns; one warp per row)
+__global__ void rowmax_kernel(const double *__restrict__ A, int64_t rows, int64_t n, int64_t ld,
+                              double *__restrict__ rm) {
   const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (i >= n) return;
+  if (i >= rows) return;
   double m = 0.0;
   for (int64_t j = lane; j < n; j += 32) m = fmax(m, fabs(A[i * ld + j]));
 #pragma unroll
@@ -501,6 +548,10 @@ PFN_encodeTiled get_encode() {
 struct SymvPlan {
   int64_t n = 0, ld = 0, T = 0, ldcp = 0;
   int nb = 0, nct = 0, maxseg = 0, grid = 0, fin_grid = 0, br = 0, tc = 0;
+  int rank = 0, world = 1;  // tri_plan_dist: nb local block-rows starting at global I0
+  bool dist = false;        // built by tri_plan_dist (also at world = 1: the sharded pipeline)
+  int32_t I0 = 0;
+  int32_t *jt_of = nullptr, *cr_lo = nullptr, *cr_hi = nullptr;
   int64_t *toff = nullptr;
   int32_t *segfirst = nullptr, *nseg = nullptr;
   dd_pair *colpart = nullptr, *rowpart = nullptr;
@@ -520,6 +571,9 @@ void symv_init() {
 void symv_free(SymvPlan *&p) {
   if (!p) return;
   cudaFree(p->toff);
+  cudaFree(p->jt_of);
+  cudaFree(p->cr_lo);
+  cudaFree(p->cr_hi);
   cudaFree(p->segfirst);
   cudaFree(p->nseg);
   cudaFree(p->colpart);
@@ -531,20 +585,55 @@ void symv_free(SymvPlan *&p) {
   p = nullptr;
 }
 
-cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
-  if (p && p->n == n && p->br == br && p->tc == tc && p->grid == (int)std::max<int64_t>(1, grid)) return cudaSuccess;
-  symv_free(p);
-  p = new SymvPlan();
-  p->n = n;
-  p->br = br;
-  p->tc = tc;
-  p->nb = (int)((n + br - 1) / br);
-  p->nct = (int)((n + tc - 1) / tc);
-  const int tpd = br / tc;
-  std::vector<int64_t> toff(p->nb + 1, 0);
-  for (int I = 0; I < p->nb; ++I) toff[I + 1] = toff[I] + (p->nct - tpd * I);
+bool dist_tiles(int64_t n, int br, int tc, int rank, int world, std::vector<int64_t> &toff,
+                std::vector<int32_t> &jt, std::vector<int32_t> &cr_lo, std::vector<int32_t> &cr_hi) {
+  if (world < 1 || rank < 0 || rank >= world || br % tc != 0 || n % world != 0) return false;
+  const int64_t nloc = n / world;
+  if (nloc % br != 0 || (world % 2 == 0 && world > 1 && nloc % (2 * br) != 0)) return false;
+  const int L = (int)(nloc / br), tpd = br / tc, tpb = (int)(nloc / tc);  // column tiles per block
+  const int nct = (int)(n / tc), W = world, w = rank;
+  const int I0 = w * L;
+  const int D = (W % 2 == 1) ? (W - 1) / 2 : W / 2 - 1;
+  const int hc = (W % 2 == 0 && W > 1) ? (w + W / 2) % W : -1;  // the half-shared block
+  toff.assign(L + 1, 0);
+  jt.clear();
+  cr_lo.assign(nct, 0);
+  cr_hi.assign(nct, 0);
+  for (int I = 0; I < L; ++I) {
+    for (int j = tpd * (I0 + I); j < (w + 1) * tpb; ++j) jt.push_back(j);  // own block, from the diagonal
+    for (int d = 1; d <= D; ++d) {
+      const int c = (w + d) % W;
+      for (int j = c * tpb; j < (c + 1) * tpb; ++j) jt.push_back(j);
+    }
+    if (hc >= 0) {
+      if (w < hc) {
+        if (I < L / 2)
+          for (int j = hc * tpb; j < (hc + 1) * tpb; ++j) jt.push_back(j);
+      } else {
+        for (int j = hc * tpb + tpb / 2; j < (hc + 1) * tpb; ++j) jt.push_back(j);
+      }
+    }
+    toff[I + 1] = (int64_t)jt.size();
+  }
+  // column partials: own block -> the local block-rows above the tile's diagonal block;
+  // blocks at distance 1..D -> all; the half block -> the half this rank streams
+  for (int j = w * tpb; j < (w + 1) * tpb; ++j) cr_hi[j] = j / tpd - I0;
+  for (int d = 1; d <= D; ++d) {
+    const int c = (w + d) % W;
+    for (int j = c * tpb; j < (c + 1) * tpb; ++j) cr_hi[j] = L;
+  }
+  if (hc >= 0) {
+    if (w < hc)
+      for (int j = hc * tpb; j < (hc + 1) * tpb; ++j) cr_hi[j] = L / 2;
+    else
+      for (int j = hc * tpb + tpb / 2; j < (hc + 1) * tpb; ++j) cr_hi[j] = L;
+  }
+  return true;
+}
+
+static cudaError_t tri_plan_common(SymvPlan *p, const std::vector<int64_t> &toff, int br) {
   p->T = toff[p->nb];
-  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, p->T));
+  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(p->grid, p->T));
   std::vector<int32_t> segfirst(p->nb), nseg(p->nb);
   auto cta_of = [&](int64_t t) {  // CTA b with floor(T b / G) <= t < floor(T (b+1) / G)
     int64_t b = (t * p->grid) / p->T;
@@ -558,8 +647,8 @@ cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
     nseg[I] = cta_of(toff[I + 1] - 1) - segfirst[I] + 1;
     p->maxseg = std::max(p->maxseg, (int)nseg[I]);
   }
-  p->ldcp = (int64_t)p->nct * tc;
-  const int64_t groups = (n + 31) / 32;  // 32-row groups of the finalize
+  p->ldcp = (int64_t)p->nct * p->tc;
+  const int64_t groups = (p->n + 31) / 32;  // 32-row groups of the finalize
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   p->fin_grid = (int)std::min<int64_t>(4 * sms, groups);
@@ -575,9 +664,59 @@ cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
   return cudaSuccess;
 }
 
-cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms) {
-  if (p && p->n == n && p->ld == ld && p->br == kSR && p->tc == kSC) return cudaSuccess;
-  cudaError_t e = tri_plan(p, n, kSR, kSC, num_sms);
+cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid) {
+  if (p && p->n == n && p->br == br && p->tc == tc && !p->dist && p->grid == (int)std::max<int64_t>(1, grid))
+    return cudaSuccess;
+  symv_free(p);
+  p = new SymvPlan();
+  p->n = n;
+  p->br = br;
+  p->tc = tc;
+  p->nb = (int)((n + br - 1) / br);
+  p->nct = (int)((n + tc - 1) / tc);
+  p->grid = grid;
+  const int tpd = br / tc;
+  std::vector<int64_t> toff(p->nb + 1, 0);
+  for (int I = 0; I < p->nb; ++I) toff[I + 1] = toff[I] + (p->nct - tpd * I);
+  return tri_plan_common(p, toff, br);
+}
+
+cudaError_t tri_plan_dist(SymvPlan *&p, int64_t n, int br, int tc, int grid, int rank, int world) {
+  if (p && p->dist && p->n == n && p->br == br && p->tc == tc && p->rank == rank && p->world == world &&
+      p->grid == (int)std::max<int64_t>(1, grid))
+    return cudaSuccess;
+  std::vector<int64_t> toff;
+  std::vector<int32_t> jt, lo, hi;
+  if (!dist_tiles(n, br, tc, rank, world, toff, jt, lo, hi)) return cudaErrorInvalidValue;
+  symv_free(p);
+  p = new SymvPlan();
+  p->n = n;
+  p->br = br;
+  p->tc = tc;
+  p->rank = rank;
+  p->world = world;
+  p->dist = true;
+  p->nb = (int)(toff.size() - 1);
+  p->I0 = rank * p->nb;
+  p->nct = (int)(n / tc);
+  p->grid = grid;
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->jt_of, std::max<size_t>(jt.size(), 1) * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->cr_lo, lo.size() * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->cr_hi, hi.size() * sizeof(int32_t))) != cudaSuccess) return e;
+  cudaMemcpy(p->jt_of, jt.data(), jt.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->cr_lo, lo.data(), lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->cr_hi, hi.data(), hi.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  return tri_plan_common(p, toff, br);
+}
+
+bool tri_is_dist(const SymvPlan *p) { return p && p->dist; }
+
+cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms, int rank, int world, bool dist) {
+  if (p && p->n == n && p->ld == ld && p->br == kSR && p->tc == kSC && p->dist == dist && p->rank == rank &&
+      p->world == world)
+    return cudaSuccess;
+  cudaError_t e = dist ? tri_plan_dist(p, n, kSR, kSC, num_sms, rank, world) : tri_plan(p, n, kSR, kSC, num_sms);
   if (e != cudaSuccess) return e;
   p->ld = ld;
   const size_t len = (size_t)p->nct * kSC;
@@ -600,6 +739,12 @@ void tri_fill(const SymvPlan *p, SymvArgs &a) {
   a.colpart = p->colpart;
   a.ldcp = p->ldcp;
   a.rowpart = p->rowpart;
+  a.I0 = p->I0;
+  a.jt_of = p->jt_of;
+  a.cr_lo = p->cr_lo;
+  a.cr_hi = p->cr_hi;
+  a.own0 = (int64_t)p->I0 * p->br;
+  a.own1 = a.own0 + (int64_t)p->nb * p->br;
 }
 
 int tri_grid(const SymvPlan *p) { return p->grid; }
@@ -607,6 +752,15 @@ int64_t tri_n(const SymvPlan *p) { return p->n; }
 int tri_br(const SymvPlan *p) { return p->br; }
 
 void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s) {
+  if (p->dist) {
+    if (p->br == 128 && p->tc == 64)
+      tri_finalize_dist_kernel<128, 64><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+    else if (p->br == 128 && p->tc == 128)
+      tri_finalize_dist_kernel<128, 128><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+    else
+      tri_finalize_dist_kernel<64, 64><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+    return;
+  }
   if (p->br == 128)
     symv_finalize_kernel<128><<<p->fin_grid, kFinThreads, 0, s>>>(a);
   else
@@ -615,17 +769,24 @@ void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s) {
 
 int symv_finalize_grid(const SymvPlan *p) { return p->fin_grid; }
 
-// which = 0 (K) or 1 (P): the row maxima of the (new) contents of A
+// which = 0 (K) or 1 (P): the row maxima of the (new) contents of A (sharded: of the
+// rank's rows, into their global slots; the caller all-gathers the rest)
 void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s) {
-  rowmax_kernel<<<(unsigned)((p->n + 7) / 8), 256, 0, s>>>(A, p->n, p->ld, p->rowmax[which]);
+  const int64_t rows = p->dist ? (int64_t)p->nb * p->br : p->n;
+  const int64_t r0 = p->dist ? (int64_t)p->I0 * p->br : 0;
+  rowmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(A, rows, p->n, p->ld, p->rowmax[which] + r0);
 }
+
+double *symv_rowmax_ptr(SymvPlan *p, int which) { return p->rowmax[which]; }
 
 // which = 0 (K) or 1 (P); (re)encodes the tensor map when the base pointer changed
 bool symv_bind(SymvPlan *p, int which, const double *A) {
   if (p->tm_base[which] == A) return true;
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)p->n, (cuuint64_t)p->n};
+  // the rows this rank stores: all n, or its n / W (sharded; tile rows are local)
+  const int64_t rows = p->dist ? (int64_t)p->nb * p->br : p->n;
+  cuuint64_t dims[2] = {(cuuint64_t)p->n, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)p->ld * sizeof(double)};
   cuuint32_t box[2] = {kSC, kSR};
   cuuint32_t estr[2] = {1, 1};
@@ -659,11 +820,15 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     a.xparts = p->xparts;
     a.nxparts = kXParts;
   }
+  a.ypair = g.ypair;
   if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else
     symv_dot2_kernel<false><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
-  symv_finalize_kernel<kSR><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
+  if (p->dist)
+    tri_finalize_dist_kernel<kSR, kSC><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
+  else
+    symv_finalize_kernel<kSR><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
 }
 
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s) {

@@ -12,6 +12,8 @@
 // sum_s rowpart[J(i)][s][i mod BR] + lambda x_i) in that fixed order, the Dot2
 // pair x.y per CTA, and the last CTA runs the PCG scalar epilogue.
 #pragma once
+#include <vector>
+
 #include "laker_internal.h"
 
 namespace laker {
@@ -41,10 +43,39 @@ struct SymvArgs {
   const double *rowmax;
   const double *xparts;
   int nxparts;
+  // row-sharded plans (tri_plan_dist): block-rows are the local ones, global index I0 + I;
+  // the tiles of a block-row are listed explicitly (jt_of) and every column tile jt has
+  // its column partials in the local block-rows [cr_lo[jt], cr_hi[jt]); the finalize then
+  // writes the unrounded pair of every row i < n to ypair (no lambda term, no epilogue)
+  // for the exchange (pcg_dist.cu).  Single-rank plans: I0 = 0, jt_of = null.
+  int32_t I0;
+  const int32_t *jt_of;
+  const int32_t *cr_lo, *cr_hi;
+  dd_pair *ypair;
+  int64_t own0, own1;  // global rows whose row partials this rank holds
 };
 
 // partition of an n x n symmetric apply into BR x TC tiles over `grid` CTAs
 cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid);
+// the row-sharded version: rank `rank` of `world` owns rows [rank n/W, (rank+1) n/W) and
+// takes the tiles of dist_tiles() (each pair of symmetric entries once over all ranks)
+cudaError_t tri_plan_dist(SymvPlan *&p, int64_t n, int br, int tc, int grid, int rank, int world);
+bool tri_is_dist(const SymvPlan *p);
+// Host: the tile lists of the row-sharded symmetric apply (n / world a multiple of 2 br).
+// Rank w's block-rows I (local, global w L + I, L = n / (world br)) take, in this order:
+//   the tiles of its own diagonal block from the diagonal on (jt >= (br/tc)(w L + I));
+//   every tile of the blocks c = w + d (mod W), d = 1 .. D  (D = (W - 1) / 2, W odd;
+//   W / 2 - 1, W even);
+//   W even, c = w + W/2: rank min(w, c) takes block c for its first L/2 block-rows,
+//   rank max(w, c) takes the second half of block c's columns for all its block-rows.
+// Every off-diagonal block pair is then streamed once (its transpose never), so each rank
+// streams (n/W)^2/2 + (W/2 - 1/2)(n/W)^2 ... = n^2 / (2 W) entries: the single-GPU
+// triangle divided by W.  toff [L + 1], jt [T] (global column tiles), cr_lo / cr_hi [nct]
+// (local block-rows with column partials for column tile jt: off-diagonal-block tiles).
+bool dist_tiles(int64_t n, int br, int tc, int rank, int world, std::vector<int64_t> &toff,
+                std::vector<int32_t> &jt, std::vector<int32_t> &cr_lo, std::vector<int32_t> &cr_hi);
+// ranks that receive this rank's column partials: w + d (mod W), d = 1 .. nsend
+inline int dist_nsend(int world) { return world / 2; }
 // the plan's partition fields of SymvArgs
 void tri_fill(const SymvPlan *p, SymvArgs &a);
 int tri_grid(const SymvPlan *p);

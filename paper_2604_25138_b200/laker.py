@@ -37,7 +37,8 @@ EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_statu
             "laker_predict", "laker_load_kernel_rows", "laker_get_kernel_rows", "laker_set_preconditioner",
             "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_get_preconditioner_qm",
             "laker_apply_operator",
-            "laker_get_stats", "laker_debug_igemm_s8", "laker_debug_ozaki_gemm"]
+            "laker_get_stats", "laker_debug_igemm_s8", "laker_debug_ozaki_gemm", "laker_debug_dist_tiles",
+            "laker_debug_dist_symv_partials", "laker_debug_dist_symv_combine"]
 
 
 class LakerError(RuntimeError):
@@ -107,6 +108,9 @@ def _load() -> ctypes.CDLL:
         "laker_get_stats": [vp, ctypes.POINTER(Stats)],
         "laker_debug_igemm_s8": [vp, vp, vp, i64, i64, i64],
         "laker_debug_ozaki_gemm": [vp, vp, vp, i64, i64, i64, i32, i32],
+        "laker_debug_dist_tiles": [i64, i32, i32, i32, i32, vp, vp, vp, vp, vp],
+        "laker_debug_dist_symv_partials": [vp, vp, vp, vp],
+        "laker_debug_dist_symv_combine": [vp, vp, vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -261,6 +265,31 @@ def laker_debug_ozaki_gemm(A, B, C, slices: int = 0, kernel: int = -1) -> None:
         raise LakerError(s, "laker_debug_ozaki_gemm")
 
 
+def laker_debug_dist_tiles(n: int, br: int, tc: int, rank: int, world: int) -> dict:
+    """The tile lists of the row-sharded symmetric apply (host only, no GPU needed)."""
+    cnt = np.zeros(3, dtype=np.int64)
+    s = lib.laker_debug_dist_tiles(n, br, tc, rank, world, _ptr(cnt, np.int64), None, None, None, None)
+    if s != LAKER_OK:
+        raise LakerError(s, "laker_debug_dist_tiles")
+    L, T, nct = (int(v) for v in cnt)
+    toff = np.zeros(L + 1, dtype=np.int64)
+    jt = np.zeros(max(T, 1), dtype=np.int32)
+    lo, hi = np.zeros(nct, dtype=np.int32), np.zeros(nct, dtype=np.int32)
+    s = lib.laker_debug_dist_tiles(n, br, tc, rank, world, _ptr(cnt, np.int64), _ptr(toff, np.int64),
+                                   _ptr(jt, np.int32), _ptr(lo, np.int32), _ptr(hi, np.int32))
+    if s != LAKER_OK:
+        raise LakerError(s, "laker_debug_dist_tiles")
+    return {"toff": toff, "jt": jt[:T], "cr_lo": lo, "cr_hi": hi}
+
+
+def laker_debug_dist_symv_partials(ctx, x, rowmax, pairs):
+    _check(ctx, lib.laker_debug_dist_symv_partials(ctx, _ptr(x), _ptr(rowmax), _ptr(pairs)))
+
+
+def laker_debug_dist_symv_combine(ctx, x, own, recv, q_loc, pq_pair=None):
+    _check(ctx, lib.laker_debug_dist_symv_combine(ctx, _ptr(x), _ptr(own), _ptr(recv), _ptr(q_loc), _ptr(pq_pair)))
+
+
 # ------------------------------------------------------------ convenience
 class Context:
     """Owns one laker_ctx.  Methods are the C calls without the `laker_` prefix."""
@@ -345,7 +374,7 @@ class Context:
     def get_preconditioner_factors(self):
         """(Q n x N_r, M N_r x N_r, a^{-1/2}) of a factored LEARNED P."""
         nr = self.stats()["n_dirs"]
-        Q, M, ai = np.empty((self.n, nr)), np.empty((nr, nr)), np.zeros(1)
+        Q, M, ai = np.empty((self.local_rows, nr)), np.empty((nr, nr)), np.zeros(1)
         laker_get_preconditioner_factors(self.h, Q, M, ai)
         return Q, M, float(ai[0])
 
@@ -353,7 +382,7 @@ class Context:
         """QM = Q M (n x N_r) of a factored LEARNED P in the QM form (R21), or None."""
         if self.stats()["p_factored"] != 2:
             return None
-        QM = np.empty((self.n, self.stats()["n_dirs"]))
+        QM = np.empty((self.local_rows, self.stats()["n_dirs"]))
         laker_get_preconditioner_qm(self.h, QM)
         return QM
 

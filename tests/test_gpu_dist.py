@@ -89,3 +89,85 @@ def test_row_sharded_assembly_and_predict_layouts(L, W):
                 c.pcg_solve(P.y, 1e-8)
             c.close()
     full.close()
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_sharded_symmetric_apply_detached_ranks(L, W):
+    """The row-sharded symmetric K apply (symv.cu tri_plan_dist + pcg_dist.cu combine) run
+    rank by rank on one GPU (detached shards, no communicator): each rank's tile partials
+    (laker_debug_dist_symv_partials) are exchanged here exactly as pcg_dist.cu's
+    send/recv does (rank w's rows receive the pairs of ranks w-1 .. w-W/2) and combined
+    by the library's own combine kernel; the concatenated rows must equal the single-GPU
+    symmetric apply -- and so the oracle's O2 rows -- bitwise, and every pair a rank
+    would not send must be zero."""
+    n = 3072 if W == 3 else 4096
+    P = make_problem(3, n=n)
+    full = L.Context(0)
+    full.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    assert full.stats()["symmetric_k"] == 1
+    Kf = full.get_kernel_rows()
+    rowmax = np.ascontiguousarray(np.abs(Kf).max(axis=1))
+    rng = np.random.default_rng(W)
+    xs = [rng.standard_normal(n), np.where(rng.random(n) < 0.5, -1.0, 1.0) * np.exp(rng.uniform(-6, 6, n))]
+    refs = [full.apply_operator(x) for x in xs]
+    full.close()
+    nloc, D = n // W, W // 2
+    ctxs = []
+    for w in range(W):
+        c = L.Context(0, w, W, None)
+        c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+        assert c.stats()["symmetric_k"] == 1
+        ctxs.append(c)
+    for x, ref in zip(xs, refs):
+        parts = []
+        for w, c in enumerate(ctxs):
+            pr = np.zeros(2 * n)
+            L.laker_debug_dist_symv_partials(c.h, x, rowmax, pr)
+            pr = pr.reshape(n, 2)
+            sent = {w} | {(w + d) % W for d in range(1, D + 1)}
+            for o in range(W):
+                if o not in sent:
+                    assert (pr[o * nloc:(o + 1) * nloc] == 0).all(), (w, o)
+            parts.append(pr)
+        q = np.empty(n)
+        for w, c in enumerate(ctxs):
+            rows = slice(w * nloc, (w + 1) * nloc)
+            own = np.ascontiguousarray(parts[w][rows])
+            recv = np.ascontiguousarray(np.stack([parts[(w - d) % W][rows] for d in range(1, D + 1)]))
+            ql = np.zeros(nloc)
+            L.laker_debug_dist_symv_combine(c.h, x, own, recv, ql)
+            q[rows] = ql
+        bad = np.flatnonzero(q != ref)
+        assert bad.size == 0, (W, bad.size, bad[:5])
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("kind", ["jacobi", "learned"])
+def test_collective_block_solve_equals_single(L, kind):
+    """The row-sharded multi-RHS solve (pcg_block.cu pcg_solve_block_dist: per-rank column
+    pairs all-gathered and combined in rank order, the factored P's Q^T R from gathered
+    partial products) on a 1-rank communicator equals the single-GPU block solve bitwise,
+    and every column equals the single-RHS oracle solve (T18)."""
+    P = make_problem(4, n=1024, nrhs=6, tol=1e-8)
+    Y = np.asfortranarray(P.Y)
+    res = []
+    for use_nccl in (False, True):
+        c = L.Context(0, 0, 1, L.laker_get_unique_id() if use_nccl else None)
+        c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+        if kind == "jacobi":
+            c.set_preconditioner(L.PRECOND_JACOBI)
+        else:
+            Z = np.asfortranarray(make_directions(4, P.n, P.n_dirs))
+            c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+        A, reps, _ = c.pcg_solve(Y, P.tol)
+        res.append((A, [r["iters"] for r in reps], [r["true_rel_residual"] for r in reps]))
+        c.close()
+    (A0, i0, t0), (A1, i1, t1) = res
+    assert i0 == i1 and t0 == t1 and (A0 == A1).all()
+    if kind == "jacobi":
+        K, _ = O.assemble(P.E, P.scale)
+        d = O.jacobi_diag(P.E, P.scale, P.lam)
+        for j in range(Y.shape[1]):
+            ao, ro = O.pcg(K, P.lam, Y[:, j], O.P_JACOBI, d, tol=P.tol)
+            assert ro.iters == i1[j] and (ao == A1[:, j]).all()
