@@ -39,9 +39,9 @@ constexpr uint32_t kQChunk = kQM * kQK;   // 8 KiB
 constexpr int kQBufs = 4;                 // TMEM level buffers of 128 columns
 constexpr int kQEpiWarps = 16;
 constexpr int kQThreads = (2 + kQEpiWarps) * 32;
-constexpr size_t kQRedOff = 2 * kQSmax * kQChunk;          // red[4][128] doubles
-constexpr size_t kQCredOff = kQRedOff + 4 * kQM * 8;        // cred[2][4][128] doubles
-constexpr size_t kQTabOff = kQCredOff + 2 * 4 * kQM * 8;    // exp table [16] doubles
+constexpr size_t kQRedOff = 2 * kQSmax * kQChunk;          // red[4][128] pairs
+constexpr size_t kQCredOff = kQRedOff + 4 * kQM * 16;       // cred[2][4][128] pairs
+constexpr size_t kQTabOff = kQCredOff + 2 * 4 * kQM * 16;   // exp table [16] doubles
 constexpr size_t kQBarOff = kQTabOff + 16 * 8;
 constexpr size_t kQSmem = 1024 + kQBarOff + 256;
 
@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
   unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);
   unsigned char *sA = smem;
   unsigned char *sB = smem + kQSmax * kQChunk;
-  double *red = reinterpret_cast<double *>(smem + kQRedOff);
-  double *cred = reinterpret_cast<double *>(smem + kQCredOff);
+  dd_pair *red = reinterpret_cast<dd_pair *>(smem + kQRedOff);
+  dd_pair *cred = reinterpret_cast<dd_pair *>(smem + kQCredOff);
   double *tab = reinterpret_cast<double *>(smem + kQTabOff);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kQBarOff);  // [7]
   uint64_t *empty = full + kQSmax;                                  // [7]
@@ -236,7 +236,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
     int64_t row = 0;
     bool rok = false;
     int ea = 0;
-    double wr = 0.0, rsum = 0.0;
+    double wr = 0.0;
+    // compensated sums (Dot2: TwoProd + TwoSum, pairs combined by TwoSum): the operator's
+    // rounding error stays ~u |K p| instead of ~u |K| |p|, which in the late CG iterations
+    // (|K| |p| / |K p| up to ~kappa) cost +38% Jacobi iterations at the C5 regime (n = 8192,
+    // lambda = 1e-5) with plain fp64 sums; the entries themselves stay FAST (tcgen05 + exp_tab)
+    dd_pair rsum = {0.0, 0.0};
     int64_t job = 0;
     int cbuf = 0;
     auto flush_rows = [&](int Iblk) {
@@ -244,16 +249,20 @@ __global__ void __launch_bounds__(kQThreads, 1)
       red[qt * kQM + rl] = rsum;
       named_bar(1, kQEpiWarps * 32);
       if (qt == 0) {
-        const double v = (red[rl] + red[kQM + rl]) + (red[2 * kQM + rl] + red[3 * kQM + rl]);
+        dd_pair v = red[rl];
+        pair_add(v, red[kQM + rl]);
+        pair_add(v, red[2 * kQM + rl]);
+        pair_add(v, red[3 * kQM + rl]);
         if (KIND == kSym) {
           const int s = (int)blockIdx.x - f.t.segfirst[Iblk];
-          f.t.rowpart[((int64_t)Iblk * f.t.maxseg + s) * kQM + rl] = dd_pair{v, 0.0};
+          f.t.rowpart[((int64_t)Iblk * f.t.maxseg + s) * kQM + rl] = v;
         } else if (rok) {
-          f.out[row] = f.lambda != 0.0 ? fma(f.lambda, f.xdiag[row], v) : v;
+          if (f.lambda != 0.0) dot2_step(v, f.lambda, f.xdiag[row]);
+          f.out[row] = pair_value(v);
         }
       }
       named_bar(1, kQEpiWarps * 32);
-      rsum = 0.0;
+      rsum = dd_pair{0.0, 0.0};
     };
     for (int64_t t = t0; t < t1; ++t) {
       bool newI = (t == t0);
@@ -320,28 +329,52 @@ __global__ void __launch_bounds__(kQThreads, 1)
       for (int j = 0; j < 32; ++j) {
         const double2 cf = ld_cf(f.cf + cb + j);
         const double kv = exp_tab(acc[j] * cf.x, tab);
-        rsum = fma(kv, cf.y, rsum);
-        acc[j] = kv * wr;
+        dot2_step(rsum, kv, cf.y);
+        acc[j] = kv;
       }
       if (cols) {
-        // reduce-scatter over the warp's 32 rows: lane l ends with column qt*32 + l
+        // reduce-scatter over the warp's 32 rows of the exact products kv w_row (TwoProd
+        // pairs, combined by TwoSum): lane l ends with column qt*32 + l
+        dd_pair pr[16];
+        {
+          const bool up = (lane & 16) != 0;
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
+          for (int i = 0; i < 16; ++i) {
+            dd_pair lo, hi;
+            two_prod(acc[i], wr, lo.s, lo.c);
+            two_prod(acc[i + 16], wr, hi.s, hi.c);
+            const dd_pair snd = up ? lo : hi;
+            dd_pair rcv;
+            rcv.s = __shfl_xor_sync(0xffffffffu, snd.s, 16);
+            rcv.c = __shfl_xor_sync(0xffffffffu, snd.c, 16);
+            pr[i] = up ? hi : lo;
+            pair_add(pr[i], rcv);
+          }
+        }
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) {
           const bool up = (lane & off) != 0;
 #pragma unroll
           for (int i = 0; i < off; ++i) {
-            const double lo = acc[i], hi = acc[i + off];
-            const double recv = __shfl_xor_sync(0xffffffffu, up ? lo : hi, off);
-            acc[i] = (up ? hi : lo) + recv;
+            const dd_pair lo = pr[i], hi = pr[i + off];
+            const dd_pair snd = up ? lo : hi;
+            dd_pair rcv;
+            rcv.s = __shfl_xor_sync(0xffffffffu, snd.s, off);
+            rcv.c = __shfl_xor_sync(0xffffffffu, snd.c, off);
+            pr[i] = up ? hi : lo;
+            pair_add(pr[i], rcv);
           }
         }
-        double *cr = cred + cbuf * 4 * kQM;
-        cr[q * kQM + qt * 32 + lane] = acc[0];
+        dd_pair *cr = cred + cbuf * 4 * kQM;
+        cr[q * kQM + qt * 32 + lane] = pr[0];
         named_bar(2 + qt, 128);  // the four lane quadrants of this column quarter
         if (q == 0) {
           const int c = qt * 32 + lane;
-          const double v = (cr[c] + cr[kQM + c]) + (cr[2 * kQM + c] + cr[3 * kQM + c]);
-          f.t.colpart[(int64_t)I * f.t.ldcp + J * kQM + c] = dd_pair{v, 0.0};
+          dd_pair v = cr[c];
+          pair_add(v, cr[kQM + c]);
+          pair_add(v, cr[2 * kQM + c]);
+          pair_add(v, cr[3 * kQM + c]);
+          f.t.colpart[(int64_t)I * f.t.ldcp + J * kQM + c] = v;
         }
         cbuf ^= 1;
       }
