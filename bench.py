@@ -125,6 +125,78 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def _json(name):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
+    except Exception:
+        return {}
+
+
+def side_measurements(L, dev):
+    """North-star records beside the headline (rank 0, N = 1, after the timed region, not in
+    `value`): kernel assembly in both modes against the measured fp64 peaks (SURVEY §8(d) M4:
+    the FAST QK^T runs on the fp64 tensor cores, DMMA; EXACT on the fp64 ALU with correctly
+    rounded entries), the C4 multi-RHS block solve (64 maps, FAST and EXACT products) and the
+    C5 on-the-fly operator (n = 65536) per apply."""
+    import torch
+    from synth import make_problem
+    out = {}
+    peaks = _json("r01_box_peaks.json")
+    pipes = _json("pipe_fractions.json")
+    P = make_problem(3)
+    n, d = P.n, P.d
+    E = torch.from_numpy(P.E).to(dev)
+    c = L.Context(dev.index or 0)
+    asm = {}
+    for name, mode in (("exact", L.MODE_EXACT), ("fast", L.MODE_FAST)):
+        ms = []
+        for _ in range(3):
+            c.assemble_kernel(E, P.scale, P.lam, L.STORE_MATERIALIZED, mode)
+            ms.append(c.stats()["assemble_ms"])
+        t = min(ms)
+        flops = (n * (n + 1) / 2) * 2 * d     # the QK^T of the stored triangle (mirrored)
+        rec = {"ms": t, "qkt_tflops": flops / (t * 1e-3) / 1e12, "entries": n * (n + 1) // 2}
+        pk = peaks.get("dmma_tflops" if mode == L.MODE_FAST else "dfma_tflops")
+        if pk:
+            rec["peak_tflops"] = pk
+            rec["peak_source"] = ("profiles/r01_box_peaks.json " + ("dmma_tflops (fp64 tensor, DMMA)"
+                                                                    if mode == L.MODE_FAST else "dfma_tflops (fp64 ALU)"))
+            rec["frac_of_peak_qkt_only"] = rec["qkt_tflops"] / pk
+        if name in pipes:
+            rec["ncu_pipe"] = pipes[name]
+        asm[name] = rec
+    out["assembly_c3"] = asm
+    c.close()
+    # C4: 64 radio maps, LEARNED P shared across bands, block PCG
+    P4 = make_problem(4)
+    c = L.Context(dev.index or 0)
+    c4 = {}
+    for name, mode in (("fast", L.MODE_FAST), ("exact", L.MODE_EXACT)):
+        c.assemble_kernel(torch.from_numpy(P4.E).to(dev), P4.scale, P4.lam, L.STORE_MATERIALIZED, mode)
+        c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P4.n_dirs, seed=7)
+        Y = torch.from_numpy(np.ascontiguousarray(P4.Y.T)).to(dev)   # (nrhs, n) rows = columns
+        _, reps, _ = c.pcg_solve(Y, P4.tol)
+        its = [r["iters"] for r in reps]
+        c4[name] = {"solve_s": reps[0]["seconds"], "nrhs": len(reps), "iters_min": min(its), "iters_max": max(its),
+                    "all_converged": all(r["termination"] == L.TERM_RESIDUAL_TOL for r in reps),
+                    "worst_true_rel_residual": max(r["true_rel_residual"] for r in reps)}
+    out["c4_block_solve"] = c4
+    c.close()
+    # C5: the on-the-fly operator at n = 65536 (K never stored), Jacobi P, capped iterations
+    P5 = make_problem(5, grid=64)
+    c = L.Context(dev.index or 0)
+    c5 = {}
+    for name, mode, k in (("fast", L.MODE_FAST, 20), ("exact", L.MODE_EXACT, 2)):
+        c.assemble_kernel(torch.from_numpy(P5.E).to(dev), P5.scale, P5.lam, L.STORE_ON_THE_FLY, mode)
+        c.set_preconditioner(L.PRECOND_JACOBI)
+        _, reps, _ = c.pcg_solve(torch.from_numpy(P5.y).to(dev), P5.tol, max_iters=k)
+        c5[name] = {"ms_per_apply": reps[0]["seconds"] / reps[0]["iters"] * 1e3, "iters_timed": reps[0]["iters"],
+                    "n": P5.n, "entries_per_apply_symmetric": P5.n * (P5.n + 1) // 2}
+    out["c5_on_the_fly_operator"] = c5
+    c.close()
+    return out
+
+
 def cpu_baseline_sample(prob, iters: int = 48):
     """The oracle as it stands on this host's cores: orc_pcg at n = 16384 with a
     dense P (identity stored densely -- the same per-iteration work, two Dot2
@@ -339,6 +411,8 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms / args.steps},
             "roofline": roof, "gpu_launches": launches, "clocks": clocks}
+    if world == 1 and not args.no_side:
+        line["side"] = side_measurements(L, dev)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(prob)
     print(json.dumps(line), flush=True)
@@ -354,6 +428,7 @@ def main():
                     choices=["learned", "jacobi", "none"])
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-side", action="store_true", help="skip the assembly / C4 / C5 side records")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` launches its own N ranks (one process per GPU) the way

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   __shared__ int s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double rho_old = a.pu_p != nullptr ? a.state->rho : 0.0;  // read before any CTA updates it
   // rows split evenly over the CTAs (time ~ rows streamed), groups of ROWS from each start
   const int64_t rbeg = a.rows * blockIdx.x / gridDim.x;
   const int64_t rend = a.rows * (blockIdx.x + 1) / gridDim.x;
@@ -253,6 +254,60 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
         if ((lane & (2 * off - 1)) == 0) pair_add(part, o);
       }
     }
+  }
+  if (a.pu_p != nullptr) {
+    // ---- fused direction update: r.theta over the CTA pairs in CTA order (the same value in
+    // every CTA), beta, then p = fma(beta, p, theta) on this CTA's rows (pcg_pupdate_kernel)
+    if (warp == 0 && lane == 0) a.partials[blockIdx.x] = part;
+    grid_barrier(a.pu_bar, a.pu_bar + 1, 1, kConsumers);
+    __shared__ double s_beta;
+    __shared__ int s_ok;
+    if (warp == 0) {
+      dd_pair v = {0.0, 0.0};
+      for (int i = lane; i < (int)gridDim.x; i += 32) {
+        dd_pair o = {__ldcg(&a.partials[i].s), __ldcg(&a.partials[i].c)};
+        pair_add(v, o);
+      }
+      v = warp_reduce_pair(v);
+      if (lane == 0) {
+        const double rt = pair_value(v);
+        s_ok = rt > 0.0;
+        s_beta = s_ok ? __ddiv_rn(rt, rho_old) : 0.0;
+        if (blockIdx.x == 0) {
+          PcgState *st = a.state;
+          if (!s_ok) {
+            st->term = LAKER_TERM_INDEFINITE;
+            st->done = 1;
+          } else {
+            pcg_set_beta(st, s_beta);
+            st->rho = rt;
+          }
+        }
+      }
+    }
+    named_bar_sync(1, kConsumers);
+    if (!s_ok) return;
+    const double beta = s_beta;
+    double m = 0.0;
+    for (int64_t i = rbeg + tid; i < rend; i += kConsumers) {
+      const double pi = __fma_rn(beta, a.pu_p[a.row0 + i], __ldcg(&a.y[i]));
+      a.pu_p[a.row0 + i] = pi;
+      m = fmax(m, fabs(pi));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    __shared__ double s_m[kWarps];
+    if (lane == 0) s_m[warp] = m;
+    named_bar_sync(1, kConsumers);
+    if (tid == 0) {
+      for (int w = 1; w < kWarps; ++w) m = fmax(m, s_m[w]);
+      a.pu_pmax[blockIdx.x] = m;
+      if (blockIdx.x == gridDim.x - 1 && a.pu_budget && a.state->iters >= a.state->max_iters) {
+        a.state->term = LAKER_TERM_MAX_ITERS;
+        a.state->done = 1;
+      }
+    }
+    return;
   }
   if (warp == 0) {
     if (lane == 0) {

@@ -47,7 +47,43 @@ __device__ __forceinline__ void pcg_set_beta(PcgState *st, double b) {
 
 // Ticket counters for the "last CTA reduces" epilogues, one per reduction
 // site, reset by the last CTA.
-enum { kCtrGemv = 0, kCtrUpdate = 1, kCtrInit = 2, kCtrMisc = 3, kNumCtr = 8 };
+enum { kCtrGemv = 0, kCtrUpdate = 1, kCtrInit = 2, kCtrMisc = 3, kCtrBar = 4, kCtrBarGen = 5, kNumCtr = 8 };
+
+// Software grid barrier for kernels whose CTAs are all co-resident (persistent grids sized
+// to the SMs): the calling threads of a CTA (`nthr` of them, named barrier `bar_id`) meet,
+// thread 0 arrives on count and waits for the generation to move.  count / gen are zero /
+// arbitrary at rest (the last arriver resets count).
+__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int *gen, int bar_id, int nthr) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthr) : "memory");
+  if (threadIdx.x == 0) {
+    const unsigned int g = *(volatile unsigned int *)gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*(volatile unsigned int *)gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthr) : "memory");
+}
+
+// The PCG step that follows an operator apply, fused into the apply's finalize (symv.cu):
+// delta = rho / p.q, alpha += delta p, r -= delta q, ||r||^2 (and r.theta, Jacobi) and the
+// termination test of pcg_update_kernel (pcg_kernels.cuh) -- the same fma / Dot2 operations.
+struct FusedUpdate {
+  int on;
+  int pk;
+  const double *p;       // the direction (x of the apply)
+  double *alpha, *r, *theta;
+  const double *dvec;    // Jacobi diagonal
+  double *hist;
+  unsigned int *bar;     // [2] grid barrier count, generation
+  dd_pair *partials2;    // >= gridDim x 2
+  unsigned int *counter2;
+};
 
 struct Buf {
   void *p = nullptr;
@@ -178,6 +214,16 @@ struct GemvArgs {
   int nxparts;
   // symv on a row-sharded plan: the unrounded pair of every row i < n (pcg_dist.cu)
   dd_pair *ypair;
+  // symv on one rank inside the PCG (epi = kEpiDelta): the update step fused in
+  FusedUpdate upd;
+  // gemv with epi = kEpiBeta (the preconditioner's last pass, one rank): the direction
+  // update p = fma(beta, p, theta) of pcg_pupdate_kernel fused in after a grid barrier
+  // (persistent grid, one CTA per SM); the per-CTA max |p| go to pu_pmax[blockIdx]; with
+  // pu_budget the iteration budget is closed after it (MAX_ITERS)
+  double *pu_p;
+  double *pu_pmax;
+  int pu_budget;
+  unsigned int *pu_bar;
 };
 void launch_gemv(const GemvArgs &a, int grid, cudaStream_t s);
 void gemv_init();

@@ -61,7 +61,7 @@ void lanczos_extremes(const std::vector<double> &dl, const std::vector<double> &
 
 // The operator apply used by the solver: q = (lambda I + K) p.
 static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState *st, int epi, double *dot_out,
-                            const double *pmax = nullptr, int npmax = 0) {
+                            const double *pmax = nullptr, int npmax = 0, const FusedUpdate *upd = nullptr) {
   if (ctx->storage == LAKER_STORE_MATERIALIZED) {
     GemvArgs a{};
     a.A = ctx->K;
@@ -81,6 +81,7 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
     if (ctx->k_sym) {
       a.xparts = pmax;
       a.nxparts = npmax;
+      if (upd) a.upd = *upd;
       launch_symv(ctx->symv, 0, a, ctx->stream);
       ctx->stats.kernel_launches++;
     } else {
@@ -101,7 +102,10 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
   ctx->stats.kernel_launches++;
 }
 
-static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgState *st, int epi, double *dot_out) {
+// pu_p != null (epi = kEpiBeta, factored P): the last pass also forms p = theta + beta p
+// (gemv.cu fused direction update) and the per-CTA max |p| into pu_pmax
+static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgState *st, int epi, double *dot_out,
+                           double *pu_p = nullptr, double *pu_pmax = nullptr) {
   if (ctx->p_factored) {
     // theta = a^{-1/2} r + Q (M (Q^T r)): three Dot2 GEMV passes (NEXT-1); the last
     // one carries the a^{-1/2} r_i term and the r.theta epilogue
@@ -115,6 +119,7 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
       GemvArgs t = z;
       t.A = ctx->QMf + ctx->r0 * ldq; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fz;
       t.row0 = ctx->r0; t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
+      t.pu_p = pu_p; t.pu_pmax = pu_pmax; t.pu_budget = 1; t.pu_bar = ctx->counters + kCtrBar;
       launch_gemv(t, ctx->gemv_grid, ctx->stream);
       ctx->stats.kernel_launches += 2;
       return;
@@ -126,6 +131,7 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
     GemvArgs t = z;
     t.A = ctx->Qr + ctx->r0 * ldq; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fw; t.row0 = ctx->r0;
     t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
+    t.pu_p = pu_p; t.pu_pmax = pu_pmax; t.pu_budget = 1; t.pu_bar = ctx->counters + kCtrBar;
     launch_gemv(t, ctx->gemv_grid, ctx->stream);
     ctx->stats.kernel_launches += 3;
     return;
@@ -234,18 +240,35 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     evs.resize(4 * chunk);
     for (auto &e : evs) cudaEventCreate(&e);
   }
+  // the update step (alpha, r, ||r||, termination) rides in the symmetric apply's finalize
+  // (a grid barrier for delta instead of a kernel boundary; symv.cu)
+  const bool fuse_upd = ctx->k_sym && ctx->storage == LAKER_STORE_MATERIALIZED;
+  // the direction update rides in the factored preconditioner's last pass (gemv.cu)
+  const bool fuse_pu = dense && ctx->p_factored;
+  // symv offsets: max |p| over the per-CTA maxima of whichever kernel formed p last
+  // (pcg_first_dir_kernel: vg CTAs at init, the fused pass: <= gemv_grid CTAs; pmax is
+  // zeroed at solve start, vg <= that grid)
+  const int npmax = fuse_pu ? std::max(vg, ctx->gemv_grid) : vg;
+  FusedUpdate fu{};
+  fu.on = 1; fu.pk = pk; fu.p = w.p; fu.alpha = w.alpha; fu.r = w.r; fu.theta = w.theta; fu.dvec = ctx->Pdiag;
+  fu.hist = w.hist; fu.bar = ctx->counters + kCtrBar; fu.partials2 = ctx->partials + 2048;
+  fu.counter2 = ctx->counters + kCtrUpdate;
   auto record_iteration = [&](int j) {
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
-    launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, vg);
+    launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, npmax, fuse_upd ? &fu : nullptr);
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
-    pcg_update_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, pk, (const double *)ctx->Pdiag, (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials, ctx->counters + kCtrUpdate);
+    if (!fuse_upd)
+      pcg_update_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, pk, (const double *)ctx->Pdiag, (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials, ctx->counters + kCtrUpdate);
     if (dense) {
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
-      launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr);
+      launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr, fuse_pu ? w.p : nullptr, fuse_pu ? pmax : nullptr);
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
     }
-    pcg_pupdate_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
-    ctx->stats.kernel_launches += 2;
+    if (!fuse_pu) {
+      pcg_pupdate_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
+      ctx->stats.kernel_launches++;
+    }
+    if (!fuse_upd) ctx->stats.kernel_launches++;
   };
 
   // capture one chunk into a graph

@@ -372,6 +372,114 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
   dotp = warp_reduce_pair(dotp);
   if (lane == 0) sred[warp] = dotp;
   __syncthreads();
+  if (a.upd.on) {
+    // ---- the PCG update step fused in (all CTAs co-resident, grid <= symv_fused_grid)
+    if (tid == 0) {
+      dd_pair t = sred[0];
+      for (int w = 1; w < kFinThreads / 32; ++w) pair_add(t, sred[w]);
+      a.partials[blockIdx.x] = t;
+    }
+    grid_barrier(a.upd.bar, a.upd.bar + 1, 1, kFinThreads);
+    __shared__ double s_delta;
+    __shared__ int s_ok;
+    PcgState *st = a.state;
+    if (warp == 0) {  // p.q over the CTA pairs in CTA order: the same value in every CTA
+      dd_pair v = {0.0, 0.0};
+      for (int b = lane; b < (int)gridDim.x; b += 32) pair_add(v, ldcg_pair(&a.partials[b]));
+      v = warp_reduce_pair(v);
+      if (lane == 0) {
+        const double pq = pair_value(v);
+        s_ok = pq > 0.0;
+        s_delta = s_ok ? __ddiv_rn(st->rho, pq) : 0.0;
+      }
+    }
+    __syncthreads();
+    const bool ok = s_ok != 0;
+    const double delta = s_delta;
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) {
+      if (!ok) {
+        st->term = LAKER_TERM_BREAKDOWN;
+        st->done = 1;
+      } else {
+        pcg_set_delta(st, delta);
+      }
+    }
+    if (!ok) return;
+    const FusedUpdate &u = a.upd;
+    dd_pair v0 = {0.0, 0.0}, v1 = {0.0, 0.0};
+    for (int64_t g = blockIdx.x + (int64_t)warp * gridDim.x; g * 32 < a.n; g += (int64_t)kW * gridDim.x) {
+      const int64_t i = g * 32 + lane;
+      if (i >= a.n) continue;
+      u.alpha[i] = __fma_rn(delta, u.p[i], u.alpha[i]);
+      const double ri = __fma_rn(-delta, __ldcg(&a.y[i]), u.r[i]);
+      u.r[i] = ri;
+      dot2_step(v0, ri, ri);
+      if (u.pk == LAKER_PRECOND_JACOBI) {
+        const double th = __dmul_rn(u.dvec[i], ri);
+        u.theta[i] = th;
+        dot2_step(v1, ri, th);
+      }
+    }
+    v0 = warp_reduce_pair(v0);
+    v1 = warp_reduce_pair(v1);
+    __shared__ dd_pair sr2[kFinThreads / 32][2];
+    if (lane == 0) {
+      sr2[warp][0] = v0;
+      sr2[warp][1] = v1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      dd_pair t0 = sr2[0][0], t1 = sr2[0][1];
+      for (int w = 1; w < kW; ++w) {
+        pair_add(t0, sr2[w][0]);
+        pair_add(t1, sr2[w][1]);
+      }
+      u.partials2[2 * blockIdx.x] = t0;
+      u.partials2[2 * blockIdx.x + 1] = t1;
+      __threadfence();
+      s_last = (atomicAdd(u.counter2, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last || warp != 0) return;
+    __threadfence();
+    dd_pair t0 = {0.0, 0.0}, t1 = {0.0, 0.0};
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      pair_add(t0, ldcg_pair(&u.partials2[2 * b]));
+      pair_add(t1, ldcg_pair(&u.partials2[2 * b + 1]));
+    }
+    t0 = warp_reduce_pair(t0);
+    t1 = warp_reduce_pair(t1);
+    if (lane != 0) return;
+    *u.counter2 = 0u;
+    // the termination / beta epilogue of pcg_update_kernel
+    const double rr = pair_value(t0);
+    const double rel = __ddiv_rn(__dsqrt_rn(rr), st->ynorm);
+    const int it = st->iters + 1;
+    st->iters = it;
+    st->rel = rel;
+    if (u.hist) u.hist[it - 1] = rel;
+    if (rel <= st->tol) {
+      st->term = LAKER_TERM_RESIDUAL_TOL;
+      st->done = 1;
+      return;
+    }
+    if (u.pk != LAKER_PRECOND_EXTERNAL_DENSE && u.pk != LAKER_PRECOND_LEARNED) {
+      const double rho_new = (u.pk == LAKER_PRECOND_NONE) ? rr : pair_value(t1);
+      if (!(rho_new > 0.0)) {
+        st->term = LAKER_TERM_INDEFINITE;
+        st->done = 1;
+        return;
+      }
+      pcg_set_beta(st, __ddiv_rn(rho_new, st->rho));
+      st->rho = rho_new;
+      if (it >= st->max_iters) {
+        st->term = LAKER_TERM_MAX_ITERS;
+        st->done = 1;
+      }
+    }
+    return;
+  }
   if (tid == 0) {
     dd_pair t = sred[0];
     for (int w = 1; w < kFinThreads / 32; ++w) pair_add(t, sred[w]);
@@ -562,6 +670,18 @@ struct SymvPlan {
 };
 
 size_t symv_smem_bytes() { return kSymSmem; }
+
+// CTAs of symv_finalize_kernel<kSR> guaranteed co-resident (the fused update's grid barrier)
+int fused_fin_grid() {
+  static int g = 0;
+  if (g == 0) {
+    int per = 0, sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, symv_finalize_kernel<kSR>, kFinThreads, 0);
+    g = std::max(1, std::min(per, 2)) * sms;
+  }
+  return g;
+}
 
 void symv_init() {
   cudaFuncSetAttribute(symv_dot2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSymSmem);
@@ -821,12 +941,15 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     a.nxparts = kXParts;
   }
   a.ypair = g.ypair;
+  a.upd = g.upd;
   if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else
     symv_dot2_kernel<false><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   if (p->dist)
     tri_finalize_dist_kernel<kSR, kSC><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
+  else if (g.upd.on)  // co-resident grid for the grid barrier
+    symv_finalize_kernel<kSR><<<dim3(std::min(p->fin_grid, fused_fin_grid())), dim3(kFinThreads), 0, s>>>(a);
   else
     symv_finalize_kernel<kSR><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
 }

@@ -53,6 +53,7 @@ struct SymvArgs {
   const int32_t *cr_lo, *cr_hi;
   dd_pair *ypair;
   int64_t own0, own1;  // global rows whose row partials this rank holds
+  FusedUpdate upd;     // single-rank K apply inside the PCG: the update step fused (symv.cu)
 };
 
 // partition of an n x n symmetric apply into BR x TC tiles over `grid` CTAs
