@@ -235,7 +235,7 @@ void dgemm_init() {
 void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return;
   // large contractions: fp64 emulated on the int8 tcgen05 tensor cores (ozaki.cu)
-  if (ozaki_eligible(g) && launch_ozaki_gemm(g, b_kn, 0, s) == cudaSuccess) return;
+  if (ozaki_eligible(g) && launch_ozaki_gemm(g, b_kn, g.oz_slices, s) == cudaSuccess) return;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int64_t tiles_l = ((g.N + 127) / 128) * ((g.M + 127) / 128);

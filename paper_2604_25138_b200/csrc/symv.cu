@@ -678,7 +678,7 @@ int fused_fin_grid() {
     int per = 0, sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, symv_finalize_kernel<kSR>, kFinThreads, 0);
-    g = std::max(1, std::min(per, 2)) * sms;
+    g = std::max(1, per) * sms;
   }
   return g;
 }
