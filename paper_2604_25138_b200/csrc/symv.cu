@@ -408,12 +408,14 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
     if (!ok) return;
     const FusedUpdate &u = a.upd;
     dd_pair v0 = {0.0, 0.0}, v1 = {0.0, 0.0};
+    double rm = 0.0;
     for (int64_t g = blockIdx.x + (int64_t)warp * gridDim.x; g * 32 < a.n; g += (int64_t)kW * gridDim.x) {
       const int64_t i = g * 32 + lane;
       if (i >= a.n) continue;
       u.alpha[i] = __fma_rn(delta, u.p[i], u.alpha[i]);
       const double ri = __fma_rn(-delta, __ldcg(&a.y[i]), u.r[i]);
       u.r[i] = ri;
+      rm = fmax(rm, fabs(ri));
       dot2_step(v0, ri, ri);
       if (u.pk == LAKER_PRECOND_JACOBI) {
         const double th = __dmul_rn(u.dvec[i], ri);
@@ -423,12 +425,20 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
     }
     v0 = warp_reduce_pair(v0);
     v1 = warp_reduce_pair(v1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
     __shared__ dd_pair sr2[kFinThreads / 32][2];
+    __shared__ double srm[kFinThreads / 32];
     if (lane == 0) {
       sr2[warp][0] = v0;
       sr2[warp][1] = v1;
+      srm[warp] = rm;
     }
     __syncthreads();
+    if (tid == 0 && u.rmax_parts) {
+      for (int w = 1; w < kW; ++w) rm = fmax(rm, srm[w]);
+      u.rmax_parts[blockIdx.x] = rm;
+    }
     if (tid == 0) {
       dd_pair t0 = sr2[0][0], t1 = sr2[0][1];
       for (int w = 1; w < kW; ++w) {
@@ -898,6 +908,8 @@ void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s) {
 }
 
 double *symv_rowmax_ptr(SymvPlan *p, int which) { return p->rowmax[which]; }
+
+int symv_fused_grid(const SymvPlan *p) { return std::min(p->fin_grid, fused_fin_grid()); }
 
 // which = 0 (K) or 1 (P); (re)encodes the tensor map when the base pointer changed
 bool symv_bind(SymvPlan *p, int which, const double *A) {
