@@ -771,10 +771,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     const double sk = std::sqrt(sigma);
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.lda = g.ldb = g.ldc = nrp; g.tri = 1;
-    // the coupled phase only has to bring ||W - I|| below 1e-3 for the self-correcting
-    // uncoupled refinement below (full precision), so its products run with 5 int8 slices
-    // (~2^-34 relative to |A||B|, 15 slice pairs instead of 36)
-    g.oz_slices = 5;
+
     g.A = Zm; g.B = Y; g.C = W; g.alpha = -0.5 * sigma; g.diag = 1.5;
     launch_dgemm(g, true, s);
     launch_mirror_lower(W, nrp, nrp, s);

@@ -127,7 +127,7 @@ def run_c5_learned(max_iters=4000):
     c = L.Context(0)
     E = torch.from_numpy(P.E).to(dev)
     c.assemble_kernel(E, P.scale, P.lam, L.STORE_ON_THE_FLY, L.MODE_FAST)
-    fit = c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7, p_layout=L.P_FACTORED)
+    fit = c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7)
     a, reps, _ = c.pcg_solve(torch.from_numpy(P.y).to(dev), P.tol, max_iters=max_iters, instrument=True)
     r = reps[0]
     st = c.stats()
