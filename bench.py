@@ -362,15 +362,18 @@ def run_ours(args, rank, world, local_rank):
     # algorithmic bytes per operator apply: the stored
     # triangle of the symmetric K (symv) or the local rows (gemv), plus x read and y written
     if sym:
-        bytes_per_launch = 8.0 * n * (n + 1) / 2 + 16.0 * n
-        kname = "symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, offset-Fast2Sum compensated sums)"
+        # the stored triangle + x read + y written, + the fused update's alpha/r read+write and p read
+        bytes_per_launch = 8.0 * n * (n + 1) / 2 + 16.0 * n + (40.0 * n if world == 1 else 0.0)
+        kname = ("symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, offset-Fast2Sum "
+                 "compensated sums; the PCG update step fused into the finalize)")
     else:
         bytes_per_launch = 8.0 * rows * n + 16.0 * n
         kname = "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)"
     if fac == 2:
         # QM form (R21); sharded: N_r/W rows of Q^T and n/W rows of QM per rank
-        prec_bytes = 8.0 * (2 * n * nr) / world + 8.0 * (3 * n + 2 * nr)
-        pname = "2 x gemv_dot2_kernel: z = Q^T r, theta = a^-1/2 r + QM z (factored P, QM = Q M)"
+        prec_bytes = 8.0 * (2 * n * nr) / world + 8.0 * (3 * n + 2 * nr) + (16.0 * n if world == 1 else 0.0)
+        pname = ("2 x gemv_dot2_kernel: z = Q^T r, theta = a^-1/2 r + QM z (factored P, QM = Q M; offset-Fast2Sum "
+                 "rows; the direction update p = theta + beta p fused into the theta pass)")
     elif fac:
         # sharded (pcg_dist.cu): each rank streams N_r/W rows of Q^T and M and n/W rows of Q
         prec_bytes = 8.0 * (2 * n * nr + nr * nr) / world + 8.0 * (3 * n + 4 * nr)

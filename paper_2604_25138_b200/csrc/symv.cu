@@ -35,6 +35,7 @@
 // the oracle's sequential Dot2 (tests/test_gpu_symv.py).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "laker_internal.h"
@@ -133,9 +134,13 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         const int jt = a.jt_of ? a.jt_of[t] : kTPD * I + (int)(t - rbeg);
         if (!first) mbar_wait(&empty[slot], ph ^ 1u);
         unsigned char *st = smem + slot * kStageBytes;
-        mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
-        tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
-        bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
+        if (a.dbg_noload && !first) {
+          mbar_arrive(&full[slot]);
+        } else {
+          mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
+          tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
+          bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
+        }
         if (++slot == kSStages) {
           slot = 0;
           ph ^= 1u;
@@ -269,8 +274,8 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         }
       }
     } else {
-      // k-major over both column halves: per row k the products with x_c and x_{c+32}
-      // (in that order, as the diagonal tiles do), and two independent column chains
+      // k-major over the thread's two columns: per row k the products with x_{2c} and
+      // x_{2c+1} (in that order, as the diagonal tiles do), and two independent column chains
       const double2 xcv = reinterpret_cast<const double2 *>(tile + kSR * kSC)[c];
       const double xc0 = xcv.x, xc1 = xcv.y;
       const double *tp = tile + warp * kRPT * kSC + 2 * c;
@@ -954,6 +959,11 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   }
   a.ypair = g.ypair;
   a.upd = g.upd;
+  {
+    static int nl = -1;  // TEMP experiment
+    if (nl < 0) nl = std::getenv("LAKER_DBG_NOLOAD") ? 1 : 0;
+    a.dbg_noload = nl;
+  }
   if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else

@@ -19,9 +19,11 @@ def L():
     return laker
 
 
+# n = 1000: n/W is not a multiple of 256, so the sharded path streams full K rows (gemv)
 @pytest.mark.parametrize("cid,n,kind", [(1, None, "none"), (1, None, "jacobi"), (2, None, "learned"),
                                         (2, None, "factored"), (3, 2048, "factored"),
-                                        (3, 1024, "jacobi"), (1, None, "onthefly")])
+                                        (3, 1024, "jacobi"), (3, 1000, "jacobi"), (3, 1000, "factored"),
+                                        (1, None, "onthefly")])
 def test_collective_path_equals_single(L, cid, n, kind):
     P = make_problem(cid, n=n)
     res = []
