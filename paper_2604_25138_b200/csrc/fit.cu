@@ -346,19 +346,6 @@ struct DevMem {
   }
 };
 
-// rm[i] = max_j |A_ij| over `cols` columns (one warp per row)
-__global__ void rowabs_max_kernel(const double *__restrict__ A, int64_t rows, int64_t cols, int64_t lda,
-                                  double *__restrict__ rm) {
-  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (i >= rows) return;
-  double v = 0.0;
-  for (int64_t j = lane; j < cols; j += 32) v = fmax(v, fabs(A[i * lda + j]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if (lane == 0) rm[i] = v;
-}
-
 double host_rho(int64_t nr, int64_t n, double gamma, double lmin, double rho_floor) {
   double rho;
   if (nr >= n) {
@@ -374,8 +361,6 @@ double host_rho(int64_t nr, int64_t n, double gamma, double lmin, double rho_flo
 }  // namespace
 
 void free_factors(laker_ctx ctx) {
-  cudaFree(ctx->f_rm_qt);
-  ctx->f_rm_qt = ctx->f_rm_qm = nullptr;
   cudaFree(ctx->Qt);
   cudaFree(ctx->Qr);
   cudaFree(ctx->Mf);
@@ -771,7 +756,6 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     const double sk = std::sqrt(sigma);
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.lda = g.ldb = g.ldc = nrp; g.tri = 1;
-
     g.A = Zm; g.B = Y; g.C = W; g.alpha = -0.5 * sigma; g.diag = 1.5;
     launch_dgemm(g, true, s);
     launch_mirror_lower(W, nrp, nrp, s);
@@ -928,15 +912,6 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     ctx->f_ldq = ldq;
     ctx->f_ainv = ainv;
     ctx->p_factored = true;
-    if (!loc && ctx->p_qm) {  // the QM-form passes' offsets (one rank): row maxima of Q^T and QM
-      if (!ctx->f_rm_qt) {
-        LAKER_CUDA(ctx, cudaMalloc(&ctx->f_rm_qt, (size_t)(nrp + n) * 8));
-      }
-      ctx->f_rm_qm = ctx->f_rm_qt + nrp;
-      rowabs_max_kernel<<<(unsigned)((nrp + 7) / 8), 256, 0, s>>>(ctx->Qt, nrp, n, ld, ctx->f_rm_qt);
-      rowabs_max_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(ctx->QMf, n, nrp, ldq, ctx->f_rm_qm);
-      L += 2;
-    }
   } else {
     free_factors(ctx);
     LAKER_TRY(form_dense_p(ctx, Ut, Zm, nrp, nrp, ainv));

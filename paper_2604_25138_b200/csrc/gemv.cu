@@ -85,13 +85,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
   const int64_t ncp = (a.ncols + 255) / 256 * 256;  // padded columns actually streamed
   const int64_t nchunks = (ncp + kChunk - 1) / kChunk;
   const double *xsrc0 = a.x;
-  // offset accumulation: C_r = pow2_above(2 kprod rowmax_r max|x|), kprod products per
-  // thread and row (two per 1024-column chunk)
-  const bool off = a.arowmax != nullptr;
-  double xm = 0.0;
-  if (off)
-    for (int k = 0; k < a.nxmax; ++k) xm = fmax(xm, a.xmax_parts[k]);
-  const double okp = 2.0 * (double)(nchunks * kCPT) * xm;
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -145,12 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
     double *xrow = xrow_buf[gpar];
     const int64_t own0 = a.row0 + rb;  // global index of the group's first row
     dd_pair acc[ROWS];
-    double coff[ROWS];
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      coff[r] = (off && r < nr) ? pow2_above(a.arowmax[rb + r] * okp) : 0.0;
-      acc[r] = dd_pair{coff[r], 0.0};
-    }
+    for (int r = 0; r < ROWS; ++r) acc[r] = dd_pair{0.0, 0.0};
     for (int64_t c = 0; c < nchunks; ++c) {
       mbar_wait(&full[slot], ph);
       const int64_t col0 = c * kChunk;
@@ -164,23 +153,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
             if (o <= 0 && -o < nr) xrow[-o] = x0.x;
             if (o <= 1 && 1 - o < nr) xrow[1 - o] = x0.y;
           }
-          if (off) {
 #pragma unroll
-            for (int r = 0; r < ROWS; ++r) {
-              if (r < nr) {
-                const double2 v0 = *reinterpret_cast<const double2 *>(sp + r * kChunk);
-                dot2_step_off(acc[r], v0.x, x0.x);
-                dot2_step_off(acc[r], v0.y, x0.y);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int r = 0; r < ROWS; ++r) {
-              if (r < nr) {
-                const double2 v0 = *reinterpret_cast<const double2 *>(sp + r * kChunk);
-                dot2_step(acc[r], v0.x, x0.x);
-                dot2_step(acc[r], v0.y, x0.y);
-              }
+          for (int r = 0; r < ROWS; ++r) {
+            if (r < nr) {
+              const double2 v0 = *reinterpret_cast<const double2 *>(sp + r * kChunk);
+              dot2_step(acc[r], v0.x, x0.x);
+              dot2_step(acc[r], v0.y, x0.y);
             }
           }
         }
@@ -198,10 +176,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       // fixed-shape shuffle tree; red / xrow double-buffered by group parity, so one
       // CTA barrier per group
       static_assert(ROWS == 8, "reduce-scatter layout assumes 8 rows");
-      if (off) {
-#pragma unroll
-        for (int r = 0; r < ROWS; ++r) acc[r].s = __dsub_rn(acc[r].s, coff[r]);  // exact: acc.s in [C/2, 3C/2]
-      }
       dd_pair v4[4], v2[2], v1;
       const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
@@ -352,13 +326,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       pair_add(v, o);
     }
     v = warp_reduce_pair(v);
-    if (a.ymax_out != nullptr) {  // max |y| over every CTA's rows (the next pass's offsets)
-      double m = 0.0;
-      for (int64_t i = lane; i < a.rows; i += 32) m = fmax(m, fabs(__ldcg(&a.y[i])));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) *a.ymax_out = m;
-    }
     if (lane == 0) {
       *a.counter = 0u;
       if (a.epi == kEpiStorePair)

@@ -83,7 +83,6 @@ struct FusedUpdate {
   unsigned int *bar;     // [2] grid barrier count, generation
   dd_pair *partials2;    // >= gridDim x 2
   unsigned int *counter2;
-  double *rmax_parts;    // nullable: per-CTA max |r_i| of the updated residual
 };
 
 struct Buf {
@@ -151,9 +150,6 @@ struct laker_ctx_s {
   double *QMf = nullptr;            // n x f_ldq  QM = Q M (R21: theta = a^-1/2 r + QM (Q^T r))
   bool f_local = false;
   int64_t f_ldl = 0;
-  // max_k |Q^T_jk| per row of Q^T (nrp) and max_k |QM_ik| per row of QM (n): the offsets of
-  // the factored apply's GEMV passes (one rank)
-  double *f_rm_qt = nullptr, *f_rm_qm = nullptr;
   bool p_qm = false;                // the factored apply uses QMf (two passes)
   double *Mf = nullptr;             // nrp x f_ldq
   double *fz = nullptr, *fw = nullptr;  // f_ldq workspaces (z = Q^T r, w = M z), zero padded
@@ -216,16 +212,6 @@ struct GemvArgs {
   // null -> launch_symv computes them
   const double *xparts;
   int nxparts;
-  // offset accumulation (the symmetric apply's scheme, B6): with arowmax (max_j
-  // |A_ij| of the local rows) and the partial maxima xmax_parts[0 .. nxmax) of |x|, every
-  // row accumulator starts at the power of two C >= 2 kprod rowmax max|x| above its
-  // products, so each step is TwoProd + Fast2Sum (7 fp64 ops instead of Dot2's 10); null ->
-  // plain Dot2.  zmax_out (nullable): the last CTA writes max_i |y_i| there (the next
-  // pass's x maximum).
-  const double *arowmax;
-  const double *xmax_parts;
-  int nxmax;
-  double *ymax_out;
   // symv on a row-sharded plan: the unrounded pair of every row i < n (pcg_dist.cu)
   dd_pair *ypair;
   // symv on one rank inside the PCG (epi = kEpiDelta): the update step fused in
@@ -253,8 +239,6 @@ cudaError_t symv_plan(SymvPlan *&p, int64_t n, int64_t ld, int num_sms, int rank
                       bool dist = false);
 bool tri_is_dist(const SymvPlan *p);
 double *symv_rowmax_ptr(SymvPlan *p, int which);
-// CTAs of the finalize with the fused update (FusedUpdate::rmax_parts entries written)
-int symv_fused_grid(const SymvPlan *p);
 void symv_free(SymvPlan *&p);
 bool symv_bind(SymvPlan *p, int which, const double *A);
 void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s);

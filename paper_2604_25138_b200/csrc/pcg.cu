@@ -104,17 +104,8 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
 
 // pu_p != null (epi = kEpiBeta, factored P): the last pass also forms p = theta + beta p
 // (gemv.cu fused direction update) and the per-CTA max |p| into pu_pmax
-// off (QM form, one rank): offset accumulation in both passes -- the z pass with the
-// per-CTA maxima of |r| from the fused update (rmax, nrmax of them), the theta pass with
-// max |z| written by the z pass into *zmax
-struct PrecOffsets {
-  const double *rmax = nullptr;
-  int nrmax = 0;
-  double *zmax = nullptr;
-};
-
 static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgState *st, int epi, double *dot_out,
-                           double *pu_p = nullptr, double *pu_pmax = nullptr, const PrecOffsets *off = nullptr) {
+                           double *pu_p = nullptr, double *pu_pmax = nullptr) {
   if (ctx->p_factored) {
     // theta = a^{-1/2} r + Q (M (Q^T r)): three Dot2 GEMV passes (NEXT-1); the last
     // one carries the a^{-1/2} r_i term and the r.theta epilogue
@@ -123,22 +114,9 @@ static void launch_precond(laker_ctx ctx, const double *r, double *theta, PcgSta
     z.A = ctx->Qt; z.ld = ctx->ld; z.rows = nrp; z.ncols = ctx->n; z.x = r; z.row0 = 0; z.y = ctx->fz;
     z.state = st; z.partials = ctx->partials; z.counter = ctx->counters + kCtrGemv; z.epi = kEpiNone;
     z.evict_first = true;
-    const bool qoff = ctx->p_qm && ctx->f_rm_qt && off && off->zmax;
-    if (qoff) {
-      z.ymax_out = off->zmax;
-      if (off->rmax) {
-        z.arowmax = ctx->f_rm_qt;
-        z.xmax_parts = off->rmax;
-        z.nxmax = off->nrmax;
-      }
-    }
     launch_gemv(z, ctx->gemv_grid, ctx->stream);
     if (ctx->p_qm) {  // R21: theta = a^-1/2 r + QM z
       GemvArgs t = z;
-      t.ymax_out = nullptr;
-      t.arowmax = qoff ? ctx->f_rm_qm : nullptr;
-      t.xmax_parts = qoff ? off->zmax : nullptr;
-      t.nxmax = qoff ? 1 : 0;
       t.A = ctx->QMf + ctx->r0 * ldq; t.ld = ldq; t.rows = ctx->r1 - ctx->r0; t.ncols = nrp; t.x = ctx->fz;
       t.row0 = ctx->r0; t.y = theta; t.lambda = ctx->f_ainv; t.xd = r; t.epi = epi; t.dot_out = dot_out;
       t.pu_p = pu_p; t.pu_pmax = pu_pmax; t.pu_budget = 1; t.pu_bar = ctx->counters + kCtrBar;
@@ -214,7 +192,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
 
   Workspace w;
   const size_t vb = (size_t)ld * sizeof(double);
-  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 6 * vb + (2 + 256 + 1024 + 8) * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMallocAsync(&w.alpha, 6 * vb + (2 + 256) * sizeof(double), s));
   w.r = w.alpha + ld;
   w.theta = w.r + ld;
   w.p = w.theta + ld;
@@ -222,8 +200,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   w.y = w.q + ld;
   w.scal = w.y + ld;
   double *pmax = w.scal + 2;  // per-CTA max |p| from the vector kernels (vg <= 148 entries), for symv
-  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 6 * vb + (2 + 256 + 1024 + 8) * sizeof(double), s));
-  double *rmaxp = pmax + 256, *zmax = rmaxp + 1024;  // fused update's per-CTA max |r|; max |z|
+  LAKER_CUDA(ctx, cudaMemsetAsync(w.alpha, 0, 6 * vb + (2 + 256) * sizeof(double), s));
   LAKER_CUDA(ctx, cudaMallocAsync(&w.hist, (size_t)3 * max_iters * sizeof(double), s));
   double *dh = w.hist + max_iters, *bh = dh + max_iters;  // CG coefficients (Lanczos estimates)
   LAKER_CUDA(ctx, cudaMallocAsync(&w.st, sizeof(PcgState), s));
@@ -244,9 +221,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   tmark("ev0");
 
   pcg_init_kernel<<<vg, kVecThreads, 0, s>>>(n, w.y, w.alpha, w.r, w.st, ctx->partials, ctx->counters + kCtrInit);
-  PrecOffsets poff0;  // theta^0: no |r| maxima yet (r = y); the z pass still records max |z|
-  poff0.zmax = zmax;
-  if (dense) launch_precond(ctx, w.r, w.theta, w.st, kEpiStoreDot, &w.st->rho, nullptr, nullptr, &poff0);
+  if (dense) launch_precond(ctx, w.r, w.theta, w.st, kEpiStoreDot, &w.st->rho);
   pcg_first_dir_kernel<<<vg, kVecThreads, 0, s>>>(n, pk, ctx->Pdiag, w.r, w.theta, w.p, w.st, ctx->partials,
                                                   ctx->counters + kCtrInit, pmax);
   ctx->stats.kernel_launches += 2;
@@ -278,13 +253,6 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   fu.on = 1; fu.pk = pk; fu.p = w.p; fu.alpha = w.alpha; fu.r = w.r; fu.theta = w.theta; fu.dvec = ctx->Pdiag;
   fu.hist = w.hist; fu.bar = ctx->counters + kCtrBar; fu.partials2 = ctx->partials + 2048;
   fu.counter2 = ctx->counters + kCtrUpdate;
-  fu.rmax_parts = rmaxp;
-  PrecOffsets poff;
-  if (fuse_upd && symv_fused_grid(ctx->symv) <= 1024) {
-    poff.rmax = rmaxp;
-    poff.nrmax = symv_fused_grid(ctx->symv);
-  }
-  poff.zmax = zmax;
   auto record_iteration = [&](int j) {
     if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
     launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, npmax, fuse_upd ? &fu : nullptr);
@@ -293,8 +261,7 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
       pcg_update_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, pk, (const double *)ctx->Pdiag, (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials, ctx->counters + kCtrUpdate);
     if (dense) {
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
-      launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr, fuse_pu ? w.p : nullptr, fuse_pu ? pmax : nullptr,
-                     &poff);
+      launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr, fuse_pu ? w.p : nullptr, fuse_pu ? pmax : nullptr);
       if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
     }
     if (!fuse_pu) {

@@ -35,7 +35,6 @@
 // the oracle's sequential Dot2 (tests/test_gpu_symv.py).
 #include <cuda.h>
 
-#include <cstdlib>
 #include <vector>
 
 #include "laker_internal.h"
@@ -134,13 +133,9 @@ __global__ void __launch_bounds__(kSymThreads, 1)
         const int jt = a.jt_of ? a.jt_of[t] : kTPD * I + (int)(t - rbeg);
         if (!first) mbar_wait(&empty[slot], ph ^ 1u);
         unsigned char *st = smem + slot * kStageBytes;
-        if (a.dbg_noload && !first) {
-          mbar_arrive(&full[slot]);
-        } else {
-          mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
-          tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
-          bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
-        }
+        mbar_arrive_expect_tx(&full[slot], kTileBytes + kXBytes);
+        tma_load_2d(st, &tm, jt * kSC, I * kSR, &full[slot], pol_a);
+        bulk_g2s(st + kTileBytes, a.x + (int64_t)jt * kSC, kXBytes, &full[slot], pol_x);
         if (++slot == kSStages) {
           slot = 0;
           ph ^= 1u;
@@ -413,14 +408,12 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
     if (!ok) return;
     const FusedUpdate &u = a.upd;
     dd_pair v0 = {0.0, 0.0}, v1 = {0.0, 0.0};
-    double rm = 0.0;
     for (int64_t g = blockIdx.x + (int64_t)warp * gridDim.x; g * 32 < a.n; g += (int64_t)kW * gridDim.x) {
       const int64_t i = g * 32 + lane;
       if (i >= a.n) continue;
       u.alpha[i] = __fma_rn(delta, u.p[i], u.alpha[i]);
       const double ri = __fma_rn(-delta, __ldcg(&a.y[i]), u.r[i]);
       u.r[i] = ri;
-      rm = fmax(rm, fabs(ri));
       dot2_step(v0, ri, ri);
       if (u.pk == LAKER_PRECOND_JACOBI) {
         const double th = __dmul_rn(u.dvec[i], ri);
@@ -430,20 +423,12 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
     }
     v0 = warp_reduce_pair(v0);
     v1 = warp_reduce_pair(v1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
     __shared__ dd_pair sr2[kFinThreads / 32][2];
-    __shared__ double srm[kFinThreads / 32];
     if (lane == 0) {
       sr2[warp][0] = v0;
       sr2[warp][1] = v1;
-      srm[warp] = rm;
     }
     __syncthreads();
-    if (tid == 0 && u.rmax_parts) {
-      for (int w = 1; w < kW; ++w) rm = fmax(rm, srm[w]);
-      u.rmax_parts[blockIdx.x] = rm;
-    }
     if (tid == 0) {
       dd_pair t0 = sr2[0][0], t1 = sr2[0][1];
       for (int w = 1; w < kW; ++w) {
@@ -914,8 +899,6 @@ void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s) {
 
 double *symv_rowmax_ptr(SymvPlan *p, int which) { return p->rowmax[which]; }
 
-int symv_fused_grid(const SymvPlan *p) { return std::min(p->fin_grid, fused_fin_grid()); }
-
 // which = 0 (K) or 1 (P); (re)encodes the tensor map when the base pointer changed
 bool symv_bind(SymvPlan *p, int which, const double *A) {
   if (p->tm_base[which] == A) return true;
@@ -959,11 +942,6 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   }
   a.ypair = g.ypair;
   a.upd = g.upd;
-  {
-    static int nl = -1;  // TEMP experiment
-    if (nl < 0) nl = std::getenv("LAKER_DBG_NOLOAD") ? 1 : 0;
-    a.dbg_noload = nl;
-  }
   if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else

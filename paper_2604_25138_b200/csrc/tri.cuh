@@ -38,7 +38,6 @@ struct SymvArgs {
   dd_pair *partials;  // finalize: per-CTA pairs
   unsigned int *counter;
   int evict_first;
-  int dbg_noload;  // TEMP experiment: after the first ring fill the producer re-arms without loading
   // symv: per-row max |A_ij| (padded with zeros to nct * TC) and per-CTA maxima of |x_j|
   // (max over nxparts values = max |x|): the offsets of dot2_step_off
   const double *rowmax;
