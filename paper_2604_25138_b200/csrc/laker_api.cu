@@ -375,11 +375,6 @@ laker_status laker_assemble_kernel(laker_ctx ctx, int64_t n, int32_t d, const do
       else
         laker::launch_assemble_exact_rows(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags,
                                           ctx->emax, s);
-    } else if (ctx->ozE_valid && std::getenv("LAKER_ASSEMBLE_TC") && std::getenv("LAKER_ASSEMBLE_TC")[0] == '1') {
-      // QK^T on tcgen05 with the fused exp epilogue (otf_tc.cu).  Opt-in: it computes
-      // every tile (no mirroring) and measured 3.8 ms at C3 vs 1.24 ms for the DMMA
-      // kernel, which computes the upper triangle and mirrors it
-      LAKER_CUDA(ctx, laker::launch_assemble_tc(ctx->ozE, ctx->r0, rows, n, scale, ctx->K, ctx->ld, s, ctx->cf));
     } else {
       laker::launch_assemble_fast(ctx->E, n, d, scale, ctx->r0, ctx->r1, ctx->K, ctx->ld, ctx->flags, s);
     }

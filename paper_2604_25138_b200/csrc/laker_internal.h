@@ -378,15 +378,13 @@ cudaError_t launch_otf_tc(const OzSlices &A, int64_t a0, int64_t m, const OzSlic
                           cudaStream_t s);
 void otf_tc_init();
 cudaError_t max_rownorm2(const double *E, int64_t n, int d, double *out, cudaStream_t s);
-cudaError_t launch_assemble_tc(const OzSlices &E, int64_t a0, int64_t m, int64_t n, double scale, double *K,
-                               int64_t ldk, cudaStream_t s, double2 *cf);
+
 // ------------------------------------------------------------- otf_tc2.cu (d <= 64, K = 64 slices)
 void otf_tc2_init();
 cudaError_t launch_otf_tc2_rect(const OzSlices &A, int64_t a0, int64_t m, const OzSlices &B, int64_t n, double scale,
                                 const double *w, double2 *cf, double lambda, const double *xdiag, double *out,
                                 const int32_t *done, cudaStream_t s);
-cudaError_t launch_assemble_tc2(const OzSlices &E, int64_t a0, int64_t m, int64_t n, double scale, double2 *cf,
-                                double *K, int64_t ldk, cudaStream_t s);
+
 
 // ---------------------------------------------------------- ozaki_skinny.cu
 // multi-RHS products C (M x N<=64) = alpha A op(B) + beta Cin with A pre-sliced (tcgen05)

@@ -67,8 +67,6 @@ __device__ __forceinline__ double pow2i(int k) {
 
 struct OtfArgs {
   int64_t a0, m, n;
-  double *K;    // MATERIALIZE: K[row][col] (local row, stride ldk) instead of row sums
-  int64_t ldk;
   int S;
   const int32_t *ea, *eb;
   double scale, lambda;
@@ -191,18 +189,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
       const int64_t cb = J * kON + qt * 32;
       const bool okl = cb + lane < f.n;
       const double pl = okl ? f.scale * pow2i(f.eb[cb + lane]) : 0.0;
-      if (MATERIALIZE) {
-        // K entries of this row segment: exp(scale 2^(e_i + e_j) acc) -- the same
-        // operations for (i, j) and (j, i), so K is bitwise symmetric
-        double *kr = f.K + row * f.ldk + cb;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double pj = __shfl_sync(0xffffffffu, pl, j);
-          const double kv = exp_fast(acc[j] * pe * pj);
-          if (rok && cb + j < f.n) kr[j] = kv;
-          acc[j] = 0.0;
-        }
-      } else {
+      {
         const double wl = okl ? f.w[cb + lane] : 0.0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -218,7 +205,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, 256);
-  if (!MATERIALIZE && threadIdx.x >= 64 && threadIdx.x < 64 + kOM) {
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + kOM) {
     const int rl = threadIdx.x - 64;
     const int64_t row = r0 + rl;
     if (row < f.m) {
@@ -233,7 +220,6 @@ __global__ void __launch_bounds__(kOThreads, 1)
 
 void otf_tc_init() {
   cudaFuncSetAttribute(otf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOSmem);
-  cudaFuncSetAttribute(otf_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOSmem);
 }
 
 cudaError_t oz_slices_make(OzSlices &o, const double *X, int64_t rows, int32_t d, int S, cudaStream_t s) {
@@ -312,27 +298,6 @@ cudaError_t max_rownorm2(const double *E, int64_t n, int d, double *out, cudaStr
 
 // FAST assembly: K rows [a0, a0 + m) (local row index) x all n columns, from the slices
 // of E (ctx->ozE), entries exp(scale <e_i, e_j>) on the tcgen05 QK^T path
-cudaError_t launch_assemble_tc(const OzSlices &E, int64_t a0, int64_t m, int64_t n, double scale, double *K,
-                               int64_t ldk, cudaStream_t s, double2 *cf) {
-  if (m <= 0) return cudaSuccess;
-  if (E.Kp == 64) return launch_assemble_tc2(E, a0, m, n, scale, cf, K, ldk, s);
-  CUtensorMap ta, tb;
-  const int64_t ld = (int64_t)E.S * E.Kp;
-  if (!make_tmap_s8(&ta, E.s, E.rows, ld, ld, kOM) || !make_tmap_s8(&tb, E.s, E.rows, ld, ld, kON))
-    return cudaErrorInvalidValue;
-  OtfArgs f{};
-  f.a0 = a0;
-  f.m = m;
-  f.n = n;
-  f.S = E.S;
-  f.ea = E.e;
-  f.eb = E.e;
-  f.scale = scale;
-  f.K = K;
-  f.ldk = ldk;
-  otf_tc_kernel<true><<<(unsigned)((m + kOM - 1) / kOM), kOThreads, kOSmem, s>>>(ta, tb, f);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_kernel_matvec_ctx(laker_ctx ctx, int mode, const double *Eq, int64_t m, bool Eq_is_E,
                                      int64_t eq_row0, const double *w, double lambda, const double *xdiag,

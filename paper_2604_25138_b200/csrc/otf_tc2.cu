@@ -45,7 +45,7 @@ constexpr size_t kQTabOff = kQCredOff + 2 * 4 * kQM * 16;   // exp table [16] do
 constexpr size_t kQBarOff = kQTabOff + 16 * 8;
 constexpr size_t kQSmem = 1024 + kQBarOff + 256;
 
-enum { kRectSum = 0, kRectMat = 1, kSym = 2 };
+enum { kRectSum = 0, kSym = 2 };
 
 struct Q2Args {
   SymvArgs t;           // kSym: partition and partial buffers
@@ -57,8 +57,6 @@ struct Q2Args {
   double lambda;
   const double *xdiag;
   double *out;          // kRectSum
-  double *K;            // kRectMat
-  int64_t ldk;
   const int32_t *done;
 };
 
@@ -314,16 +312,6 @@ __global__ void __launch_bounds__(kQThreads, 1)
       }
       // ---- entries exp(scale 2^(e_i + e_j) acc), row sums, column sums
       const int64_t cb = J * kQM + qt * 32;
-      if (KIND == kRectMat) {
-        double *kr = f.K + row * f.ldk + cb;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double2 cf = ld_cf(f.cf + cb + j);
-          const double kv = exp_tab(acc[j] * cf.x, tab);
-          if (rok && cb + j < f.n) kr[j] = kv;
-        }
-        continue;
-      }
       const bool cols = KIND == kSym && J != I;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -379,7 +367,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         cbuf ^= 1;
       }
     }
-    if (KIND != kRectMat) flush_rows(I);
+    flush_rows(I);
   }
   tc::fence_before();
   __syncthreads();
@@ -408,7 +396,6 @@ cudaError_t launch_q2(const OzSlices &A, const OzSlices &B, const Q2Args &f, uns
 
 void otf_tc2_init() {
   cudaFuncSetAttribute(otf_q2_kernel<kRectSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmem);
-  cudaFuncSetAttribute(otf_q2_kernel<kRectMat>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmem);
   cudaFuncSetAttribute(otf_q2_kernel<kSym>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmem);
 }
 
@@ -442,22 +429,6 @@ cudaError_t launch_otf_tc2_rect(const OzSlices &A, int64_t a0, int64_t m, const 
   return launch_q2<kRectSum>(A, B, f, (unsigned)((m + kQM - 1) / kQM), s);
 }
 
-// K rows [a0, a0 + m) (local row index) x n columns
-cudaError_t launch_assemble_tc2(const OzSlices &E, int64_t a0, int64_t m, int64_t n, double scale, double2 *cf,
-                                double *K, int64_t ldk, cudaStream_t s) {
-  if (m <= 0) return cudaSuccess;
-  launch_colfac(E, n, scale, nullptr, cf, s);
-  Q2Args f{};
-  f.a0 = a0;
-  f.m = m;
-  f.n = n;
-  f.S = E.S;
-  f.ea = E.e;
-  f.cf = cf;
-  f.K = K;
-  f.ldk = ldk;
-  return launch_q2<kRectMat>(E, E, f, (unsigned)((m + kQM - 1) / kQM), s);
-}
 
 // symmetric operator: tiles of the plan (BR = TC = 128) -> rowpart / colpart of ta
 cudaError_t launch_otf_tc2_sym(const OzSlices &E, int64_t n, double scale, const double *w, double2 *cf,

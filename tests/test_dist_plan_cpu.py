@@ -17,7 +17,7 @@ def L():
     return laker
 
 
-@pytest.mark.parametrize("n,W", [(1024, 1), (2048, 2), (3072, 3), (2048, 4), (4096, 8), (1536, 6)])
+@pytest.mark.parametrize("n,W", [(1024, 1), (2048, 2), (3072, 3), (2048, 4), (2560, 5), (4096, 8), (1536, 6), (7168, 7)])
 def test_plan_covers_each_entry_once_and_balances(L, n, W):
     nsb = n // TC                     # 64-wide sub-blocks: a tile is 2 x 1 of them
     count = np.zeros((nsb, nsb), dtype=np.int64)

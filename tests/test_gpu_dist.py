@@ -93,7 +93,7 @@ def test_row_sharded_assembly_and_predict_layouts(L, W):
     full.close()
 
 
-@pytest.mark.parametrize("W", [2, 3, 4])
+@pytest.mark.parametrize("W", [2, 3, 4, 5, 8])
 def test_sharded_symmetric_apply_detached_ranks(L, W):
     """The row-sharded symmetric K apply (symv.cu tri_plan_dist + pcg_dist.cu combine) run
     rank by rank on one GPU (detached shards, no communicator): each rank's tile partials
@@ -102,7 +102,7 @@ def test_sharded_symmetric_apply_detached_ranks(L, W):
     by the library's own combine kernel; the concatenated rows must equal the single-GPU
     symmetric apply -- and so the oracle's O2 rows -- bitwise, and every pair a rank
     would not send must be zero."""
-    n = 3072 if W == 3 else 4096
+    n = {3: 3072, 5: 2560}.get(W, 4096)
     P = make_problem(3, n=n)
     full = L.Context(0)
     full.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)

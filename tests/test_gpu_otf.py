@@ -42,23 +42,3 @@ def test_fast_on_the_fly_apply_and_predict(L, cid, n):
         assert reps[0]["termination"] == L.TERM_RESIDUAL_TOL
         assert np.linalg.norm(a - ref) / np.linalg.norm(ref) <= 1e-6
     c.close()
-
-
-def test_fast_assembly_tensor_core_path(L):
-    """LAKER_ASSEMBLE_TC=1: FAST K from the tcgen05 QK^T with the fused exp epilogue
-    (otf_tc.cu, S = 7 digit slices): entries within 1e-13 of the correctly rounded
-    ones and bitwise symmetric (so the symmetric apply is selected)."""
-    import os
-    P = make_problem(2)
-    os.environ["LAKER_ASSEMBLE_TC"] = "1"
-    try:
-        c = L.Context(0)
-        c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_FAST)
-        Kf = c.get_kernel_rows()
-        st = c.stats()
-        c.close()
-    finally:
-        del os.environ["LAKER_ASSEMBLE_TC"]
-    Ko, _ = O.assemble(P.E, P.scale)
-    assert np.abs(Kf / Ko - 1).max() <= 1e-13
-    assert (Kf == Kf.T).all() and st["symmetric_k"] == 1
