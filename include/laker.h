@@ -271,6 +271,8 @@ typedef struct {
                                        PCG applies stream only their block upper triangle (symv) */
   int32_t p_factored, n_dirs;    /* LEARNED P held as Q, M, a (LAKER_P_FACTORED): 1 applied in three
                                     passes Q (M (Q^T r)), 2 in the QM form (R21); its N_r */
+  int32_t k_tensor_core, pad0;   /* 1: the symmetric K apply runs exactly on the int8 tensor cores
+                                    (K held as 8 digit slices, csrc/symv_tc.cu); 0: fp64 kernel */
 } laker_stats;
 laker_status laker_get_stats(laker_ctx ctx, laker_stats *out);
 

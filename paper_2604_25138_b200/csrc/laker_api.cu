@@ -32,6 +32,7 @@ laker_status cuda_err(laker_ctx ctx, cudaError_t e, const char *what) {
 laker_status refresh_symmetry(laker_ctx ctx, int which, bool symmetric_rows) {
   bool &flag = which == 0 ? ctx->k_sym : ctx->p_sym;
   flag = false;
+  if (which == 0) ctx->k_tc = false;
   const double *A = which == 0 ? ctx->K : ctx->P;
   if (!A || ctx->storage != LAKER_STORE_MATERIALIZED) return LAKER_OK;
   const char *env = std::getenv("LAKER_SYMV");
@@ -65,6 +66,16 @@ laker_status refresh_symmetry(laker_ctx ctx, int which, bool symmetric_rows) {
       symv_rowmax(ctx->symv, which, A, ctx->stream);
       ctx->stats.kernel_launches++;
       LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  if (which == 0) {
+    // the exact int8 tensor-core form (symv_tc.cu) when every entry of K is exact in 8
+    // digit slices with one exponent; LAKER_SYMV_TC=0 keeps the fp64 kernel (A/B)
+    const char *tenv = std::getenv("LAKER_SYMV_TC");
+    if (flag && !(tenv && tenv[0] == '0')) {
+      ctx->k_tc = symv_tc_prepare(ctx->symv_tc, A, ctx->n, ctx->ld, symv_rowmax_ptr(ctx->symv, 0), ctx->stream);
+      ctx->stats.kernel_launches += 2;
+      cudaGetLastError();
     }
   }
   return LAKER_OK;
@@ -222,6 +233,7 @@ laker_status laker_create(laker_ctx *out, int device, int rank, int world, const
   c->gemv_grid = laker::gemv_max_grid(c->num_sms);
   laker::gemv_init();
   laker::symv_init();
+  laker::symv_tc_init();
   laker::otf_sym_init();
   laker::otf_tc2_init();
   laker::dgemm_init();
@@ -271,6 +283,7 @@ laker_status laker_destroy(laker_ctx ctx) {
   cudaFree(ctx->partials);
   cudaFree(ctx->flags);
   laker::symv_free(ctx->symv);
+  laker::symv_tc_free(ctx->symv_tc);
   laker::symv_free(ctx->otf_sym);
   if (ctx->cf) cudaFree(ctx->cf);
   if (ctx->emax) cudaFree(ctx->emax);
@@ -658,6 +671,7 @@ laker_status laker_get_stats(laker_ctx ctx, laker_stats *out) {
   ctx->stats.storage = ctx->storage;
   ctx->stats.mode = ctx->mode;
   ctx->stats.symmetric_k = ctx->k_sym ? 1 : 0;
+  ctx->stats.k_tensor_core = ctx->k_sym && ctx->k_tc ? 1 : 0;
   ctx->stats.symmetric_p = ctx->p_sym ? 1 : 0;
   ctx->stats.p_factored = ctx->p_factored ? (ctx->p_qm ? 2 : 1) : 0;
   ctx->stats.n_dirs = (int32_t)ctx->f_nr;

@@ -91,6 +91,7 @@ struct Buf {
 };
 
 struct SymvPlan;  // symv.cu
+struct SymvTc;    // symv_tc.cu: K as int8 digit slices for the exact tensor-core apply
 
 // digit slices of a row-major fp64 matrix for the Ozaki products (otf_tc.cu)
 struct OzSlices {
@@ -132,6 +133,9 @@ struct laker_ctx_s {
   // symmetric (upper-triangle) GEMV, single rank: used for K / P only after a
   // device check found them bitwise symmetric (symv.cu)
   laker::SymvPlan *symv = nullptr;
+  // the exact tensor-core form of the symmetric K apply (one rank, K's slices exact)
+  laker::SymvTc *symv_tc = nullptr;
+  bool k_tc = false;
   // tile partition of the symmetric on-the-fly operator (otf_sym.cu), built at assembly
   laker::SymvPlan *otf_sym = nullptr;
   // per-column factors {scale 2^(e_j), w_j} of the FAST tcgen05 on-the-fly kernels (otf_tc2.cu)
@@ -216,6 +220,8 @@ struct GemvArgs {
   dd_pair *ypair;
   // symv on one rank inside the PCG (epi = kEpiDelta): the update step fused in
   FusedUpdate upd;
+  // symv (which = 0): the exact int8 tensor-core tile pass instead of the fp64 one
+  SymvTc *tc;
   // gemv with epi = kEpiBeta (the preconditioner's last pass, one rank): the direction
   // update p = fma(beta, p, theta) of pcg_pupdate_kernel fused in after a grid barrier
   // (persistent grid, one CTA per SM); the per-CTA max |p| go to pu_pmax[blockIdx]; with
@@ -245,6 +251,12 @@ void symv_rowmax(SymvPlan *p, int which, const double *A, cudaStream_t s);
 void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s);
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s);
 void symv_init();
+// ------------------------------------------------------------- symv_tc.cu
+void symv_tc_init();
+void symv_tc_free(SymvTc *&p);
+// slice K (n x n, stride ld, bitwise symmetric) into 8 int8 digit slices with one global
+// exponent; false if not every entry is exact in that form
+bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const double *rowmax, cudaStream_t s);
 // ------------------------------------------------------------- otf_sym.cu
 void otf_sym_init();
 cudaError_t otf_sym_prepare(laker_ctx ctx);

@@ -82,6 +82,7 @@ static void launch_operator(laker_ctx ctx, const double *p, double *q, PcgState 
       a.xparts = pmax;
       a.nxparts = npmax;
       if (upd) a.upd = *upd;
+      a.tc = ctx->k_tc ? ctx->symv_tc : nullptr;
       launch_symv(ctx->symv, 0, a, ctx->stream);
       ctx->stats.kernel_launches++;
     } else {

@@ -81,7 +81,8 @@ class Stats(ctypes.Structure):
                 ("solve_ms", ctypes.c_double), ("predict_ms", ctypes.c_double),
                 ("kernel_launches", ctypes.c_int64),
                 ("symmetric_k", ctypes.c_int32), ("symmetric_p", ctypes.c_int32),
-                ("p_factored", ctypes.c_int32), ("n_dirs", ctypes.c_int32)]
+                ("p_factored", ctypes.c_int32), ("n_dirs", ctypes.c_int32),
+                ("k_tensor_core", ctypes.c_int32), ("pad0", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:

@@ -139,3 +139,77 @@ def test_symv_c3_full_size_pcg_matches_full_gemv(ctx, L):
     assert r1[0]["iters"] == r2[0]["iters"]
     _bitwise(h1, h2, "C3 history")
     _bitwise(a1, a2, "C3 alpha")
+
+
+def _with_env(name, value, fn):
+    old = os.environ.get(name)
+    os.environ[name] = value
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[name]
+        else:
+            os.environ[name] = old
+
+
+# The exact int8 tensor-core form of the same apply (csrc/symv_tc.cu): K's entries are
+# exact in 8 seven-bit digit slices with one exponent, so every tile product is an exact
+# integer sum and each row is again the unrounded pair the finalize rounds once.  Bars:
+# it is selected for the configs' K, and every row is bitwise the oracle's and the fp64
+# symmetric kernel's (LAKER_SYMV_TC=0).
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, None), (3, 1), (3, 65), (3, 129), (3, 1000), (3, 2048),
+                                   (3, 4133), (4, 3000), (5, 2500)])
+def test_symv_tensor_core_bitwise(ctx, L, cfg, n):
+    P = make_problem(cfg, n=n) if n else make_problem(cfg)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    st = ctx.stats()
+    assert st["symmetric_k"] == 1 and st["k_tensor_core"] == 1
+    Ko, _ = O.assemble(P.E, P.scale)
+    xs = _vectors(P.n, 300 + P.n) + [np.zeros(P.n)]
+    ys = [ctx.apply_operator(x) for x in xs]
+    for x, y in zip(xs, ys):
+        _bitwise(y, O.apply(Ko, P.lam, x), f"tensor-core symv vs oracle cfg={cfg} n={P.n}")
+
+    def fp64():
+        ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+        assert ctx.stats()["k_tensor_core"] == 0
+        return [ctx.apply_operator(x) for x in xs]
+    for y, yf in zip(ys, _with_env("LAKER_SYMV_TC", "0", fp64)):
+        _bitwise(y, yf, f"tensor-core vs fp64 symv n={P.n}")
+
+
+def test_symv_tensor_core_not_used_when_inexact(ctx, L):
+    """A K entry off the 8-slice grid (one entry scaled by 2^-3: below max/8 its last
+    mantissa bits fall under 2^(eK-55)) keeps the fp64 kernel."""
+    n = 600
+    P = make_problem(1, n=n)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    K, _ = O.assemble(P.E, P.scale)
+    A = K.copy()
+    A[5, 400] = A[400, 5] = np.nextafter(A[5, 400] / 8.0, 0.0)
+    ctx.load_kernel_rows(A)
+    st = ctx.stats()
+    assert st["symmetric_k"] == 1 and st["k_tensor_core"] == 0
+    x = _vectors(n, 8)[0]
+    _bitwise(ctx.apply_operator(x), O.apply(A, P.lam, x), "inexact K -> fp64 symv")
+
+
+def test_symv_tensor_core_c3_pcg_matches_fp64(ctx, L):
+    """C3 (n = 16384), the default learned solve: the tensor-core apply and the fp64
+    symmetric apply give the same history and alpha bitwise."""
+    P = make_problem(3)
+    Z = np.asfortranarray(make_directions(3, P.n, P.n_dirs))
+
+    def run():
+        ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+        tc = ctx.stats()["k_tensor_core"]
+        ctx.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z)
+        a, r, h = ctx.pcg_solve(P.y, P.tol, want_history=True)
+        return tc, a, r, h
+    tc1, a1, r1, h1 = run()
+    tc0, a0, r0, h0 = _with_env("LAKER_SYMV_TC", "0", run)
+    assert tc1 == 1 and tc0 == 0
+    assert r1[0]["iters"] == r0[0]["iters"]
+    _bitwise(h1, h0, "C3 history")
+    _bitwise(a1, a0, "C3 alpha")
