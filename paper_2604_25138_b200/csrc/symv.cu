@@ -943,7 +943,7 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   a.ypair = g.ypair;
   a.upd = g.upd;
   if (g.tc != nullptr && which == 0 && !p->dist)
-    launch_symv_tc(g.tc, a, a.xparts, a.nxparts, p->grid, s);
+    launch_symv_tc(g.tc, a, s);
   else if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else

@@ -1,34 +1,39 @@
-// Exact symmetric K apply on the int8 tensor cores (round 2): the same block-upper-
-// triangle tiles, partials and finalize as symv.cu (K.p for the PCG, Alg. 1 l.16,
+// Exact symmetric K apply on the int8 tensor cores (round 2): the block upper triangle of K
+// streamed once, the partials and finalize of symv.cu (K.p for the PCG, Alg. 1 l.16,
 // P:306-321; rows a4/a9), with every product computed exactly in integers.
 //
 // K is stored as 8 signed 7-bit digit slices per entry with one global exponent,
 //   K_ij = 2^(eK+1) sum_{s<8} d_ijs 2^(-7(s+1)),   d in [-64, 64],
-// exact when every entry's mantissa falls on that 2^(eK-55) grid (the assembly checks
-// it; K = exp(scale <e_i, e_j>) of the configs lies in [0.5, 4)), and x (the CG
+// exact when every entry's mantissa falls on that 2^(eK-55) grid (symv_tc_prepare checks
+// it; K = exp(scale <e_i, e_j>) of the configs lies in [0.8, 2.9]), and x (the CG
 // direction) as 16 slices with its own exponent, x_j = 2^(F+1) sum_{t<16} c_jt
-// 2^(-7(t+1)) + (a remainder below 2^(F-111), ~2^-112 max|x|: under Dot2's own error).
+// 2^(-7(t+1)) + (a remainder below 2^(F-112), ~2^-112 max|x|: under Dot2's own error).
 // A row sum is then sum_{s,t} 2^(eK+F+2-7(s+t+2)) D_st with D_st = sum_j d_ijs c_jt an
-// exact int32 (|D| <= 2^12 n < 2^31 for n <= 2^18): tcgen05 kind::i8 accumulates it in TMEM per
-// slice pair, the level sums D_L = sum_{s+t=L} D_st are exact int64, and a TwoSum chain
-// over the 23 levels gives the row's unrounded (s, c) pair -- the same contract as the
-// fp64 kernel's compensated pairs (the finalize rounds once; correctly rounded in
-// practice, so bitwise the oracle's O2 rows).  The fp64 work per matrix element drops
-// from 14 operations (two offset-Fast2Sum products) to none: the apply streams K's
-// slices (8 bytes per entry, as fp64) at the tile-stream rate.
+// exact int32 (|D| <= 2^12 n < 2^31 for n <= 2^18): tcgen05 kind::i8 accumulates it in
+// TMEM per slice pair, the level sums are folded exactly in int64 and a short TwoSum chain
+// gives the row's unrounded (s, c) pair -- the same contract as the fp64 kernel's
+// compensated pairs (the finalize rounds once; correctly rounded in practice, so bitwise
+// the oracle's O2 rows).  The fp64 work per matrix element drops from 14 operations (two
+// offset-Fast2Sum products) to none: the apply streams K's slices (8 bytes per entry,
+// as fp64) at the tile-stream rate.
 //
-// Per 128 x 64 tile (I, jt), one row-major SWIZZLE_64B shared-memory copy of the 8
-// slices feeds both products (tools/mma_mn_major_test.cu):
-//   rows    D_row[s] (M = 128, N = 16) += K_s (K-major: contraction over the 64 columns)
-//           x x_J slices; accumulated over the whole block-row segment in TMEM;
-//   columns D_col[s] (M = 64, N = 16)   = K_s^T (MN-major A, "transpose A": contraction
-//           over the 128 rows) x x_I slices; read out per tile (off the diagonal block).
-// TMEM (512 columns): D_row double-buffered [0, 256), D_col double-buffered [256, 512).
+// Tiles are 128 x 128 (block-row I takes the column blocks J = I .. nb - 1; persistent
+// CTAs take contiguous tile ranges).  A slice of a tile (16 KiB: two SWIZZLE_64B halves
+// of 64 columns) is the unit of the shared-memory ring; it feeds both products
+// (tools/mma_mn128_test.cu):
+//   rows    D_row[s] (M = 128, N = 16) += K_s (K-major, contraction over the 128 columns)
+//           x x_J slices, accumulated over the block-row segment in TMEM;
+//   columns D_col[s] (M = 128, N = 16)  = K_s^T (MN-major A spanning both halves: LBO =
+//           8 KiB, "transpose A"; contraction over the 128 rows) x x_I slices, read out per
+//           tile (off the diagonal block).
+// At ~45 cycles per tcgen05.mma (tools/mma_rate.cu) the 64 MMAs of a tile take ~60% of
+// its HBM time.  TMEM (512 columns): D_row double-buffered [0, 256), D_col [256, 512).
 // Warps: 0 TMA producer, 1 MMA issuer, 2..5 epilogue (TMEM lane quadrants 2, 3, 0, 1).
 #include <cuda.h>
 
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "laker_internal.h"
 #include "tc_int8.cuh"
@@ -37,28 +42,29 @@
 namespace laker {
 namespace {
 
-constexpr int kTR = 128, kTC = 64;                 // tile rows / columns (symv.cu's plan)
+constexpr int kT = 128;                             // tile rows = columns
 constexpr int kSK = 8;                              // slices of K
 constexpr int kSX = 16;                             // slices of x (MMA N)
-constexpr int kStg = 3;                             // ring stages
-constexpr uint32_t kSliceBytes = kTR * kTC;         // 8 KiB
-constexpr uint32_t kKBytes = kSK * kSliceBytes;     // 64 KiB
-constexpr uint32_t kXJBytes = kSX * kTC;            // 1 KiB
-constexpr uint32_t kXIBytes = kSX * kTR;            // 2 KiB
+constexpr int kRing = 12;                           // slice slots in the ring
+constexpr int kXJSlots = 3;                         // x_J tiles in flight
+constexpr uint32_t kHalfBytes = kT * 64;            // 8 KiB: 128 rows x 64 columns
+constexpr uint32_t kSliceBytes = 2 * kHalfBytes;    // 16 KiB
+constexpr uint32_t kXBytes = kSX * kT;              // 2 KiB: 16 slices x 128
 constexpr int kTcThreads = 6 * 32;
 constexpr int kLevels = kSK + kSX - 1;              // 23
-// shared layout (1024-aligned base): [kStg][K 64 KiB] [kStg][xJ 1 KiB] [2][xI 2 KiB] barriers
-constexpr size_t kOffXJ = (size_t)kStg * kKBytes;
-constexpr size_t kOffXI = kOffXJ + (size_t)kStg * kXJBytes;
-constexpr size_t kOffBar = kOffXI + 2 * kXIBytes;
-constexpr size_t kTcSmem = 1024 + kOffBar + 256;
+// shared layout (1024-aligned base): [kRing][slice 16 KiB] [kXJSlots][x_J] [2][x_I] barriers
+constexpr size_t kOffXJ = (size_t)kRing * kSliceBytes;
+constexpr size_t kOffXI = kOffXJ + (size_t)kXJSlots * kXBytes;
+constexpr size_t kOffBar = kOffXI + 2 * kXBytes;
+constexpr size_t kTcSmem = 1024 + kOffBar + 512;
 
 // descriptor of a K slice as the MN-major A operand of the column product (SWIZZLE_64B,
-// 8-row atoms of 64 B, SBO 512 B between atoms along the contraction)
+// 8-row atoms of 64 B: SBO 512 B between atoms along the contraction, LBO 8 KiB between
+// the two 64-column halves along M)
 __device__ __forceinline__ uint64_t sdesc_mn_sw64(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(kHalfBytes >> 4) << 16;
   d |= (uint64_t)(512 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)4 << 61;
@@ -74,15 +80,43 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, in
       : "memory");
 }
 
-// 2^e for a compile-time e (exact; folded once the level loop is unrolled)
+// Single-thread tcgen05 operations issued from converged warp code: one lane is elected
+// inside the asm block, so the surrounding loop stays warp-uniform and its operands live
+// in uniform registers (no per-MMA ELECT / R2UR.BROADCAST loop: tools/mma_issue.cu
+// measured 39 instead of 50 cycles per MMA in isolation, and far less under load)
+__device__ __forceinline__ void mma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void commit_elect(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// 2^e for a compile-time e (exact; folded once the loops are unrolled)
 __device__ __forceinline__ double pow2c(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
-// the exact level sums of one output (s slices x 16 t values read from TMEM columns
-// base + 16 s), folded to an unrounded pair scaled by 2^escale
+constexpr int kGroups = (kLevels + 2) / 3;  // 8 groups of 3 levels
+
+// One output's exact sum from its 8 x 16 slice-pair accumulators (TMEM columns base + 16 s,
+// t = 0..15), as an unrounded pair scaled by 2^escale.  Level L = s + t carries 2^(-7L);
+// three consecutive levels fold exactly into one int64 G_g = sum_{L in g} D_L 2^(7(3g+2-L))
+// (|G_g| < 2^31 * 8 * (2^14 + 2^7 + 1) < 2^48: exact in fp64), and a TwoSum chain over the
+// 8 group values G_g 2^(-7(3g+2)) gives the pair.
 __device__ __forceinline__ dd_pair combine_levels(uint32_t taddr, int escale) {
-  long long lv[kLevels];
+  long long G[kGroups];
 #pragma unroll
-  for (int L = 0; L < kLevels; ++L) lv[L] = 0;
+  for (int g = 0; g < kGroups; ++g) G[g] = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {  // two batches of 4 slices: 64 registers in flight
     uint32_t v[4][16];
@@ -92,13 +126,15 @@ __device__ __forceinline__ dd_pair combine_levels(uint32_t taddr, int escale) {
 #pragma unroll
     for (int s = 0; s < 4; ++s)
 #pragma unroll
-      for (int t = 0; t < kSX; ++t) lv[4 * h + s + t] += (long long)(int32_t)v[s][t];
+      for (int t = 0; t < kSX; ++t) {
+        const int L = 4 * h + s + t;
+        G[L / 3] += (long long)(int32_t)v[s][t] << (7 * (2 - L % 3));
+      }
   }
-  // sum_L lv_L 2^(-7L), each term exact in fp64 (|lv| < 2^34), TwoSum chain from L = 0
-  dd_pair r = {(double)lv[0], 0.0};
+  dd_pair r = {__dmul_rn((double)G[0], pow2c(-14)), 0.0};
 #pragma unroll
-  for (int L = 1; L < kLevels; ++L) {
-    const double t = __dmul_rn((double)lv[L], pow2c(-7 * L));
+  for (int g = 1; g < kGroups; ++g) {
+    const double t = __dmul_rn((double)G[g], pow2c(-7 * (3 * g + 2)));
     double s, e;
     two_sum(r.s, t, s, e);
     r.s = s;
@@ -110,14 +146,20 @@ __device__ __forceinline__ dd_pair combine_levels(uint32_t taddr, int escale) {
 }
 
 struct TcArgs {
-  SymvArgs t;
+  SymvArgs t;       // partials, x, plan of the finalize
+  const int64_t *toff;  // [nb + 1] first 128 x 128 tile of each block-row
+  int64_t T;            // tiles
+  int32_t nb;
+  const int32_t *segfirst;  // [nb] first CTA covering block-row I
+  int32_t maxseg;
+  dd_pair *rowpart;         // [nb][maxseg][128]
   const int *eK;  // global exponent of K's slices (device)
   const int *F;   // exponent of this x's slices (device, written by the slicing kernel)
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1)
-    symv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmXJ,
-                   const __grid_constant__ CUtensorMap tmXI, const TcArgs ta) {
+    symv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmX,
+                   const TcArgs ta) {
   const SymvArgs &a = ta.t;
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   extern __shared__ unsigned char smem_raw[];
@@ -126,9 +168,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   unsigned char *sK = smem;
   unsigned char *sXJ = smem + kOffXJ;
   unsigned char *sXI = smem + kOffXI;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kOffBar);  // [kStg]
-  uint64_t *empty = full + kStg;                                  // [kStg]
-  uint64_t *xif = empty + kStg;                                   // [2]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kOffBar);  // [kRing]
+  uint64_t *empty = full + kRing;                                 // [kRing]
+  uint64_t *xjf = empty + kRing;                                  // [kXJSlots]
+  uint64_t *xje = xjf + kXJSlots;                                 // [kXJSlots]
+  uint64_t *xif = xje + kXJSlots;                                 // [2]
   uint64_t *xie = xif + 2;                                        // [2]
   uint64_t *rowf = xie + 2;                                       // [2]
   uint64_t *rowe = rowf + 2;                                      // [2]
@@ -136,12 +180,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t *cole = colf + 2;                                      // [2]
   uint32_t *holder = reinterpret_cast<uint32_t *>(cole + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t0 = a.T * blockIdx.x / gridDim.x, t1 = a.T * (blockIdx.x + 1) / gridDim.x;
+  const int64_t t0 = ta.T * blockIdx.x / gridDim.x, t1 = ta.T * (blockIdx.x + 1) / gridDim.x;
   if (t0 >= t1) return;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStg; ++s) {
+    for (int s = 0; s < kRing; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kXJSlots; ++s) {
+      mbar_init(&xjf[s], 1);
+      mbar_init(&xje[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&xif[b], 1);
@@ -158,35 +206,47 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *holder;
-  const int I0 = find_block_row(a.toff, a.nb, t0);
+  const int I0 = find_block_row(ta.toff, ta.nb, t0);
 
   if (warp == 0) {
     // ---------------------------------------------------------- TMA producer
     if (lane == 0) {
       int I = I0;
-      int64_t rend = a.toff[I + 1];
-      int slot = 0, xb = 0, nseg = 0;
-      uint32_t ph = 0;
-      bool first = true;
+      int64_t rend = ta.toff[I + 1];
+      int xb = 0, nseg = 0, slot = 0, tb = 0;
+      uint32_t ph = 0, tph = 0;
+      bool ring_full = false, xj_full = false;  // past the first pass over the slots
       for (int64_t t = t0; t < t1; ++t) {
         const bool newI = (t == t0) || (t >= rend);
-        while (t >= rend) rend = a.toff[++I + 1];
-        const int jt = 2 * I + (int)(t - a.toff[I]);
+        while (t >= rend) rend = ta.toff[++I + 1];
+        const int J = I + (int)(t - ta.toff[I]);
         if (newI) {
           if (nseg >= 2) mbar_wait(&xie[xb], (uint32_t)(((nseg - 2) >> 1) & 1));
-          mbar_arrive_expect_tx(&xif[xb], kXIBytes);
-          tc::tma_load_2d(sXI + xb * kXIBytes, &tmXI, I * kTR, 0, &xif[xb]);
+          mbar_arrive_expect_tx(&xif[xb], kXBytes);
+          tc::tma_load_2d(sXI + xb * kXBytes, &tmX, I * kT, 0, &xif[xb]);
           xb ^= 1;
           ++nseg;
         }
-        if (!first) mbar_wait(&empty[slot], ph ^ 1u);
-        mbar_arrive_expect_tx(&full[slot], kKBytes + kXJBytes);
-        tma_load_3d(sK + slot * kKBytes, &tmK, jt * kTC, I * kTR, 0, &full[slot]);
-        tc::tma_load_2d(sXJ + slot * kXJBytes, &tmXJ, jt * kTC, 0, &full[slot]);
-        if (++slot == kStg) {
-          slot = 0;
-          ph ^= 1u;
-          first = false;
+        if (xj_full) mbar_wait(&xje[tb], tph ^ 1u);
+        mbar_arrive_expect_tx(&xjf[tb], kXBytes);
+        tc::tma_load_2d(sXJ + tb * kXBytes, &tmX, J * kT, 0, &xjf[tb]);
+        if (++tb == kXJSlots) {
+          tb = 0;
+          tph ^= 1u;
+          xj_full = true;
+        }
+#pragma unroll 1
+        for (int s = 0; s < kSK; ++s) {
+          if (ring_full) mbar_wait(&empty[slot], ph ^ 1u);
+          unsigned char *dst = sK + (size_t)slot * kSliceBytes;
+          mbar_arrive_expect_tx(&full[slot], kSliceBytes);
+          tma_load_3d(dst, &tmK, J * kT, I * kT, s, &full[slot]);
+          tma_load_3d(dst + kHalfBytes, &tmK, J * kT + 64, I * kT, s, &full[slot]);
+          if (++slot == kRing) {
+            slot = 0;
+            ph ^= 1u;
+            ring_full = true;
+          }
         }
       }
     }
@@ -194,62 +254,76 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 
   if (warp == 1) {
-    // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idr = tc::idesc_i8(kTR, kSX);
-      constexpr uint32_t idc = tc::idesc_i8(kTC, kSX) | (1u << 15);  // A = K_s^T (MN-major)
-      int I = I0;
-      int64_t rend = a.toff[I + 1];
-      int slot = 0, xb = 0, rb = 0, cb = 0, nseg = 0, ncol = 0;
-      uint32_t ph = 0;
-      bool acc = false;
-      for (int64_t t = t0; t < t1; ++t) {
-        const bool newI = (t == t0) || (t >= rend);
-        while (t >= rend) rend = a.toff[++I + 1];
-        const int jt = 2 * I + (int)(t - a.toff[I]);
-        if (newI) {
-          if (nseg >= 2) mbar_wait(&rowe[rb], (uint32_t)(((nseg - 2) >> 1) & 1));  // row buffer drained
-          mbar_wait(&xif[xb], (uint32_t)((nseg >> 1) & 1));
-          ++nseg;
-          acc = false;
-        }
+    // ---------------------------------------------------------- MMA issuer (whole warp,
+    // one lane elected per MMA / commit)
+    constexpr uint32_t idr = tc::idesc_i8(kT, kSX);
+    constexpr uint32_t idc = tc::idesc_i8(kT, kSX) | (1u << 15);  // A = K_s^T (MN-major)
+    const uint64_t dK0 = tc::sdesc_k_sw64(smem_u32(sK));
+    const uint64_t dKt0 = sdesc_mn_sw64(smem_u32(sK));
+    const uint64_t dXJ0 = tc::sdesc_k_sw128(smem_u32(sXJ));
+    const uint64_t dXI0 = tc::sdesc_k_sw128(smem_u32(sXI));
+    int I = I0;
+    int64_t rend = ta.toff[I + 1];
+    int xb = 0, rb = 0, cb = 0, nseg = 0, ncol = 0;
+    int slot = 0, tb = 0;
+    uint32_t ph = 0, tph = 0;
+    bool acc = false;
+    for (int64_t t = t0; t < t1; ++t) {
+      const bool newI = (t == t0) || (t >= rend);
+      while (t >= rend) rend = ta.toff[++I + 1];
+      const int J = I + (int)(t - ta.toff[I]);
+      if (newI) {
+        if (nseg >= 2) mbar_wait(&rowe[rb], (uint32_t)(((nseg - 2) >> 1) & 1));  // row buffer drained
+        mbar_wait(&xif[xb], (uint32_t)((nseg >> 1) & 1));
+        ++nseg;
+        acc = false;
+      }
+      mbar_wait(&xjf[tb], tph);
+      const bool off = J != I;  // off the diagonal block: the column product too
+      if (off && ncol >= 2) mbar_wait(&cole[cb], (uint32_t)(((ncol - 2) >> 1) & 1));
+      tc::fence_after();
+      const uint32_t trow = tmem + (uint32_t)(rb * 128), tcol = tmem + 256 + (uint32_t)(cb * 128);
+      // descriptors: the start-address field is addr >> 4 in the low 14 bits, so an
+      // offset inside shared memory is added to the base descriptor (no carry: < 256 KiB)
+      const uint64_t dXJ = dXJ0 + (uint64_t)((tb * kXBytes) >> 4);
+      const uint64_t dXI = dXI0 + (uint64_t)((xb * kXBytes) >> 4);
+#pragma unroll 1
+      for (int s = 0; s < kSK; ++s) {
         mbar_wait(&full[slot], ph);
         tc::fence_after();
-        const uint32_t kb = smem_u32(sK + slot * kKBytes), xj = smem_u32(sXJ + slot * kXJBytes);
-        const uint32_t trow = tmem + (uint32_t)(rb * 128);
+        const uint64_t so = (uint64_t)((slot * kSliceBytes) >> 4);
 #pragma unroll
-        for (int s = 0; s < kSK; ++s)
+        for (int kk = 0; kk < 4; ++kk)  // columns 32 kk ..: half kk / 2, +32 B inside it
+          mma_i8_elect(trow + 16 * s, dK0 + so + (uint64_t)(((kk >> 1) * kHalfBytes + (kk & 1) * 32) >> 4),
+                       dXJ + (uint64_t)((kk * 32) >> 4), idr, (acc || kk > 0) ? 1u : 0u);
+        if (off) {
 #pragma unroll
-          for (int kk = 0; kk < kTC / 32; ++kk)
-            tc::mma_i8(trow + 16 * s, tc::sdesc_k_sw64(kb + s * kSliceBytes + kk * 32), tc::sdesc_k_sw64(xj + kk * 32),
-                       idr, (acc || kk > 0) ? 1u : 0u);
-        acc = true;
-        if (jt / 2 != I + a.I0) {  // off the diagonal block: the column product of this tile
-          if (ncol >= 2) mbar_wait(&cole[cb], (uint32_t)(((ncol - 2) >> 1) & 1));
-          tc::fence_after();
-          const uint32_t tcol = tmem + 256 + (uint32_t)(cb * 128);
-          const uint32_t xi = smem_u32(sXI + xb * kXIBytes);
-#pragma unroll
-          for (int s = 0; s < kSK; ++s)
-#pragma unroll
-            for (int kk = 0; kk < kTR / 32; ++kk)
-              tc::mma_i8(tcol + 16 * s, sdesc_mn_sw64(kb + s * kSliceBytes + kk * 2048), tc::sdesc_k_sw128(xi + kk * 32),
+          for (int kk = 0; kk < 4; ++kk)  // rows 32 kk ..: 2 KiB into each half
+            mma_i8_elect(tcol + 16 * s, dKt0 + so + (uint64_t)((kk * 2048) >> 4), dXI + (uint64_t)((kk * 32) >> 4),
                          idc, kk > 0 ? 1u : 0u);
-          tc::mma_commit(&colf[cb]);
-          cb ^= 1;
-          ++ncol;
         }
-        tc::mma_commit(&empty[slot]);
-        if (++slot == kStg) {
+        commit_elect(&empty[slot]);
+        if (++slot == kRing) {
           slot = 0;
           ph ^= 1u;
         }
-        if (t + 1 == t1 || t + 1 >= rend) {  // segment complete: rows to the epilogue, x_I slot free
-          tc::mma_commit(&rowf[rb]);
-          tc::mma_commit(&xie[xb]);
-          rb ^= 1;
-          xb ^= 1;
-        }
+      }
+      acc = true;
+      commit_elect(&xje[tb]);
+      if (++tb == kXJSlots) {
+        tb = 0;
+        tph ^= 1u;
+      }
+      if (off) {
+        commit_elect(&colf[cb]);
+        cb ^= 1;
+        ++ncol;
+      }
+      if (t + 1 == t1 || t + 1 >= rend) {  // segment complete: rows to the epilogue, x_I slot free
+        commit_elect(&rowf[rb]);
+        commit_elect(&xie[xb]);
+        rb ^= 1;
+        xb ^= 1;
       }
     }
     __syncwarp();
@@ -264,36 +338,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int q = warp & 3;  // TMEM lane quadrant this warp may access
   const int escale = *ta.eK + *ta.F + 2 - 14;
   int I = I0;
-  int64_t rend = a.toff[I + 1];
+  int64_t rend = ta.toff[I + 1];
   int rb = 0, cb = 0, nseg = 0, ncol = 0;
   for (int64_t t = t0; t < t1; ++t) {
     const bool newI = (t == t0) || (t >= rend);
-    while (t >= rend) rend = a.toff[++I + 1];
+    while (t >= rend) rend = ta.toff[++I + 1];
     if (newI) ++nseg;
-    const int jt = 2 * I + (int)(t - a.toff[I]);
-    if (jt / 2 != I + a.I0) {
+    const int J = I + (int)(t - ta.toff[I]);
+    if (J != I) {
       mbar_wait(&colf[cb], (uint32_t)((ncol >> 1) & 1));
       tc::fence_after();
-      // M = 64 accumulator: columns 16 q .. 16 q + 15 in lanes 32 q .. 32 q + 15
-      const uint32_t taddr = tmem + 256 + (uint32_t)(cb * 128) + ((uint32_t)(32 * q) << 16);
-      const dd_pair v = combine_levels(taddr, escale);
-      if (lane < 16) a.colpart[(int64_t)I * a.ldcp + (int64_t)jt * kTC + 16 * q + lane] = v;
+      const dd_pair v = combine_levels(tmem + 256 + (uint32_t)(cb * 128) + ((uint32_t)(32 * q) << 16), escale);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&cole[cb]);
+      const int64_t j = (int64_t)J * kT + 32 * q + lane;
+      if (j < a.n) a.colpart[(int64_t)I * a.ldcp + j] = v;
       cb ^= 1;
       ++ncol;
     }
     if (t + 1 == t1 || t + 1 >= rend) {
       mbar_wait(&rowf[rb], (uint32_t)(((nseg - 1) >> 1) & 1));
       tc::fence_after();
-      const uint32_t taddr = tmem + (uint32_t)(rb * 128) + ((uint32_t)(32 * q) << 16);
-      const dd_pair v = combine_levels(taddr, escale);
-      const int sg = (int)blockIdx.x - a.segfirst[I];
-      a.rowpart[((int64_t)I * a.maxseg + sg) * kTR + 32 * q + lane] = v;
+      const dd_pair v = combine_levels(tmem + (uint32_t)(rb * 128) + ((uint32_t)(32 * q) << 16), escale);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&rowe[rb]);
+      const int sg = (int)blockIdx.x - ta.segfirst[I];
+      ta.rowpart[((int64_t)I * ta.maxseg + sg) * kT + 32 * q + lane] = v;
       rb ^= 1;
     }
   }
@@ -398,7 +470,13 @@ struct SymvTc {
   int8_t *ks = nullptr, *xs = nullptr;
   int *dexp = nullptr;  // [0] eK, [1] F of the last sliced x, [2] exactness flag
   double *dmax = nullptr;
-  CUtensorMap tmK, tmXJ, tmXI;
+  CUtensorMap tmK, tmX;
+  // the 128 x 128 tile plan for `grid` persistent CTAs (the finalize's segments)
+  int grid = 0, nb = 0, maxseg = 0;
+  int64_t T = 0;
+  int64_t *toff = nullptr;
+  int32_t *segfirst = nullptr, *nseg = nullptr;
+  dd_pair *rowpart = nullptr;
 };
 
 void symv_tc_free(SymvTc *&p) {
@@ -407,6 +485,10 @@ void symv_tc_free(SymvTc *&p) {
   cudaFree(p->xs);
   cudaFree(p->dexp);
   cudaFree(p->dmax);
+  cudaFree(p->toff);
+  cudaFree(p->segfirst);
+  cudaFree(p->nseg);
+  cudaFree(p->rowpart);
   delete p;
   p = nullptr;
 }
@@ -415,39 +497,80 @@ void symv_tc_init() {
   cudaFuncSetAttribute(symv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
 }
 
+namespace {
+// block-row I takes tiles J = I .. nb - 1 (row-major order); CTA b the range
+// [T b / G, T (b + 1) / G), G = min(SMs, T); the segments of a block-row are its CTAs in order
+cudaError_t tc_plan(SymvTc *p, int sms) {
+  const int nb = (int)((p->n + kT - 1) / kT);
+  std::vector<int64_t> toff(nb + 1, 0);
+  for (int I = 0; I < nb; ++I) toff[I + 1] = toff[I] + (nb - I);
+  const int64_t T = toff[nb];
+  // every CTA gets at least one tile: the segments of a block-row are then consecutive CTAs
+  const int grid = (int)std::min<int64_t>(sms, T);
+  auto cta_of = [&](int64_t t) {  // the CTA whose range holds tile t
+    int64_t b = t * grid / T;
+    while (b + 1 < grid && T * (b + 1) / grid <= t) ++b;
+    while (b > 0 && T * b / grid > t) --b;
+    return (int32_t)b;
+  };
+  std::vector<int32_t> segfirst(nb), nseg(nb);
+  int maxseg = 1;
+  for (int I = 0; I < nb; ++I) {
+    segfirst[I] = cta_of(toff[I]);
+    nseg[I] = cta_of(toff[I + 1] - 1) - segfirst[I] + 1;
+    maxseg = std::max(maxseg, (int)nseg[I]);
+  }
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->segfirst, nb * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->nseg, nb * sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&p->rowpart, (size_t)nb * maxseg * kT * sizeof(dd_pair))) != cudaSuccess) return e;
+  cudaMemcpy(p->toff, toff.data(), toff.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->segfirst, segfirst.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->nseg, nseg.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice);
+  p->grid = grid;
+  p->nb = nb;
+  p->T = T;
+  p->maxseg = maxseg;
+  return cudaSuccess;
+}
+}  // namespace
+
 // Slice the (bitwise symmetric, single-rank) K into the int8 form; false if some entry is
 // not exactly representable (the fp64 symmetric kernel stays in use then)
 bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const double *rowmax, cudaStream_t s) {
   if (n < 1 || n > (1 << 18)) return false;  // |D_st| <= 64 * 64 * n < 2^31 in the int32 accumulators
   PFN_enc enc = get_enc();
   if (!enc) return false;
-  const int64_t ldk = (n + 127) / 128 * 128;
+  const int64_t ldk = (n + kT - 1) / kT * kT;
   if (!p || p->n != n) {
     symv_tc_free(p);
     p = new SymvTc();
     p->n = n;
     p->ldk = ldk;
     p->ldx = ldk;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaMalloc(&p->ks, (size_t)kSK * n * ldk) != cudaSuccess ||
         cudaMalloc(&p->xs, (size_t)kSX * p->ldx) != cudaSuccess || cudaMalloc(&p->dexp, 4 * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess) {
+        cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess || tc_plan(p, sms) != cudaSuccess) {
       cudaGetLastError();
       symv_tc_free(p);
       return false;
     }
     cudaMemset(p->xs, 0, (size_t)kSX * p->ldx);
-    cuuint64_t dk[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)kSK};
+    // K slices: [8][n rows][ldk] bytes (columns n .. ldk zero), boxes of 64 columns x 128 rows
+    cuuint64_t dk[3] = {(cuuint64_t)ldk, (cuuint64_t)n, (cuuint64_t)kSK};
     cuuint64_t sk[2] = {(cuuint64_t)ldk, (cuuint64_t)ldk * (cuuint64_t)n};
-    cuuint32_t bk[3] = {kTC, kTR, kSK}, es[3] = {1, 1, 1};
-    cuuint64_t dx[2] = {(cuuint64_t)n, (cuuint64_t)kSX}, sx[1] = {(cuuint64_t)p->ldx};
-    cuuint32_t bj[2] = {kTC, kSX}, bi[2] = {kTR, kSX};
+    cuuint32_t bk[3] = {64, kT, 1}, es[3] = {1, 1, 1};
+    // x slices: [16][ldx] bytes, boxes of 128 columns x 16 slices
+    cuuint64_t dx[2] = {(cuuint64_t)p->ldx, (cuuint64_t)kSX}, sx[1] = {(cuuint64_t)p->ldx};
+    cuuint32_t bx[2] = {kT, kSX};
     if (enc(&p->tmK, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->ks, dk, sk, bk, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS ||
-        enc(&p->tmXJ, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, p->xs, dx, sx, bj, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-            CUDA_SUCCESS ||
-        enc(&p->tmXI, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, p->xs, dx, sx, bi, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        enc(&p->tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, p->xs, dx, sx, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS) {
       symv_tc_free(p);
@@ -472,16 +595,25 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
   return flag == 0;
 }
 
-// the tile pass of the exact tensor-core apply: x's slices, then the tiles; the caller
-// (symv.cu) launches the shared finalize
-void launch_symv_tc(SymvTc *p, const SymvArgs &a, const double *xparts, int nxparts, int grid, cudaStream_t s) {
+// the tile pass of the exact tensor-core apply: x's slices, then the tiles; the row
+// segments are this plan's, so the finalize (launched by the caller, symv.cu) reads them
+void launch_symv_tc(SymvTc *p, SymvArgs &a, cudaStream_t s) {
   slice_x_kernel<<<(unsigned)std::min<int64_t>((p->n + 255) / 256, 296), 256, 0, s>>>(
-      a.x, p->n, xparts, nxparts, p->xs, p->ldx, p->dexp + 1, a.state);
+      a.x, p->n, a.xparts, a.nxparts, p->xs, p->ldx, p->dexp + 1, a.state);
   TcArgs ta{};
   ta.t = a;
+  ta.toff = p->toff;
+  ta.T = p->T;
+  ta.nb = p->nb;
+  ta.segfirst = p->segfirst;
+  ta.maxseg = p->maxseg;
+  ta.rowpart = p->rowpart;
   ta.eK = p->dexp;
   ta.F = p->dexp + 1;
-  symv_tc_kernel<<<grid, kTcThreads, kTcSmem, s>>>(p->tmK, p->tmXJ, p->tmXI, ta);
+  symv_tc_kernel<<<p->grid, kTcThreads, kTcSmem, s>>>(p->tmK, p->tmX, ta);
+  a.nseg = p->nseg;
+  a.maxseg = p->maxseg;
+  a.rowpart = p->rowpart;
 }
 
 }  // namespace laker

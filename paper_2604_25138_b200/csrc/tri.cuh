@@ -85,8 +85,9 @@ int tri_br(const SymvPlan *p);
 // otf_tc2.cu: the FAST symmetric on-the-fly tiles of a (128, 128) plan
 cudaError_t launch_otf_tc2_sym(const OzSlices &E, int64_t n, double scale, const double *w, double2 *cf,
                                const SymvArgs &ta, int grid, cudaStream_t s);
-// symv_tc.cu: x's digit slices, then the exact tensor-core tile pass writing a's partials
-void launch_symv_tc(SymvTc *p, const SymvArgs &a, const double *xparts, int nxparts, int grid, cudaStream_t s);
+// symv_tc.cu: x's digit slices, then the exact tensor-core tile pass writing a's column
+// partials and its own row segments (a's nseg / maxseg / rowpart are set to them)
+void launch_symv_tc(SymvTc *p, SymvArgs &a, cudaStream_t s);
 // y (and the epilogue of a.epi) from the partials written by a tile kernel of this plan
 void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s);
 

@@ -180,14 +180,15 @@ def test_symv_tensor_core_bitwise(ctx, L, cfg, n):
 
 
 def test_symv_tensor_core_not_used_when_inexact(ctx, L):
-    """A K entry off the 8-slice grid (one entry scaled by 2^-3: below max/8 its last
-    mantissa bits fall under 2^(eK-55)) keeps the fp64 kernel."""
+    """A K entry off the 8-slice grid (an odd multiple of 2^-55 while max |K| in [2, 4)
+    puts the grid at 2^(eK-55) = 2^-53) keeps the fp64 kernel."""
     n = 600
     P = make_problem(1, n=n)
     ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
     K, _ = O.assemble(P.E, P.scale)
     A = K.copy()
-    A[5, 400] = A[400, 5] = np.nextafter(A[5, 400] / 8.0, 0.0)
+    assert 2.0 <= K.max() < 4.0
+    A[5, 400] = A[400, 5] = np.ldexp(float(2 ** 52 + 1), -55)
     ctx.load_kernel_rows(A)
     st = ctx.stats()
     assert st["symmetric_k"] == 1 and st["k_tensor_core"] == 0
