@@ -18,17 +18,22 @@
 // as fp64) at the tile-stream rate.
 //
 // Tiles are 128 x 128 (block-row I takes the column blocks J = I .. nb - 1; persistent
-// CTAs take contiguous tile ranges).  A slice of a tile (16 KiB: two SWIZZLE_64B halves
-// of 64 columns) is the unit of the shared-memory ring; it feeds both products
-// (tools/mma_mn128_test.cu):
+// CTAs take contiguous tile ranges).  The slices are stored tile-major, upper triangle only
+// (n^2 / 2 entries x 8 bytes, as the fp64 triangle): slice s of tile t is 16 KiB contiguous,
+// two 64-column halves of 128 rows x 64 B, already in the SWIZZLE_64B image, so the producer
+// moves 4 slices (64 KiB) per ring slot with plain bulk copies (3 slots).  One slice feeds
+// both products (tools/mma_mn128_test.cu):
 //   rows    D_row[s] (M = 128, N = 16) += K_s (K-major, contraction over the 128 columns)
-//           x x_J slices, accumulated over the block-row segment in TMEM;
+//           x x_J slices, accumulated over the block-row segment in TMEM (warp 1);
 //   columns D_col[s] (M = 128, N = 16)  = K_s^T (MN-major A spanning both halves: LBO =
 //           8 KiB, "transpose A"; contraction over the 128 rows) x x_I slices, read out per
-//           tile (off the diagonal block).
-// At ~45 cycles per tcgen05.mma (tools/mma_rate.cu) the 64 MMAs of a tile take ~60% of
-// its HBM time.  TMEM (512 columns): D_row double-buffered [0, 256), D_col [256, 512).
-// Warps: 0 TMA producer, 1 MMA issuer, 2..5 epilogue (TMEM lane quadrants 2, 3, 0, 1).
+//           tile off the diagonal block (warp 6).
+// tools/mma_rate.cu, tools/mma_issue.cu: ~39 cycles per M = 128, N = 16 int8 MMA; the 64
+// MMAs of a tile then take ~60% of its HBM time, and the kernel runs at the bulk-copy
+// stream's rate (tools/tc_variants.sh: 170 us with the MMAs vs 159 us streaming alone at
+// C3; TC work alone 104 us).  TMEM (512 columns): D_row double-buffered [0, 256), D_col
+// [256, 512).  Warps: 0 producer, 1 row-product MMA issuer, 6 column-product MMA issuer,
+// 2..5 epilogue (TMEM lane quadrants 2, 3, 0, 1).
 #include <cuda.h>
 
 #include <algorithm>
@@ -39,21 +44,29 @@
 #include "tc_int8.cuh"
 #include "tri.cuh"
 
+// TC_EXP (tools/tc_variants.sh builds only; the library is built with 0): 1 = epilogue
+// without the level combine, 2 = producer without K loads (TC + epilogue alone), 3 = MMA
+// warp without MMAs (the bulk-copy stream alone), 4 = 1 + 2.
+#ifndef TC_EXP
+#define TC_EXP 0
+#endif
+
 namespace laker {
 namespace {
 
 constexpr int kT = 128;                             // tile rows = columns
 constexpr int kSK = 8;                              // slices of K
 constexpr int kSX = 16;                             // slices of x (MMA N)
-constexpr int kRing = 12;                           // slice slots in the ring
+constexpr int kSS = 4;                              // slices per ring slot (one mbarrier wait)
+constexpr int kRing = 3;                            // ring slots (12 slices, 192 KiB in flight)
 constexpr int kXJSlots = 3;                         // x_J tiles in flight
 constexpr uint32_t kHalfBytes = kT * 64;            // 8 KiB: 128 rows x 64 columns
 constexpr uint32_t kSliceBytes = 2 * kHalfBytes;    // 16 KiB
 constexpr uint32_t kXBytes = kSX * kT;              // 2 KiB: 16 slices x 128
-constexpr int kTcThreads = 6 * 32;
+constexpr int kTcThreads = 7 * 32;
 constexpr int kLevels = kSK + kSX - 1;              // 23
-// shared layout (1024-aligned base): [kRing][slice 16 KiB] [kXJSlots][x_J] [2][x_I] barriers
-constexpr size_t kOffXJ = (size_t)kRing * kSliceBytes;
+// shared layout (1024-aligned base): [kRing][kSS slices of 16 KiB] [kXJSlots][x_J] [2][x_I] barriers
+constexpr size_t kOffXJ = (size_t)kRing * kSS * kSliceBytes;
 constexpr size_t kOffXI = kOffXJ + (size_t)kXJSlots * kXBytes;
 constexpr size_t kOffBar = kOffXI + 2 * kXBytes;
 constexpr size_t kTcSmem = 1024 + kOffBar + 512;
@@ -69,15 +82,6 @@ __device__ __forceinline__ uint64_t sdesc_mn_sw64(uint32_t addr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)4 << 61;
   return d;
-}
-
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int32_t c0, int32_t c1, int32_t c2,
-                                            uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // Single-thread tcgen05 operations issued from converged warp code: one lane is elected
@@ -153,13 +157,13 @@ struct TcArgs {
   const int32_t *segfirst;  // [nb] first CTA covering block-row I
   int32_t maxseg;
   dd_pair *rowpart;         // [nb][maxseg][128]
+  const int8_t *ks;         // the tile-major slice store
   const int *eK;  // global exponent of K's slices (device)
   const int *F;   // exponent of this x's slices (device, written by the slicing kernel)
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1)
-    symv_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmX,
-                   const TcArgs ta) {
+    symv_tc_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs ta) {
   const SymvArgs &a = ta.t;
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   extern __shared__ unsigned char smem_raw[];
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);
     }
     for (int s = 0; s < kXJSlots; ++s) {
       mbar_init(&xjf[s], 1);
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------- TMA producer
     if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
       int I = I0;
       int64_t rend = ta.toff[I + 1];
       int xb = 0, nseg = 0, slot = 0, tb = 0;
@@ -236,12 +241,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           xj_full = true;
         }
 #pragma unroll 1
-        for (int s = 0; s < kSK; ++s) {
+        for (int g = 0; g < kSK / kSS; ++g) {
           if (ring_full) mbar_wait(&empty[slot], ph ^ 1u);
-          unsigned char *dst = sK + (size_t)slot * kSliceBytes;
-          mbar_arrive_expect_tx(&full[slot], kSliceBytes);
-          tma_load_3d(dst, &tmK, J * kT, I * kT, s, &full[slot]);
-          tma_load_3d(dst + kHalfBytes, &tmK, J * kT + 64, I * kT, s, &full[slot]);
+          // slices g kSS .. of tile t: 16 KiB contiguous each in the tile-major store, one box each
+#if TC_EXP == 2 || TC_EXP == 4
+          mbar_arrive(&full[slot]);
+#else
+          mbar_arrive_expect_tx(&full[slot], kSS * kSliceBytes);
+#pragma unroll
+          for (int ss = 0; ss < kSS; ++ss)
+            bulk_g2s(sK + (size_t)(slot * kSS + ss) * kSliceBytes, ta.ks + (t * kSK + g * kSS + ss) * kSliceBytes,
+                     kSliceBytes, &full[slot], pol);
+#endif
           if (++slot == kRing) {
             slot = 0;
             ph ^= 1u;
@@ -253,13 +264,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     return;
   }
 
-  if (warp == 1) {
-    // ---------------------------------------------------------- MMA issuer (whole warp,
-    // one lane elected per MMA / commit)
+  if (warp == 1 || warp == 6) {
+    // ---------------------------------------------------------- MMA issuers (whole warps,
+    // one lane elected per MMA / commit): warp 1 the row products, warp 6 the column
+    // products; each releases every ring slot (empty: 2 arrivals)
+    const bool rows = warp == 1;
     constexpr uint32_t idr = tc::idesc_i8(kT, kSX);
     constexpr uint32_t idc = tc::idesc_i8(kT, kSX) | (1u << 15);  // A = K_s^T (MN-major)
-    const uint64_t dK0 = tc::sdesc_k_sw64(smem_u32(sK));
-    const uint64_t dKt0 = sdesc_mn_sw64(smem_u32(sK));
+    const uint64_t dK0 = rows ? tc::sdesc_k_sw64(smem_u32(sK)) : sdesc_mn_sw64(smem_u32(sK));
     const uint64_t dXJ0 = tc::sdesc_k_sw128(smem_u32(sXJ));
     const uint64_t dXI0 = tc::sdesc_k_sw128(smem_u32(sXI));
     int I = I0;
@@ -272,36 +284,51 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const bool newI = (t == t0) || (t >= rend);
       while (t >= rend) rend = ta.toff[++I + 1];
       const int J = I + (int)(t - ta.toff[I]);
+      const bool off = J != I;  // off the diagonal block: the column product too
       if (newI) {
-        if (nseg >= 2) mbar_wait(&rowe[rb], (uint32_t)(((nseg - 2) >> 1) & 1));  // row buffer drained
-        mbar_wait(&xif[xb], (uint32_t)((nseg >> 1) & 1));
+        if (rows) {
+          if (nseg >= 2) mbar_wait(&rowe[rb], (uint32_t)(((nseg - 2) >> 1) & 1));  // row buffer drained
+        } else {
+          mbar_wait(&xif[xb], (uint32_t)((nseg >> 1) & 1));
+        }
         ++nseg;
         acc = false;
       }
-      mbar_wait(&xjf[tb], tph);
-      const bool off = J != I;  // off the diagonal block: the column product too
-      if (off && ncol >= 2) mbar_wait(&cole[cb], (uint32_t)(((ncol - 2) >> 1) & 1));
+      if (rows) {
+        mbar_wait(&xjf[tb], tph);
+      } else if (off && ncol >= 2) {
+        mbar_wait(&cole[cb], (uint32_t)(((ncol - 2) >> 1) & 1));
+      }
       tc::fence_after();
-      const uint32_t trow = tmem + (uint32_t)(rb * 128), tcol = tmem + 256 + (uint32_t)(cb * 128);
       // descriptors: the start-address field is addr >> 4 in the low 14 bits, so an
       // offset inside shared memory is added to the base descriptor (no carry: < 256 KiB)
-      const uint64_t dXJ = dXJ0 + (uint64_t)((tb * kXBytes) >> 4);
-      const uint64_t dXI = dXI0 + (uint64_t)((xb * kXBytes) >> 4);
+      const uint32_t td = rows ? tmem + (uint32_t)(rb * 128) : tmem + 256 + (uint32_t)(cb * 128);
+      const uint64_t dX = rows ? dXJ0 + (uint64_t)((tb * kXBytes) >> 4) : dXI0 + (uint64_t)((xb * kXBytes) >> 4);
+      const bool work = rows || off;
 #pragma unroll 1
-      for (int s = 0; s < kSK; ++s) {
+      for (int g = 0; g < kSK / kSS; ++g) {
         mbar_wait(&full[slot], ph);
         tc::fence_after();
-        const uint64_t so = (uint64_t)((slot * kSliceBytes) >> 4);
+#if TC_EXP != 3
+        if (work) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // columns 32 kk ..: half kk / 2, +32 B inside it
-          mma_i8_elect(trow + 16 * s, dK0 + so + (uint64_t)(((kk >> 1) * kHalfBytes + (kk & 1) * 32) >> 4),
-                       dXJ + (uint64_t)((kk * 32) >> 4), idr, (acc || kk > 0) ? 1u : 0u);
-        if (off) {
+          for (int ss = 0; ss < kSS; ++ss) {
+            const int s = g * kSS + ss;
+            const uint64_t so = (uint64_t)(((slot * kSS + ss) * kSliceBytes) >> 4);
+            if (rows) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // rows 32 kk ..: 2 KiB into each half
-            mma_i8_elect(tcol + 16 * s, dKt0 + so + (uint64_t)((kk * 2048) >> 4), dXI + (uint64_t)((kk * 32) >> 4),
-                         idc, kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < 4; ++kk)  // columns 32 kk ..: half kk / 2, +32 B inside it
+                mma_i8_elect(td + 16 * s, dK0 + so + (uint64_t)(((kk >> 1) * kHalfBytes + (kk & 1) * 32) >> 4),
+                             dX + (uint64_t)((kk * 32) >> 4), idr, (acc || kk > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)  // rows 32 kk ..: 2 KiB into each half
+                mma_i8_elect(td + 16 * s, dK0 + so + (uint64_t)((kk * 2048) >> 4), dX + (uint64_t)((kk * 32) >> 4),
+                             idc, kk > 0 ? 1u : 0u);
+            }
+          }
         }
+#endif
         commit_elect(&empty[slot]);
         if (++slot == kRing) {
           slot = 0;
@@ -309,28 +336,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       acc = true;
-      commit_elect(&xje[tb]);
-      if (++tb == kXJSlots) {
-        tb = 0;
-        tph ^= 1u;
-      }
-      if (off) {
+      if (rows) {
+        commit_elect(&xje[tb]);
+        if (++tb == kXJSlots) {
+          tb = 0;
+          tph ^= 1u;
+        }
+      } else if (off) {
         commit_elect(&colf[cb]);
         cb ^= 1;
         ++ncol;
       }
-      if (t + 1 == t1 || t + 1 >= rend) {  // segment complete: rows to the epilogue, x_I slot free
-        commit_elect(&rowf[rb]);
-        commit_elect(&xie[xb]);
-        rb ^= 1;
-        xb ^= 1;
+      if (t + 1 == t1 || t + 1 >= rend) {  // segment complete: rows to the epilogue / x_I slot free
+        if (rows) {
+          commit_elect(&rowf[rb]);
+          rb ^= 1;
+        } else {
+          commit_elect(&xie[xb]);
+          xb ^= 1;
+        }
       }
     }
     __syncwarp();
-    // the allocating warp releases TMEM once the epilogue has drained every accumulator
-    asm volatile("bar.sync 1, 160;" ::: "memory");
-    tc::fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    // the allocating warp releases TMEM once both issuers and the epilogue are done
+    asm volatile("bar.sync 1, 192;" ::: "memory");
+    if (rows) {
+      tc::fence_after();
+      tc::tmem_dealloc(tmem, 512);
+    }
     return;
   }
 
@@ -348,7 +381,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (J != I) {
       mbar_wait(&colf[cb], (uint32_t)((ncol >> 1) & 1));
       tc::fence_after();
+#if TC_EXP == 1 || TC_EXP == 4
+      const dd_pair v = {0.0, 0.0};
+#else
       const dd_pair v = combine_levels(tmem + 256 + (uint32_t)(cb * 128) + ((uint32_t)(32 * q) << 16), escale);
+#endif
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&cole[cb]);
@@ -370,7 +407,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   }
   tc::fence_before();
-  asm volatile("bar.sync 1, 160;" ::: "memory");
+  asm volatile("bar.sync 1, 192;" ::: "memory");
 }
 
 // x -> 16 digit slices with one exponent: F with max|x| < 2^F (from the per-CTA maxima
@@ -380,12 +417,21 @@ __global__ void __launch_bounds__(256) slice_x_kernel(const double *__restrict__
                                                       int8_t *__restrict__ xs, int64_t ldx, int *Fout,
                                                       const PcgState *st) {
   if (st && *(volatile const int32_t *)&st->done) return;
-  double m = 0.0;
-  for (int k = 0; k < nparts; ++k) m = fmax(m, parts[k]);
-  int F = 0;
-  if (m > 0.0) frexp(m, &F);  // m = f 2^F, f in [0.5, 1): |x| <= m < 2^F
-  if (blockIdx.x == 0 && threadIdx.x == 0) *Fout = F;
-  const double sc = ldexp(1.0, -(F + 1));
+  __shared__ int sF;
+  if (threadIdx.x < 32) {
+    double m = 0.0;
+    for (int k = threadIdx.x; k < nparts; k += 32) m = fmax(m, parts[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int F = 0;
+    if (m > 0.0) frexp(m, &F);  // m = f 2^F, f in [0.5, 1): |x| <= m < 2^F
+    if (threadIdx.x == 0) {
+      sF = F;
+      if (blockIdx.x == 0) *Fout = F;
+    }
+  }
+  __syncthreads();
+  const double sc = ldexp(1.0, -(sF + 1));
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     double v = __dmul_rn(x[j], sc);  // exact (power of two), |v| < 0.5
 #pragma unroll
@@ -398,37 +444,48 @@ __global__ void __launch_bounds__(256) slice_x_kernel(const double *__restrict__
   }
 }
 
-// K (rows x n, stride ld) -> 8 slices (slice s: rows x ldk bytes at ks + s rows ldk, the
-// padding columns n .. ldk zero) with the global exponent eK (max |K| < 2^eK); flag[0] = 1
-// if some entry is not exact.  Thread: 8 consecutive columns of one row, 8-byte stores.
-__global__ void __launch_bounds__(256) slice_k_kernel(const double *__restrict__ K, int64_t rows, int64_t n,
-                                                      int64_t ld, int eK, int8_t *__restrict__ ks, int64_t ldk,
-                                                      int *flag) {
+// K (n x n, stride ld) -> the tile-major slice store: for upper-triangle tile t = (I, J)
+// (plan order) and slice s, 16 KiB at ks + (8 t + s) 16 KiB holding [half h][row r][64 B]
+// = the digits of K[128 I + r][128 J + 64 h + b] (zero past n): the shared-memory image of
+// one ring slot before the SWIZZLE_64B the TMA applies.  eK: max |K| < 2^eK; flag[0] = 1
+// if some entry is not exact.  Block: one tile; thread: 8 consecutive columns of a row per
+// item, 8-byte stores.
+__global__ void __launch_bounds__(256) slice_k_kernel(const double *__restrict__ K, int64_t n, int64_t ld,
+                                                      const int64_t *__restrict__ toff, int nb, int eK,
+                                                      int8_t *__restrict__ ks, int *flag) {
+  const int64_t t = blockIdx.x;
+  const int I = find_block_row(toff, nb, t);
+  const int J = I + (int)(t - toff[I]);
   const double sc = ldexp(1.0, -(eK + 1));
-  const int64_t j0 = 8 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   bool bad = false;
-  if (j0 < ldk) {
-    for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
-      unsigned long long w[kSK];
+#pragma unroll 1
+  for (int it = threadIdx.x; it < 2 * kT * 8; it += blockDim.x) {
+    const int h = it >> 10, r = (it >> 3) & (kT - 1), b8 = it & 7;
+    const int64_t i = (int64_t)I * kT + r, j0 = (int64_t)J * kT + 64 * h + 8 * b8;
+    unsigned long long w[kSK];
 #pragma unroll
-      for (int s = 0; s < kSK; ++s) w[s] = 0ull;
+    for (int q = 0; q < kSK; ++q) w[q] = 0ull;
+    if (i < n) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (j0 + k >= n) break;
         double v = __dmul_rn(K[i * ld + j0 + k], sc);
 #pragma unroll
-        for (int s = 0; s < kSK; ++s) {
+        for (int q = 0; q < kSK; ++q) {
           v = __dmul_rn(v, 128.0);
           const double d = rint(v);
           v = __dsub_rn(v, d);
-          w[s] |= (unsigned long long)(uint8_t)(int8_t)(int)d << (8 * k);
+          w[q] |= (unsigned long long)(uint8_t)(int8_t)(int)d << (8 * k);
         }
         bad |= v != 0.0;
       }
-#pragma unroll
-      for (int s = 0; s < kSK; ++s)
-        *reinterpret_cast<unsigned long long *>(ks + ((int64_t)s * rows + i) * ldk + j0) = w[s];
     }
+    // the SWIZZLE_64B image (16-byte chunk c of a 64-byte row r at chunk c ^ ((r >> 1) & 3)),
+    // so a plain bulk copy lands the layout the MMA descriptors expect
+    int8_t *dst = ks + ((t * kSK) * 2 * kT + h * kT + r) * 64 + 16 * ((b8 >> 1) ^ ((r >> 1) & 3)) + 8 * (b8 & 1);
+#pragma unroll
+    for (int q = 0; q < kSK; ++q)
+      *reinterpret_cast<unsigned long long *>(dst + (int64_t)q * kSliceBytes) = w[q];
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
 }
@@ -466,11 +523,11 @@ PFN_enc get_enc() {
 }  // namespace
 
 struct SymvTc {
-  int64_t n = 0, ldk = 0, ldx = 0;
+  int64_t n = 0, ldx = 0;
   int8_t *ks = nullptr, *xs = nullptr;
   int *dexp = nullptr;  // [0] eK, [1] F of the last sliced x, [2] exactness flag
   double *dmax = nullptr;
-  CUtensorMap tmK, tmX;
+  CUtensorMap tmX;
   // the 128 x 128 tile plan for `grid` persistent CTAs (the finalize's segments)
   int grid = 0, nb = 0, maxseg = 0;
   int64_t T = 0;
@@ -542,35 +599,27 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
   if (n < 1 || n > (1 << 18)) return false;  // |D_st| <= 64 * 64 * n < 2^31 in the int32 accumulators
   PFN_enc enc = get_enc();
   if (!enc) return false;
-  const int64_t ldk = (n + kT - 1) / kT * kT;
+  const int64_t ldx = (n + kT - 1) / kT * kT;
   if (!p || p->n != n) {
     symv_tc_free(p);
     p = new SymvTc();
     p->n = n;
-    p->ldk = ldk;
-    p->ldx = ldk;
+    p->ldx = ldx;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaMalloc(&p->ks, (size_t)kSK * n * ldk) != cudaSuccess ||
+    if (tc_plan(p, sms) != cudaSuccess || cudaMalloc(&p->ks, (size_t)p->T * kSK * kSliceBytes) != cudaSuccess ||
         cudaMalloc(&p->xs, (size_t)kSX * p->ldx) != cudaSuccess || cudaMalloc(&p->dexp, 4 * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess || tc_plan(p, sms) != cudaSuccess) {
+        cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess) {
       cudaGetLastError();
       symv_tc_free(p);
       return false;
     }
     cudaMemset(p->xs, 0, (size_t)kSX * p->ldx);
-    // K slices: [8][n rows][ldk] bytes (columns n .. ldk zero), boxes of 64 columns x 128 rows
-    cuuint64_t dk[3] = {(cuuint64_t)ldk, (cuuint64_t)n, (cuuint64_t)kSK};
-    cuuint64_t sk[2] = {(cuuint64_t)ldk, (cuuint64_t)ldk * (cuuint64_t)n};
-    cuuint32_t bk[3] = {64, kT, 1}, es[3] = {1, 1, 1};
     // x slices: [16][ldx] bytes, boxes of 128 columns x 16 slices
     cuuint64_t dx[2] = {(cuuint64_t)p->ldx, (cuuint64_t)kSX}, sx[1] = {(cuuint64_t)p->ldx};
-    cuuint32_t bx[2] = {kT, kSX};
-    if (enc(&p->tmK, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, p->ks, dk, sk, bk, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-            CUDA_SUCCESS ||
-        enc(&p->tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, p->xs, dx, sx, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint32_t bx[2] = {kT, kSX}, es[2] = {1, 1};
+    if (enc(&p->tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, p->xs, dx, sx, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS) {
       symv_tc_free(p);
@@ -587,8 +636,7 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
   std::frexp(hmax, &eK);
   int hexp[3] = {eK, 0, 0};
   cudaMemcpyAsync(p->dexp, hexp, 3 * sizeof(int), cudaMemcpyHostToDevice, s);
-  const dim3 grid((unsigned)((ldk / 8 + 255) / 256), (unsigned)std::min<int64_t>(n, 65535));
-  slice_k_kernel<<<grid, 256, 0, s>>>(K, n, n, ld, eK, p->ks, ldk, p->dexp + 2);
+  slice_k_kernel<<<(unsigned)p->T, 256, 0, s>>>(K, n, ld, p->toff, p->nb, eK, p->ks, p->dexp + 2);
   int flag = 1;
   cudaMemcpyAsync(&flag, p->dexp + 2, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return false;
@@ -608,9 +656,10 @@ void launch_symv_tc(SymvTc *p, SymvArgs &a, cudaStream_t s) {
   ta.segfirst = p->segfirst;
   ta.maxseg = p->maxseg;
   ta.rowpart = p->rowpart;
+  ta.ks = p->ks;
   ta.eK = p->dexp;
   ta.F = p->dexp + 1;
-  symv_tc_kernel<<<p->grid, kTcThreads, kTcSmem, s>>>(p->tmK, p->tmX, ta);
+  symv_tc_kernel<<<p->grid, kTcThreads, kTcSmem, s>>>(p->tmX, ta);
   a.nseg = p->nseg;
   a.maxseg = p->maxseg;
   a.rowpart = p->rowpart;

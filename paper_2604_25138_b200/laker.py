@@ -20,7 +20,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblaker.so")
+# LAKER_LIB_PATH: an alternative build of the same library (tools/ A/B experiments only)
+LIB_PATH = os.environ.get("LAKER_LIB_PATH") or os.path.join(_HERE, "liblaker.so")
 
 LAKER_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "DIMENSION_MISMATCH", 3: "NOT_READY", 4: "CUDA", 5: "NCCL",

@@ -8,8 +8,9 @@ on-the-fly operator, and the T24 residual certificate at n = 65536).
   iteration count, residual history and alpha must be identical (protocol step 4).
 * C3 own fit (harness Z): the oracle fits its own P (O4', P:484-515) and solves;
   alpha within 1e-6 (R14) and the GPU count inside the R15(iii) envelope: the
-  oracle's own fit + solve on 8 copies of K with every entry moved +-1 ulp (seeded,
-  symmetric), [min - 2, max + 2].
+  oracle's own fit + solve on K and 8 copies of K with every entry moved +-1 ulp
+  (seeded, symmetric), each with P applied in three passes and in the QM form (R21),
+  [min - 2, max + 2].
 * C4: 4 seeded columns of the 64-RHS LEARNED block solve, each identical to the
   single-RHS oracle solve with the same P (T18 + M5).
 * C5 downscale (n = 8192, lambda = 1e-5, C5's generator): the on-the-fly EXACT
@@ -69,13 +70,15 @@ def _staged(K, lam, y, Q, M, ai, QM, **kw):
 
 def _oracle_own(K, lam, y, Z, tol):
     """The oracle end to end with its own fit: O4' structured CCCP on Z, factored P,
-    Alg. 1 PCG.  Returns (alpha, iterations)."""
+    Alg. 1 PCG, with P applied in three passes and in the QM form of reading R21 (the
+    oracle's own QM = Q M).  Returns (alpha of the three-pass solve, [iterations of both])."""
     _, rep, st = O.cccp_fit_structured(K, lam, Z, form_P=False)
     assert rep.converged
     Q, M, ai = O.factors(st)
     a, r = O.pcg_factored(K, lam, y, Q, M, ai, tol=tol)
-    assert r.termination == O.TERM_RESIDUAL_TOL
-    return a, r.iters
+    aq, rq = O.pcg_factored_qm(K, lam, y, Q, np.ascontiguousarray(Q @ M), ai, tol=tol)
+    assert r.termination == O.TERM_RESIDUAL_TOL and rq.termination == O.TERM_RESIDUAL_TOL
+    return a, [r.iters, rq.iters]
 
 
 def test_c3_staged_full_solve(L, c3):
@@ -114,9 +117,9 @@ def test_c3_own_fit_r14_r15(L, c3):
     assert rg[0]["termination"] == L.TERM_RESIDUAL_TOL
     ao, it0 = _oracle_own(K, P.lam, P.y, Z, P.tol)
     err = np.linalg.norm(ag - ao) / np.linalg.norm(ao)
-    its = [it0]
+    its = list(it0)
     for s in range(8):
-        its.append(_oracle_own(_flip_ulp(K, 1000 + s), P.lam, P.y, Z, P.tol)[1])
+        its += _oracle_own(_flip_ulp(K, 1000 + s), P.lam, P.y, Z, P.tol)[1]
     print(f"C3 own fit: GPU {rg[0]['iters']} its, oracle {it0}, envelope {sorted(its)}, R14 {err:.2e}")
     assert err <= 1e-6
     assert min(its) - 2 <= rg[0]["iters"] <= max(its) + 2, (rg[0]["iters"], its)
@@ -207,7 +210,9 @@ def test_c5_downscale_fast_on_the_fly(L, c5d):
     assert rf[0]["termination"] == L.TERM_RESIDUAL_TOL
     ao, it0 = _oracle_own(K, P.lam, P.y, Z, P.tol)
     err = np.linalg.norm(af - ao) / np.linalg.norm(ao)
-    its = [it0] + [_oracle_own(_flip_ulp(K, 2000 + s), P.lam, P.y, Z, P.tol)[1] for s in range(4)]
+    its = list(it0)
+    for s in range(4):
+        its += _oracle_own(_flip_ulp(K, 2000 + s), P.lam, P.y, Z, P.tol)[1]
     print(f"C5 downscale FAST: GPU {rf[0]['iters']} its, oracle envelope {sorted(its)}, R14 {err:.2e}")
     assert err <= 1e-6
     assert min(its) - 2 <= rf[0]["iters"] <= max(its) + 2, (rf[0]["iters"], its)

@@ -57,16 +57,22 @@ def _flip_ulp(K, seed):
 
 
 def _oracle_own_iters(K, lam, y, Z, tol):
+    """The oracle's own fit + solve in both application forms of the factored P (three
+    passes Q (M (Q^T r)), and the QM form of reading R21 the GPU applies by default, with
+    the oracle's own QM = Q M): two members of the R15(iii) envelope."""
     _, rep, st = O.cccp_fit_structured(K, lam, Z, form_P=False)
     Q, M, ai = O.factors(st)
-    return O.pcg_factored(K, lam, y, Q, M, ai, tol=tol)[1].iters
+    QM = np.ascontiguousarray(Q @ M)
+    return [O.pcg_factored(K, lam, y, Q, M, ai, tol=tol)[1].iters,
+            O.pcg_factored_qm(K, lam, y, Q, QM, ai, tol=tol)[1].iters]
 
 
 @pytest.mark.parametrize("cid,n", [(1, None), (2, None)])
 def test_learned_pcg_end_to_end(ctx, L, cid, n):
     """End-to-end (own fit, own K, the default QM-form P): alpha within 1e-6 of Cholesky
     (R14), iteration count inside the R15(iii) envelope -- the oracle's own fit + solve on
-    8 copies of K with every entry moved +-1 ulp (seeded, symmetric), [min-2, max+2] --
+    K and 8 copies of K with every entry moved +-1 ulp (seeded, symmetric), each solved
+    with P applied in both forms (three passes and QM, reading R21), [min-2, max+2] --
     and fewer iterations than Jacobi (T21).  The B5 envelope of round 1 (the oracle's P
     perturbed at the measured GPU deviation) is printed beside it for the record."""
     P, K, Pg, rep, Po, ro, st = _fit_both(ctx, L, cid, n)
@@ -75,8 +81,9 @@ def test_learned_pcg_end_to_end(ctx, L, cid, n):
     ref = O.reference_solve(K, P.lam, P.y)
     assert reps[0]["termination"] == L.TERM_RESIDUAL_TOL
     assert np.linalg.norm(ag - ref) / np.linalg.norm(ref) <= 1e-6
-    its = [_oracle_own_iters(K, P.lam, P.y, Z, P.tol)]
-    its += [_oracle_own_iters(_flip_ulp(K, 500 + s), P.lam, P.y, Z, P.tol) for s in range(8)]
+    its = _oracle_own_iters(K, P.lam, P.y, Z, P.tol)
+    for s in range(8):
+        its += _oracle_own_iters(_flip_ulp(K, 500 + s), P.lam, P.y, Z, P.tol)
     r = np.random.default_rng(0)
     dev = max(np.linalg.norm(Pg - Po) / np.linalg.norm(Po), 2.0 ** -52)
     b5 = []
