@@ -358,14 +358,19 @@ def run_ours(args, rank, world, local_rank):
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     rows = n // world
-    sym, fac, nr = s1["symmetric_k"], s1["p_factored"], s1["n_dirs"]
+    sym, fac, nr, ktc = s1["symmetric_k"], s1["p_factored"], s1["n_dirs"], s1["k_tensor_core"]
     # algorithmic bytes per operator apply: the stored
     # triangle of the symmetric K (symv) or the local rows (gemv), plus x read and y written
     if sym:
         # the stored triangle + x read + y written, + the fused update's alpha/r read+write and p read
         bytes_per_launch = 8.0 * n * (n + 1) / 2 + 16.0 * n + (40.0 * n if world == 1 else 0.0)
-        kname = ("symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, offset-Fast2Sum "
-                 "compensated sums; the PCG update step fused into the finalize)")
+        if ktc:
+            kname = ("slice_x_kernel + symv_tc_kernel + symv_finalize_kernel (K.p over the block upper triangle, "
+                     "exact on the int8 tensor cores: K as 8 seven-bit digit slices (8 B / entry, as fp64), p as 16; "
+                     "the PCG update step fused into the finalize)")
+        else:
+            kname = ("symv_dot2_kernel + symv_finalize_kernel (K.p over the block upper triangle, offset-Fast2Sum "
+                     "compensated sums; the PCG update step fused into the finalize)")
     else:
         bytes_per_launch = 8.0 * rows * n + 16.0 * n
         kname = "gemv_dot2_kernel (K.p, Dot2 rows, bulk-TMA ring)"
@@ -388,7 +393,8 @@ def run_ours(args, rank, world, local_rank):
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback",
-            "traffic": _traffic_per_launch("symv" if sym else "gemv"), "bytes_per_launch": bytes_per_launch,
+            "traffic": _traffic_per_launch(("symv_tc" if ktc else "symv") if sym else "gemv"),
+            "bytes_per_launch": bytes_per_launch,
             "mean_launch_ms": dom_ms, "launches": op_launches}
     if prec_bytes and prec_launches:
         roof["precond"] = {"kernel": pname, "bytes_per_apply": prec_bytes, "mean_apply_ms": prec_ms,
@@ -404,11 +410,13 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": "C3 (BASELINE.json configs[2]): n=16384 clustered sensors, d=64, "
                                    "lambda=1e-4, PCG to rel resid 1e-8, K materialized 2 GiB, grid 256x256",
                        "precond": args.precond, "mode": args.mode, "parallelism": f"rowshard{world}",
-                       "k_apply": "symmetric (upper triangle)" if sym else "full rows",
+                       "k_apply": ("symmetric (upper triangle), exact int8 tensor cores" if ktc else
+                                   "symmetric (upper triangle)") if sym else "full rows",
                        "p_layout": ("factored, N_r=%d" % nr) if fac else ("dense" if args.precond == "learned"
                                                                            else args.precond),
                        "l2": "inputs larger than L2 (K = 2 GiB per solve pass >> 126 MB)"},
             "time_to_solution_s": pcg_total / args.steps, "pcg_iters_per_solve": its[0],
+            "solve_us_per_iter": [round(t / max(k, 1) * 1e6, 1) for t, k in zip(pcg_s, its)],
             "kappa_PA_lanczos": rep["lanczos_lmax"] / rep["lanczos_lmin"] if rep["lanczos_lmin"] > 0 else None,
             "stage_ms": {k: v / args.steps for k, v in stage.items()},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
