@@ -322,7 +322,7 @@ __device__ __forceinline__ dd_pair ldcg_pair(const dd_pair *p) {
   return dd_pair{v.x, v.y};
 }
 
-template <int BR>
+template <int BR, bool TCP>
 __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvArgs a) {
   if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
   __shared__ dd_pair sred[kFinThreads / 32];
@@ -332,6 +332,27 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
   constexpr int kW = kFinThreads / 32;  // 16 warps
   static_assert(BR % 32 == 0, "a 32-row group lies in one block-row");
   dd_pair dotp = {0.0, 0.0};
+  if constexpr (TCP) {
+    // the exact tensor-core apply (symv_tc.cu): row i's 8 exact level groups -> its pair
+    // (zeroing them for the next apply); one 32-row group per warp, lane = row
+    const int escale = a.tc_exp[0] + a.tc_exp[1] + 2 - 14;
+    for (int64_t g = (int64_t)blockIdx.x * kW + warp; g * 32 < a.n; g += (int64_t)gridDim.x * kW) {
+      const int64_t i = g * 32 + lane;
+      if (i >= a.n) continue;
+      long long G[kTcGroups];
+#pragma unroll
+      for (int q = 0; q < kTcGroups; ++q) {
+        G[q] = __ldcg(&a.yacc[q * a.ldy + i]);
+        a.yacc[q * a.ldy + i] = 0;
+      }
+      dd_pair t = tc_groups_to_pair(G, escale);
+      const double xi = a.x[i];
+      if (a.lambda != 0.0) dot2_step(t, a.lambda, xi);
+      const double yv = pair_value(t);
+      a.y[i] = yv;
+      dot2_step(dotp, xi, yv);
+    }
+  } else {
   // one 32-row group per iteration: lane = row, warp w sums the column partials I = w
   // (mod 16) of the block-rows above (each load: 32 consecutive 16-byte pairs) and the
   // row segments q = w (mod 16); warp 0 then combines the 16 warp sums in warp order
@@ -368,6 +389,7 @@ __global__ void __launch_bounds__(kFinThreads) symv_finalize_kernel(const SymvAr
       }
     }
     __syncthreads();
+  }
   }
   dotp = warp_reduce_pair(dotp);
   if (lane == 0) sred[warp] = dotp;
@@ -671,14 +693,16 @@ struct SymvPlan {
 
 size_t symv_smem_bytes() { return kSymSmem; }
 
-// CTAs of symv_finalize_kernel<kSR> guaranteed co-resident (the fused update's grid barrier)
+// CTAs of symv_finalize_kernel<kSR, *> guaranteed co-resident (the fused update's grid barrier)
 int fused_fin_grid() {
   static int g = 0;
   if (g == 0) {
     int per = 0, sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, symv_finalize_kernel<kSR>, kFinThreads, 0);
-    g = std::max(1, per) * sms;
+    int per2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, symv_finalize_kernel<kSR, false>, kFinThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, symv_finalize_kernel<kSR, true>, kFinThreads, 0);
+    g = std::max(1, std::min(per, per2)) * sms;
   }
   return g;
 }
@@ -882,9 +906,9 @@ void launch_tri_finalize(const SymvPlan *p, const SymvArgs &a, cudaStream_t s) {
     return;
   }
   if (p->br == 128)
-    symv_finalize_kernel<128><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+    symv_finalize_kernel<128, false><<<p->fin_grid, kFinThreads, 0, s>>>(a);
   else
-    symv_finalize_kernel<64><<<p->fin_grid, kFinThreads, 0, s>>>(a);
+    symv_finalize_kernel<64, false><<<p->fin_grid, kFinThreads, 0, s>>>(a);
 }
 
 int symv_finalize_grid(const SymvPlan *p) { return p->fin_grid; }
@@ -942,7 +966,8 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   }
   a.ypair = g.ypair;
   a.upd = g.upd;
-  if (g.tc != nullptr && which == 0 && !p->dist)
+  const bool tc = g.tc != nullptr && which == 0 && !p->dist;
+  if (tc)
     launch_symv_tc(g.tc, a, s);
   else if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
@@ -950,10 +975,15 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
     symv_dot2_kernel<false><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   if (p->dist)
     tri_finalize_dist_kernel<kSR, kSC><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
-  else if (g.upd.on)  // co-resident grid for the grid barrier
-    symv_finalize_kernel<kSR><<<dim3(std::min(p->fin_grid, fused_fin_grid())), dim3(kFinThreads), 0, s>>>(a);
+  else if (tc)  // one 32-row group per warp: a small grid (a cheap grid barrier), co-resident
+    symv_finalize_kernel<kSR, true><<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(
+                                           fused_fin_grid(), (p->n + 32 * (kFinThreads / 32) - 1) /
+                                                                 (32 * (kFinThreads / 32))))),
+                                       dim3(kFinThreads), 0, s>>>(a);
+  else if (g.upd.on)
+    symv_finalize_kernel<kSR, false><<<dim3(std::min(p->fin_grid, fused_fin_grid())), dim3(kFinThreads), 0, s>>>(a);
   else
-    symv_finalize_kernel<kSR><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
+    symv_finalize_kernel<kSR, false><<<dim3(p->fin_grid), dim3(kFinThreads), 0, s>>>(a);
 }
 
 void launch_symv_check(const double *A, int64_t n, int64_t ld, int *flag, cudaStream_t s) {

@@ -64,7 +64,8 @@ constexpr uint32_t kHalfBytes = kT * 64;            // 8 KiB: 128 rows x 64 colu
 constexpr uint32_t kSliceBytes = 2 * kHalfBytes;    // 16 KiB
 constexpr uint32_t kXBytes = kSX * kT;              // 2 KiB: 16 slices x 128
 constexpr int kTcThreads = 7 * 32;
-constexpr int kLevels = kSK + kSX - 1;              // 23
+constexpr int kLevels = kSK + kSX - 1;              // 23 (8 groups of 3: tri.cuh kTcGroups)
+static_assert((kLevels + 2) / 3 == kTcGroups, "level groups");
 // shared layout (1024-aligned base): [kRing][kSS slices of 16 KiB] [kXJSlots][x_J] [2][x_I] barriers
 constexpr size_t kOffXJ = (size_t)kRing * kSS * kSliceBytes;
 constexpr size_t kOffXI = kOffXJ + (size_t)kXJSlots * kXBytes;
@@ -107,20 +108,13 @@ __device__ __forceinline__ void commit_elect(uint64_t *bar) {
       : "memory");
 }
 
-// 2^e for a compile-time e (exact; folded once the loops are unrolled)
-__device__ __forceinline__ double pow2c(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
-
-constexpr int kGroups = (kLevels + 2) / 3;  // 8 groups of 3 levels
-
-// One output's exact sum from its 8 x 16 slice-pair accumulators (TMEM columns base + 16 s,
-// t = 0..15), as an unrounded pair scaled by 2^escale.  Level L = s + t carries 2^(-7L);
-// three consecutive levels fold exactly into one int64 G_g = sum_{L in g} D_L 2^(7(3g+2-L))
-// (|G_g| < 2^31 * 8 * (2^14 + 2^7 + 1) < 2^48: exact in fp64), and a TwoSum chain over the
-// 8 group values G_g 2^(-7(3g+2)) gives the pair.
-__device__ __forceinline__ dd_pair combine_levels(uint32_t taddr, int escale) {
-  long long G[kGroups];
+// One output's exact level-group sums from its 8 x 16 slice-pair accumulators (TMEM
+// columns base + 16 s, t = 0..15): level L = s + t carries 2^(-7L); three consecutive
+// levels fold exactly into G_g = sum_{L in g} D_L 2^(7(3g+2-L)) (tri.cuh) -- |D_L| <= 8 *
+// 2^12 n, so |G_g| < 2^48 per contribution and for the whole row.
+__device__ __forceinline__ void level_groups(uint32_t taddr, long long (&G)[kTcGroups]) {
 #pragma unroll
-  for (int g = 0; g < kGroups; ++g) G[g] = 0;
+  for (int g = 0; g < kTcGroups; ++g) G[g] = 0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {  // two batches of 4 slices: 64 registers in flight
     uint32_t v[4][16];
@@ -135,37 +129,29 @@ __device__ __forceinline__ dd_pair combine_levels(uint32_t taddr, int escale) {
         G[L / 3] += (long long)(int32_t)v[s][t] << (7 * (2 - L % 3));
       }
   }
-  dd_pair r = {__dmul_rn((double)G[0], pow2c(-14)), 0.0};
+}
+
+// add an output's groups to the row accumulators (integer: exact whatever the order)
+__device__ __forceinline__ void red_groups(long long *yacc, int64_t ldy, int64_t i, const long long (&G)[kTcGroups]) {
 #pragma unroll
-  for (int g = 1; g < kGroups; ++g) {
-    const double t = __dmul_rn((double)G[g], pow2c(-7 * (3 * g + 2)));
-    double s, e;
-    two_sum(r.s, t, s, e);
-    r.s = s;
-    r.c = __dadd_rn(r.c, e);
-  }
-  r.s = ldexp(r.s, escale);
-  r.c = ldexp(r.c, escale);
-  return r;
+  for (int g = 0; g < kTcGroups; ++g)
+    atomicAdd(reinterpret_cast<unsigned long long *>(yacc + g * ldy + i), (unsigned long long)G[g]);
 }
 
 struct TcArgs {
-  SymvArgs t;       // partials, x, plan of the finalize
+  const PcgState *state;
+  int64_t n;
   const int64_t *toff;  // [nb + 1] first 128 x 128 tile of each block-row
   int64_t T;            // tiles
   int32_t nb;
-  const int32_t *segfirst;  // [nb] first CTA covering block-row I
-  int32_t maxseg;
-  dd_pair *rowpart;         // [nb][maxseg][128]
-  const int8_t *ks;         // the tile-major slice store
-  const int *eK;  // global exponent of K's slices (device)
-  const int *F;   // exponent of this x's slices (device, written by the slicing kernel)
+  const int8_t *ks;     // the tile-major slice store
+  long long *yacc;      // [8][ldy] exact level-group sums per row (tri.cuh)
+  int64_t ldy;
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     symv_tc_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs ta) {
-  const SymvArgs &a = ta.t;
-  if (a.state != nullptr && *(volatile int32_t *)&a.state->done) return;
+  if (ta.state != nullptr && *(volatile int32_t *)&ta.state->done) return;
   extern __shared__ unsigned char smem_raw[];
   const uint32_t base_s = smem_u32(smem_raw);
   unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);
@@ -369,7 +355,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   // ------------------------------------------------------------ epilogue (warps 2..5)
   const int q = warp & 3;  // TMEM lane quadrant this warp may access
-  const int escale = *ta.eK + *ta.F + 2 - 14;
   int I = I0;
   int64_t rend = ta.toff[I + 1];
   int rb = 0, cb = 0, nseg = 0, ncol = 0;
@@ -378,31 +363,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     while (t >= rend) rend = ta.toff[++I + 1];
     if (newI) ++nseg;
     const int J = I + (int)(t - ta.toff[I]);
-    if (J != I) {
+    if (J != I) {  // the tile's column sums K_IJ^T x_I -> rows of block J
       mbar_wait(&colf[cb], (uint32_t)((ncol >> 1) & 1));
       tc::fence_after();
+      long long G[kTcGroups];
 #if TC_EXP == 1 || TC_EXP == 4
-      const dd_pair v = {0.0, 0.0};
+      for (int g = 0; g < kTcGroups; ++g) G[g] = 0;
 #else
-      const dd_pair v = combine_levels(tmem + 256 + (uint32_t)(cb * 128) + ((uint32_t)(32 * q) << 16), escale);
+      level_groups(tmem + 256 + (uint32_t)(cb * 128) + ((uint32_t)(32 * q) << 16), G);
 #endif
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&cole[cb]);
-      const int64_t j = (int64_t)J * kT + 32 * q + lane;
-      if (j < a.n) a.colpart[(int64_t)I * a.ldcp + j] = v;
+      red_groups(ta.yacc, ta.ldy, (int64_t)J * kT + 32 * q + lane, G);
       cb ^= 1;
       ++ncol;
     }
-    if (t + 1 == t1 || t + 1 >= rend) {
+    if (t + 1 == t1 || t + 1 >= rend) {  // the segment's row sums -> rows of block I
       mbar_wait(&rowf[rb], (uint32_t)(((nseg - 1) >> 1) & 1));
       tc::fence_after();
-      const dd_pair v = combine_levels(tmem + (uint32_t)(rb * 128) + ((uint32_t)(32 * q) << 16), escale);
+      long long G[kTcGroups];
+      level_groups(tmem + (uint32_t)(rb * 128) + ((uint32_t)(32 * q) << 16), G);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&rowe[rb]);
-      const int sg = (int)blockIdx.x - ta.segfirst[I];
-      ta.rowpart[((int64_t)I * ta.maxseg + sg) * kT + 32 * q + lane] = v;
+      red_groups(ta.yacc, ta.ldy, (int64_t)I * kT + 32 * q + lane, G);
       rb ^= 1;
     }
   }
@@ -527,13 +512,12 @@ struct SymvTc {
   int8_t *ks = nullptr, *xs = nullptr;
   int *dexp = nullptr;  // [0] eK, [1] F of the last sliced x, [2] exactness flag
   double *dmax = nullptr;
+  long long *yacc = nullptr;  // [8][ldx] exact level-group sums per row (zero between applies)
   CUtensorMap tmX;
-  // the 128 x 128 tile plan for `grid` persistent CTAs (the finalize's segments)
-  int grid = 0, nb = 0, maxseg = 0;
+  // the 128 x 128 tile plan for `grid` persistent CTAs
+  int grid = 0, nb = 0;
   int64_t T = 0;
   int64_t *toff = nullptr;
-  int32_t *segfirst = nullptr, *nseg = nullptr;
-  dd_pair *rowpart = nullptr;
 };
 
 void symv_tc_free(SymvTc *&p) {
@@ -542,10 +526,8 @@ void symv_tc_free(SymvTc *&p) {
   cudaFree(p->xs);
   cudaFree(p->dexp);
   cudaFree(p->dmax);
+  cudaFree(p->yacc);
   cudaFree(p->toff);
-  cudaFree(p->segfirst);
-  cudaFree(p->nseg);
-  cudaFree(p->rowpart);
   delete p;
   p = nullptr;
 }
@@ -556,39 +538,17 @@ void symv_tc_init() {
 
 namespace {
 // block-row I takes tiles J = I .. nb - 1 (row-major order); CTA b the range
-// [T b / G, T (b + 1) / G), G = min(SMs, T); the segments of a block-row are its CTAs in order
+// [T b / G, T (b + 1) / G), G = min(SMs, T)
 cudaError_t tc_plan(SymvTc *p, int sms) {
   const int nb = (int)((p->n + kT - 1) / kT);
   std::vector<int64_t> toff(nb + 1, 0);
   for (int I = 0; I < nb; ++I) toff[I + 1] = toff[I] + (nb - I);
-  const int64_t T = toff[nb];
-  // every CTA gets at least one tile: the segments of a block-row are then consecutive CTAs
-  const int grid = (int)std::min<int64_t>(sms, T);
-  auto cta_of = [&](int64_t t) {  // the CTA whose range holds tile t
-    int64_t b = t * grid / T;
-    while (b + 1 < grid && T * (b + 1) / grid <= t) ++b;
-    while (b > 0 && T * b / grid > t) --b;
-    return (int32_t)b;
-  };
-  std::vector<int32_t> segfirst(nb), nseg(nb);
-  int maxseg = 1;
-  for (int I = 0; I < nb; ++I) {
-    segfirst[I] = cta_of(toff[I]);
-    nseg[I] = cta_of(toff[I + 1] - 1) - segfirst[I] + 1;
-    maxseg = std::max(maxseg, (int)nseg[I]);
-  }
   cudaError_t e;
   if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&p->segfirst, nb * sizeof(int32_t))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&p->nseg, nb * sizeof(int32_t))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&p->rowpart, (size_t)nb * maxseg * kT * sizeof(dd_pair))) != cudaSuccess) return e;
   cudaMemcpy(p->toff, toff.data(), toff.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(p->segfirst, segfirst.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(p->nseg, nseg.data(), nb * sizeof(int32_t), cudaMemcpyHostToDevice);
-  p->grid = grid;
   p->nb = nb;
-  p->T = T;
-  p->maxseg = maxseg;
+  p->T = toff[nb];
+  p->grid = (int)std::min<int64_t>(sms, p->T);
   return cudaSuccess;
 }
 }  // namespace
@@ -610,12 +570,14 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (tc_plan(p, sms) != cudaSuccess || cudaMalloc(&p->ks, (size_t)p->T * kSK * kSliceBytes) != cudaSuccess ||
         cudaMalloc(&p->xs, (size_t)kSX * p->ldx) != cudaSuccess || cudaMalloc(&p->dexp, 4 * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess) {
+        cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&p->yacc, (size_t)kTcGroups * p->ldx * sizeof(long long)) != cudaSuccess) {
       cudaGetLastError();
       symv_tc_free(p);
       return false;
     }
     cudaMemset(p->xs, 0, (size_t)kSX * p->ldx);
+    cudaMemset(p->yacc, 0, (size_t)kTcGroups * p->ldx * sizeof(long long));
     // x slices: [16][ldx] bytes, boxes of 128 columns x 16 slices
     cuuint64_t dx[2] = {(cuuint64_t)p->ldx, (cuuint64_t)kSX}, sx[1] = {(cuuint64_t)p->ldx};
     cuuint32_t bx[2] = {kT, kSX}, es[2] = {1, 1};
@@ -643,26 +605,25 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
   return flag == 0;
 }
 
-// the tile pass of the exact tensor-core apply: x's slices, then the tiles; the row
-// segments are this plan's, so the finalize (launched by the caller, symv.cu) reads them
+// the tile pass of the exact tensor-core apply: x's slices, then the tiles adding every
+// row's exact level groups to yacc; a's tensor-core fields point the finalize (launched by
+// the caller, symv.cu) at them
 void launch_symv_tc(SymvTc *p, SymvArgs &a, cudaStream_t s) {
   slice_x_kernel<<<(unsigned)std::min<int64_t>((p->n + 255) / 256, 296), 256, 0, s>>>(
       a.x, p->n, a.xparts, a.nxparts, p->xs, p->ldx, p->dexp + 1, a.state);
   TcArgs ta{};
-  ta.t = a;
+  ta.state = a.state;
+  ta.n = p->n;
   ta.toff = p->toff;
   ta.T = p->T;
   ta.nb = p->nb;
-  ta.segfirst = p->segfirst;
-  ta.maxseg = p->maxseg;
-  ta.rowpart = p->rowpart;
   ta.ks = p->ks;
-  ta.eK = p->dexp;
-  ta.F = p->dexp + 1;
+  ta.yacc = p->yacc;
+  ta.ldy = p->ldx;
   symv_tc_kernel<<<p->grid, kTcThreads, kTcSmem, s>>>(p->tmX, ta);
-  a.nseg = p->nseg;
-  a.maxseg = p->maxseg;
-  a.rowpart = p->rowpart;
+  a.yacc = p->yacc;
+  a.ldy = p->ldx;
+  a.tc_exp = p->dexp;
 }
 
 }  // namespace laker

@@ -54,7 +54,34 @@ struct SymvArgs {
   dd_pair *ypair;
   int64_t own0, own1;  // global rows whose row partials this rank holds
   FusedUpdate upd;     // single-rank K apply inside the PCG: the update step fused (symv.cu)
+  // the exact tensor-core apply (symv_tc.cu): per row, the 8 exact int64 level-group sums
+  // [8][ldy] accumulated by the tile kernel (integer atomics: exact, order-free), turned
+  // into the row's pair by the finalize with scale 2^(tc_exp[0] + tc_exp[1] + 2 - 14)
+  // (eK, F), which also zeroes them for the next apply
+  long long *yacc;
+  int64_t ldy;
+  const int *tc_exp;
 };
+
+// The exact tensor-core apply's level groups: group g holds levels L = 3g .. 3g + 2 as
+// G_g = sum_{L in g} D_L 2^(7(3g+2-L)), |G_g| < 2^48 (exact in fp64); the value is
+// sum_g G_g 2^(-7(3g+2)) 2^escale, folded by a TwoSum chain into an unrounded pair.
+constexpr int kTcGroups = 8;
+__device__ __forceinline__ double tc_pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+__device__ __forceinline__ dd_pair tc_groups_to_pair(const long long (&G)[kTcGroups], int escale) {
+  dd_pair r = {__dmul_rn((double)G[0], tc_pow2(-14)), 0.0};
+#pragma unroll
+  for (int g = 1; g < kTcGroups; ++g) {
+    const double t = __dmul_rn((double)G[g], tc_pow2(-7 * (3 * g + 2)));
+    double s, e;
+    two_sum(r.s, t, s, e);
+    r.s = s;
+    r.c = __dadd_rn(r.c, e);
+  }
+  r.s = ldexp(r.s, escale);
+  r.c = ldexp(r.c, escale);
+  return r;
+}
 
 // partition of an n x n symmetric apply into BR x TC tiles over `grid` CTAs
 cudaError_t tri_plan(SymvPlan *&p, int64_t n, int br, int tc, int grid);
