@@ -24,18 +24,12 @@ namespace {
 
 constexpr int kConsumers = 512;
 constexpr int kWarps = kConsumers / 32;
-#ifndef GEMV_STAGES
-#define GEMV_STAGES 3
-#endif
-#ifndef GEMV_CPT
-#define GEMV_CPT 2
-#endif
-constexpr int kStages = GEMV_STAGES;
+constexpr int kStages = 3;
 constexpr int kThreads = kConsumers + 32;
 struct Cfg {
   static constexpr int NX = 1;                  // staged vector chunks
   static constexpr int ROWS = 8;                // rows per group (stage = 9 x 8 KiB)
-  static constexpr int CPT = GEMV_CPT;          // columns per consumer thread
+  static constexpr int CPT = 2;                 // columns per consumer thread
   static constexpr int CHUNK = kConsumers * CPT;  // 1024 columns per unit
   static constexpr size_t STAGE = (size_t)(ROWS + NX) * CHUNK;
   static constexpr size_t SMEM = kStages * STAGE * sizeof(double) + 2 * kWarps * ROWS * sizeof(dd_pair) +
@@ -152,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
       const int width = (int)imin64(kChunk, ncp - col0);
       if (cb < width) {
         const double *sp = ring + slot * C::STAGE + cb;
-        if constexpr (kCPT == 2) {
+        {
           const double2 x0 = *reinterpret_cast<const double2 *>(sp + ROWS * kChunk);
           const int64_t o = own0 - (col0 + cb);  // own row indices falling in this thread's columns
           if (o > -ROWS && o < kCPT) {
@@ -167,13 +161,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_dot2_kernel(const GemvArgs a
               dot2_step(acc[r], v0.y, x0.y);
             }
           }
-        } else {
-          const double x0 = sp[ROWS * kChunk];
-          const int64_t o = own0 - (col0 + cb);
-          if (o > -ROWS && o <= 0 && -o < nr) xrow[-o] = x0;
-#pragma unroll
-          for (int r = 0; r < ROWS; ++r)
-            if (r < nr) dot2_step(acc[r], sp[r * kChunk], x0);
         }
       }
       __syncwarp();
