@@ -374,7 +374,7 @@ cudaError_t launch_igemm_epi(const int8_t *A, int64_t lda, const int8_t *B, int6
 // split into S signed 7-bit digit slices, all slice products with s + t <= S - 1
 // (0-based) accumulated exactly in int32 per digit level, levels summed in fp64.
 cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s, int kernel = -1);
-// route a GemmArgs to the Ozaki path when it is large enough to pay (LAKER_OZAKI=0 disables)
+// route a GemmArgs to the Ozaki path when it is large enough to pay
 bool ozaki_eligible(const GemmArgs &g);
 void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
                         int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf = nullptr);

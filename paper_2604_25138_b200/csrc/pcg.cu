@@ -229,12 +229,8 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   LAKER_CUDA(ctx, cudaGetLastError());
 
   const double *theta_src = (pk == LAKER_PRECOND_NONE) ? w.r : w.theta;
-  // iterations per captured graph; LAKER_PCG_CHUNK overrides (host-jitter experiments)
-  const int chunk = [&] {
-    const char *e = std::getenv("LAKER_PCG_CHUNK");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? v : (n >= 8192 ? 8 : (n >= 2048 ? 32 : 64));
-  }();
+  // iterations per captured graph (32 per chunk at C3 measured the same as 8, tools/iter_gap.py)
+  const int chunk = n >= 8192 ? 8 : (n >= 2048 ? 32 : 64);
   const bool instr = o.instrument != 0;
   std::vector<cudaEvent_t> evs;
   if (instr) {
