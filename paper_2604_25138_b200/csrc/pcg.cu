@@ -233,8 +233,11 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   const int chunk = n >= 8192 ? 8 : (n >= 2048 ? 32 : 64);
   const bool instr = o.instrument != 0;
   std::vector<cudaEvent_t> evs;
+  // instrumented: two event sets, one per captured graph, so the speculative loop below
+  // reads a finished chunk's events while the next chunk (the other graph) runs
+  const int nsets = instr ? 2 : 1;
   if (instr) {
-    evs.resize(4 * chunk);
+    evs.resize(4 * chunk * nsets);
     for (auto &e : evs) cudaEventCreate(&e);
   }
   // the update step (alpha, r, ||r||, termination) rides in the symmetric apply's finalize
@@ -250,16 +253,17 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   fu.on = 1; fu.pk = pk; fu.p = w.p; fu.alpha = w.alpha; fu.r = w.r; fu.theta = w.theta; fu.dvec = ctx->Pdiag;
   fu.hist = w.hist; fu.bar = ctx->counters + kCtrBar; fu.partials2 = ctx->partials + 2048;
   fu.counter2 = ctx->counters + kCtrUpdate;
-  auto record_iteration = [&](int j) {
-    if (instr) cudaEventRecordWithFlags(evs[4 * j + 0], s, cudaEventRecordExternal);
+  auto record_iteration = [&](int j, int set) {
+    cudaEvent_t *ev = instr ? &evs[4 * (set * chunk + j)] : nullptr;
+    if (instr) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
     launch_operator(ctx, w.p, w.q, w.st, kEpiDelta, nullptr, pmax, npmax, fuse_upd ? &fu : nullptr);
-    if (instr) cudaEventRecordWithFlags(evs[4 * j + 1], s, cudaEventRecordExternal);
+    if (instr) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
     if (!fuse_upd)
       pcg_update_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, pk, (const double *)ctx->Pdiag, (const double *)w.p, (const double *)w.q, w.alpha, w.r, w.theta, w.st, w.hist, ctx->partials, ctx->counters + kCtrUpdate);
     if (dense) {
-      if (instr) cudaEventRecordWithFlags(evs[4 * j + 2], s, cudaEventRecordExternal);
+      if (instr) cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal);
       launch_precond(ctx, w.r, w.theta, w.st, kEpiBeta, nullptr, fuse_pu ? w.p : nullptr, fuse_pu ? pmax : nullptr);
-      if (instr) cudaEventRecordWithFlags(evs[4 * j + 3], s, cudaEventRecordExternal);
+      if (instr) cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal);
     }
     if (!fuse_pu) {
       pcg_pupdate_kernel<<<dim3(vg), dim3(kVecThreads), 0, s>>>(n, theta_src, w.p, w.st, dense ? 1 : 0, pmax);
@@ -268,44 +272,65 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     if (!fuse_upd) ctx->stats.kernel_launches++;
   };
 
-  // capture one chunk into a graph
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
+  // capture one chunk into a graph (two when instrumented: one per event set)
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   const int64_t launches_before = ctx->stats.kernel_launches;
-  LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  for (int j = 0; j < chunk; ++j) record_iteration(j);
-  LAKER_CUDA(ctx, cudaStreamEndCapture(s, &graph));
-  const int64_t per_chunk = ctx->stats.kernel_launches - launches_before;
+  int64_t per_chunk = 0;
+  for (int set = 0; set < nsets; ++set) {
+    LAKER_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int j = 0; j < chunk; ++j) record_iteration(j, set);
+    LAKER_CUDA(ctx, cudaStreamEndCapture(s, &graph[set]));
+    per_chunk = (ctx->stats.kernel_launches - launches_before) / (set + 1);
+    LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec[set], graph[set], 0));
+  }
   ctx->stats.kernel_launches = launches_before;
-  LAKER_CUDA(ctx, cudaGraphInstantiate(&gexec, graph, 0));
   tmark("instantiated");
 
   // One chunk is always queued ahead of the host's check of the previous one, so the
   // GPU never idles for the state read-back + relaunch; a chunk queued after the solve
   // finished runs as early-exiting no-op kernels (every kernel tests st->done).  The
-  // instrumented run (event timings per chunk) keeps the synchronous loop.
+  // instrumented run alternates its two graphs and reads each finished chunk's events
+  // while the next one runs.
   PcgState *hs = nullptr, *hs2 = nullptr;
   LAKER_CUDA(ctx, cudaMallocHost(&hs, 2 * sizeof(PcgState)));
   hs2 = hs + 1;
   LAKER_CUDA(ctx, cudaMemcpyAsync(hs, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
   LAKER_CUDA(ctx, cudaStreamSynchronize(s));
-  int32_t iters_prev = 0;
-  if (!instr && !hs->done) {
+  int32_t iters_prev = hs->iters;
+  auto read_events = [&](int set, const PcgState *st_after) {
+    const int ran = st_after->iters - iters_prev;  // iterations whose operator pass did real work
+    for (int j = 0; j < std::min(ran, chunk); ++j) {
+      const cudaEvent_t *ev = &evs[4 * (set * chunk + j)];
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      ctx->stats.op_ms += ms;
+      ctx->stats.op_launches++;
+      if (dense && (j < ran - 1 || !st_after->done || st_after->term != LAKER_TERM_RESIDUAL_TOL)) {
+        cudaEventElapsedTime(&ms, ev[2], ev[3]);
+        ctx->stats.prec_ms += ms;
+        ctx->stats.prec_launches++;
+      }
+    }
+    iters_prev = st_after->iters;
+  };
+  if (!hs->done) {
     cudaEvent_t ce[2];
     cudaEventCreateWithFlags(&ce[0], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ce[1], cudaEventDisableTiming);
     PcgState *slot[2] = {hs, hs2};
     int cur = 0;
-    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
+    LAKER_CUDA(ctx, cudaGraphLaunch(gexec[0], s));
     ctx->stats.kernel_launches += per_chunk;
     LAKER_CUDA(ctx, cudaMemcpyAsync(slot[0], w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     cudaEventRecord(ce[0], s);
     for (;;) {
-      LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));  // speculative next chunk
+      LAKER_CUDA(ctx, cudaGraphLaunch(gexec[(cur ^ 1) % nsets], s));  // speculative next chunk
       ctx->stats.kernel_launches += per_chunk;
       LAKER_CUDA(ctx, cudaMemcpyAsync(slot[cur ^ 1], w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       cudaEventRecord(ce[cur ^ 1], s);
       LAKER_CUDA(ctx, cudaEventSynchronize(ce[cur]));
+      if (instr) read_events(cur, slot[cur]);
       if (slot[cur]->done) break;
       cur ^= 1;
     }
@@ -313,27 +338,6 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
     *hs = *slot[cur ^ 1];  // the state after the last queued chunk (== final state)
     cudaEventDestroy(ce[0]);
     cudaEventDestroy(ce[1]);
-  }
-  while (!hs->done) {
-    LAKER_CUDA(ctx, cudaGraphLaunch(gexec, s));
-    ctx->stats.kernel_launches += per_chunk;
-    LAKER_CUDA(ctx, cudaMemcpyAsync(hs, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
-    if (instr) {
-      const int ran = hs->iters - iters_prev;  // iterations whose operator pass did real work
-      for (int j = 0; j < std::min(ran, chunk); ++j) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, evs[4 * j + 0], evs[4 * j + 1]);
-        ctx->stats.op_ms += ms;
-        ctx->stats.op_launches++;
-        if (dense && (j < ran - 1 || !hs->done || hs->term != LAKER_TERM_RESIDUAL_TOL)) {
-          cudaEventElapsedTime(&ms, evs[4 * j + 2], evs[4 * j + 3]);
-          ctx->stats.prec_ms += ms;
-          ctx->stats.prec_launches++;
-        }
-      }
-    }
-    iters_prev = hs->iters;
   }
   cudaEventRecord(ev1, s);
   tmark("loop done");
@@ -375,8 +379,10 @@ laker_status pcg_solve_device(laker_ctx ctx, const double *y, double *alpha_out,
   for (auto &e : evs) cudaEventDestroy(e);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
-  cudaGraphExecDestroy(gexec);
-  cudaGraphDestroy(graph);
+  for (int set = 0; set < nsets; ++set) {
+    cudaGraphExecDestroy(gexec[set]);
+    cudaGraphDestroy(graph[set]);
+  }
   cudaFreeAsync(w.alpha, s);
   cudaFreeAsync(w.hist, s);
   tmark("destroyed");
