@@ -262,6 +262,13 @@ laker_status laker_debug_dist_tiles(int64_t n, int32_t br, int32_t tc, int32_t r
 laker_status laker_debug_dist_symv_partials(laker_ctx ctx, const double *x, const double *rowmax, double *pairs);
 laker_status laker_debug_dist_symv_combine(laker_ctx ctx, const double *x, const double *own, const double *recv,
                                            double *q_loc, double *pq_pair);
+/* Test hook of the exact tensor-core K apply (B13; symv_tc.cu): on a context whose
+   K uses it (stats.k_tensor_core; one rank, or a shard of the sharded plan -- detached
+   shards included), x (n) -> groups (8 n int64, [g][i]): this rank's exact level-group sums
+   G_g of every row i (tri.cuh), before any cross-rank sum; the shards' groups add up, as
+   integers, to the one-rank groups.  rowmax (n, may be NULL) replaces the row maxima a
+   detached shard cannot all-gather (it fixes K's slice exponent).  Synchronous. */
+laker_status laker_debug_tc_groups(laker_ctx ctx, const double *x, const double *rowmax, int64_t *groups);
 
 typedef struct {
   int64_t n, local_rows, ld;     /* problem size, rows held, padded row stride (doubles) */

@@ -50,6 +50,27 @@ laker_status refresh_symmetry(laker_ctx ctx, int which, bool symmetric_rows) {
     }
     LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     flag = true;
+    // the exact tensor-core tiles (B13) on this rank's tiles of the sharded plan, used only
+    // if every rank's entries are exact in the slice form (all ranks take the same path);
+    // a detached shard (no communicator, tests) decides alone
+    const char *tenv = std::getenv("LAKER_SYMV_TC");
+    if (!(tenv && tenv[0] == '0') && ctx->comm) {
+      int ok = symv_tc_prepare(ctx->symv_tc, A, ctx->n, ctx->ld, symv_rowmax_ptr(ctx->symv, 0), ctx->stream, ctx->rank,
+                               ctx->world) ? 1 : 0;
+      cudaGetLastError();
+      int *dok = reinterpret_cast<int *>(ctx->flags + 2);
+      LAKER_CUDA(ctx, cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+      LAKER_NCCL(ctx, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream));
+      LAKER_CUDA(ctx, cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      ctx->k_tc = ok == 1;
+      ctx->stats.kernel_launches += 2;
+    } else if (!(tenv && tenv[0] == '0')) {
+      ctx->k_tc = symv_tc_prepare(ctx->symv_tc, A, ctx->n, ctx->ld, symv_rowmax_ptr(ctx->symv, 0), ctx->stream,
+                                  ctx->rank, ctx->world);
+      cudaGetLastError();
+      ctx->stats.kernel_launches += 2;
+    }
     return LAKER_OK;
   }
   LAKER_CUDA(ctx, symv_plan(ctx->symv, ctx->n, ctx->ld, ctx->num_sms));
@@ -73,7 +94,7 @@ laker_status refresh_symmetry(laker_ctx ctx, int which, bool symmetric_rows) {
     // digit slices with one exponent; LAKER_SYMV_TC=0 keeps the fp64 kernel (A/B)
     const char *tenv = std::getenv("LAKER_SYMV_TC");
     if (flag && !(tenv && tenv[0] == '0')) {
-      ctx->k_tc = symv_tc_prepare(ctx->symv_tc, A, ctx->n, ctx->ld, symv_rowmax_ptr(ctx->symv, 0), ctx->stream);
+      ctx->k_tc = symv_tc_prepare(ctx->symv_tc, A, ctx->n, ctx->ld, symv_rowmax_ptr(ctx->symv, 0), ctx->stream, 0, 1);
       ctx->stats.kernel_launches += 2;
       cudaGetLastError();
     }

@@ -256,7 +256,11 @@ void symv_tc_init();
 void symv_tc_free(SymvTc *&p);
 // slice K (n x n, stride ld, bitwise symmetric) into 8 int8 digit slices with one global
 // exponent; false if not every entry is exact in that form
-bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const double *rowmax, cudaStream_t s);
+bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const double *rowmax, cudaStream_t s,
+                     int rank = 0, int world = 1);
+// the [W][8][cs] exact level-group accumulators (cs: rows per chunk) and {eK, F} of the last apply
+long long *symv_tc_groups(SymvTc *p, int64_t *cs);
+const int *symv_tc_exponents(const SymvTc *p);
 // ------------------------------------------------------------- otf_sym.cu
 void otf_sym_init();
 cudaError_t otf_sym_prepare(laker_ctx ctx);

@@ -253,20 +253,34 @@ __global__ void __launch_bounds__(kVecThreads) local_pair_kernel(int64_t n, cons
 // ranks w - 1, ..., w - D (in that order) + lambda p_i) -- the row's partials summed
 // unrounded and rounded once, as symv_finalize_kernel does on one rank; the unrounded
 // Dot2 pair p_loc.q_loc -> pair_out (last block).
+// own rows of the sharded symmetric apply: q_i = RN(row pair + lambda p_i) and the Dot2
+// pair p_loc.q_loc.  fp64 tiles: the row pair is this rank's pair plus the D received pairs
+// in rank order; tensor-core tiles (yg != null): the pair of the row's 8 exact level groups,
+// already summed over all ranks by the integer reduce-scatter ([8][nloc], tri.cuh).
 __global__ void __launch_bounds__(kVecThreads) symv_combine_kernel(
     int64_t nloc, int64_t r0, const dd_pair *__restrict__ own, const dd_pair *__restrict__ recv, int D,
     double lambda, const double *__restrict__ p_full, double *__restrict__ q_loc, const PcgState *st,
-    dd_pair *partials, unsigned int *counter, double *pair_out) {
+    dd_pair *partials, unsigned int *counter, double *pair_out, const long long *__restrict__ yg,
+    const int *tc_exp) {
   if (st && *(volatile const int32_t *)&st->done) return;
   __shared__ dd_pair sred[kVecThreads / 32];
   __shared__ int s_last;
   dd_pair v = {0.0, 0.0};
+  const int escale = yg != nullptr ? tc_exp[0] + tc_exp[1] + 2 - 14 : 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += (int64_t)gridDim.x * blockDim.x) {
-    const double2 o = __ldcg(reinterpret_cast<const double2 *>(own + i));
-    dd_pair t = {o.x, o.y};
-    for (int d = 0; d < D; ++d) {
-      const double2 r = __ldcg(reinterpret_cast<const double2 *>(recv + (int64_t)d * nloc + i));
-      pair_add(t, dd_pair{r.x, r.y});
+    dd_pair t;
+    if (yg != nullptr) {
+      long long G[kTcGroups];
+#pragma unroll
+      for (int g = 0; g < kTcGroups; ++g) G[g] = __ldcg(&yg[g * nloc + i]);
+      t = tc_groups_to_pair(G, escale);
+    } else {
+      const double2 o = __ldcg(reinterpret_cast<const double2 *>(own + i));
+      t = dd_pair{o.x, o.y};
+      for (int d = 0; d < D; ++d) {
+        const double2 r = __ldcg(reinterpret_cast<const double2 *>(recv + (int64_t)d * nloc + i));
+        pair_add(t, dd_pair{r.x, r.y});
+      }
     }
     const double pi = p_full[r0 + i];
     if (lambda != 0.0) dot2_step(t, lambda, pi);
@@ -352,6 +366,7 @@ laker_status dist_sync(laker_ctx ctx, cudaStream_t s) {
 // pairs received for its rows from ranks w - 1 .. w - D
 struct SymvDistBufs {
   dd_pair *ypair = nullptr, *recv = nullptr;
+  long long *yown = nullptr;  // tensor-core tiles: this rank's [8][nloc] groups after the reduce-scatter
 };
 
 // Sharded symmetric K (tri_plan_dist, symv.cu): this rank's tiles -> row pairs of all n
@@ -363,6 +378,32 @@ static laker_status symv_dist_apply(laker_ctx ctx, const double *p_full, double 
                                     double *pair_out, const SymvDistBufs &b, laker_status &err) {
   const int64_t nloc = ctx->r1 - ctx->r0;
   const int W = ctx->world, w = ctx->rank, D = dist_nsend(W);
+  const int g = (int)std::min<int64_t>(2 * ctx->num_sms, (nloc + kVecThreads - 1) / kVecThreads);
+  if (ctx->k_tc && b.yown) {
+    // tensor-core tiles (symv_tc.cu, B13): every row's exact level groups from this rank's
+    // tiles, summed over the ranks by an int64 reduce-scatter (exact, order-free: the
+    // reduce-scatter of the transposed contributions), then rounded once per own row
+    GemvArgs a{};
+    a.x = p_full; a.state = st; a.evict_first = true; a.tc = ctx->symv_tc;
+    launch_symv(ctx->symv, 0, a, ctx->stream);
+    ctx->stats.kernel_launches += 2;
+    int64_t cs = 0;
+    long long *yacc = symv_tc_groups(ctx->symv_tc, &cs);
+    if (ctx->comm) {
+      if (ncclReduceScatter(yacc, b.yown, (size_t)kTcGroups * nloc, ncclInt64, ncclSum, ctx->comm, ctx->stream) !=
+          ncclSuccess)
+        err = LAKER_ERR_NCCL;
+    } else {  // detached shard (tests): its own contributions only
+      cudaMemcpyAsync(b.yown, yacc + (int64_t)w * kTcGroups * nloc, (size_t)kTcGroups * nloc * sizeof(long long),
+                      cudaMemcpyDeviceToDevice, ctx->stream);
+    }
+    cudaMemsetAsync(yacc, 0, (size_t)kTcGroups * ctx->n * sizeof(long long), ctx->stream);
+    symv_combine_kernel<<<g, kVecThreads, 0, ctx->stream>>>(nloc, ctx->r0, nullptr, nullptr, 0, ctx->lambda, p_full,
+                                                            q_loc, st, ctx->partials, ctx->counters + kCtrMisc,
+                                                            pair_out, b.yown, symv_tc_exponents(ctx->symv_tc));
+    ctx->stats.kernel_launches++;
+    return err;
+  }
   GemvArgs a{};
   a.x = p_full; a.state = st; a.evict_first = true; a.ypair = b.ypair;
   launch_symv(ctx->symv, 0, a, ctx->stream);
@@ -377,10 +418,10 @@ static laker_status symv_dist_apply(laker_ctx ctx, const double *p_full, double 
     }
     if (ncclGroupEnd() != ncclSuccess) err = LAKER_ERR_NCCL;
   }
-  const int g = (int)std::min<int64_t>(2 * ctx->num_sms, (nloc + kVecThreads - 1) / kVecThreads);
   symv_combine_kernel<<<g, kVecThreads, 0, ctx->stream>>>(nloc, ctx->r0, b.ypair + ctx->r0, b.recv,
                                                           ctx->comm ? D : 0, ctx->lambda, p_full, q_loc, st,
-                                                          ctx->partials, ctx->counters + kCtrMisc, pair_out);
+                                                          ctx->partials, ctx->counters + kCtrMisc, pair_out,
+                                                          nullptr, nullptr);
   return err;
 }
 
@@ -390,6 +431,8 @@ static laker_status symv_dist_alloc(laker_ctx ctx, SymvDistBufs &b) {
   LAKER_CUDA(ctx, cudaMallocAsync(&b.ypair, ((size_t)ctx->n + (size_t)std::max(D, 1) * nloc) * sizeof(dd_pair),
                                   ctx->stream));
   b.recv = b.ypair + ctx->n;
+  if (ctx->k_tc)
+    LAKER_CUDA(ctx, cudaMallocAsync(&b.yown, (size_t)kTcGroups * nloc * sizeof(long long), ctx->stream));
   return LAKER_OK;
 }
 
@@ -441,6 +484,7 @@ laker_status apply_operator_dist(laker_ctx ctx, const double *x, double *y) {
   cudaFreeAsync(xp, s);
   cudaFreeAsync(ql, s);
   if (sb.ypair) cudaFreeAsync(sb.ypair, s);
+  if (sb.yown) cudaFreeAsync(sb.yown, s);
   return LAKER_OK;
 }
 
@@ -718,6 +762,7 @@ laker_status pcg_solve_dist(laker_ctx ctx, const double *y, double *alpha_out, c
   cudaGraphDestroy(graph);
   cudaFreeAsync(base, s);
   if (sb.ypair) cudaFreeAsync(sb.ypair, s);
+  if (sb.yown) cudaFreeAsync(sb.yown, s);
   cudaFreeAsync(st, s);
   cudaFreeAsync(hist, s);
   LAKER_CUDA(ctx, cudaStreamSynchronize(s));
@@ -796,11 +841,56 @@ extern "C" laker_status laker_debug_dist_symv_combine(laker_ctx ctx, const doubl
   symv_combine_kernel<<<g, kVecThreads, 0, s>>>(nloc, ctx->r0, reinterpret_cast<const dd_pair *>(buf),
                                                 reinterpret_cast<const dd_pair *>(buf + 2 * nloc), recv ? D : 0,
                                                 ctx->lambda, xp, q, nullptr, ctx->partials, ctx->counters + kCtrMisc,
-                                                q + nloc);
+                                                q + nloc, nullptr, nullptr);
   LAKER_CUDA(ctx, cudaMemcpyAsync(q_loc, q, nloc * sizeof(double), cudaMemcpyDefault, s));
   if (pq_pair) LAKER_CUDA(ctx, cudaMemcpyAsync(pq_pair, q + nloc, 2 * sizeof(double), cudaMemcpyDefault, s));
   LAKER_CUDA(ctx, cudaStreamSynchronize(s));
   cudaFree(xp);
   cudaFree(buf);
+  return LAKER_OK;
+}
+
+extern "C" laker_status laker_debug_tc_groups(laker_ctx ctx, const double *x, const double *rowmax, int64_t *groups) {
+  using namespace laker;
+  if (!ctx || !x || !groups) return LAKER_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  if (!ctx->k_sym || ctx->storage != LAKER_STORE_MATERIALIZED)
+    return set_err(ctx, LAKER_ERR_NOT_READY, "no symmetric stored K");
+  if (rowmax) {  // the full row maxima -> the global slice exponent of K (re-slices this rank's tiles)
+    LAKER_TRY(copy_in(ctx, symv_rowmax_ptr(ctx->symv, 0), rowmax, ctx->n));
+    ctx->k_tc = symv_tc_prepare(ctx->symv_tc, ctx->K, ctx->n, ctx->ld, symv_rowmax_ptr(ctx->symv, 0), s, ctx->rank,
+                                ctx->world);
+  }
+  if (!ctx->k_tc) return set_err(ctx, LAKER_ERR_NOT_READY, "K does not use the tensor-core apply");
+  const int64_t n = ctx->n;
+  std::vector<double> hx(n);
+  LAKER_CUDA(ctx, cudaMemcpy(hx.data(), x, n * sizeof(double), cudaMemcpyDefault));
+  double xm = 0.0;
+  for (double v : hx) xm = std::max(xm, std::fabs(v));
+  double *xp = nullptr;
+  LAKER_CUDA(ctx, cudaMallocAsync(&xp, (ctx->ld + 1) * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(xp, 0, ctx->ld * sizeof(double), s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(xp, hx.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+  LAKER_CUDA(ctx, cudaMemcpyAsync(xp + ctx->ld, &xm, sizeof(double), cudaMemcpyHostToDevice, s));
+  SymvArgs a{};
+  a.x = xp;
+  a.xparts = xp + ctx->ld;  // max |x| as the single per-CTA part
+  a.nxparts = 1;
+  launch_symv_tc(ctx->symv_tc, a, s);
+  int64_t cs = 0;
+  long long *yacc = symv_tc_groups(ctx->symv_tc, &cs);
+  const int64_t chunks = (ctx->world == 1) ? 1 : ctx->world;
+  std::vector<long long> h((size_t)chunks * kTcGroups * cs);
+  LAKER_CUDA(ctx, cudaMemcpyAsync(h.data(), yacc, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  LAKER_CUDA(ctx, cudaMemsetAsync(yacc, 0, h.size() * sizeof(long long), s));
+  LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+  cudaFree(xp);
+  std::vector<int64_t> out((size_t)kTcGroups * n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t c = i / cs;
+    for (int g = 0; g < kTcGroups; ++g) out[(size_t)g * n + i] = h[(size_t)(c * kTcGroups + g) * cs + (i - c * cs)];
+  }
+  LAKER_CUDA(ctx, cudaMemcpy(groups, out.data(), out.size() * sizeof(int64_t), cudaMemcpyDefault));
   return LAKER_OK;
 }

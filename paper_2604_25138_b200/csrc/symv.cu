@@ -966,10 +966,11 @@ void launch_symv(const SymvPlan *p, int which, const GemvArgs &g, cudaStream_t s
   }
   a.ypair = g.ypair;
   a.upd = g.upd;
-  const bool tc = g.tc != nullptr && which == 0 && !p->dist;
-  if (tc)
+  const bool tc = g.tc != nullptr && which == 0;
+  if (tc) {
     launch_symv_tc(g.tc, a, s);
-  else if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
+    if (p->dist) return;  // the sharded apply reduce-scatters the groups and combines (pcg_dist.cu)
+  } else if ((int64_t)p->nct * kCPT <= kMaxOffTiles)
     symv_dot2_kernel<true><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);
   else
     symv_dot2_kernel<false><<<dim3(p->grid), dim3(kSymThreads), kSymSmem, s>>>(p->tm[which], a);

@@ -131,23 +131,33 @@ __device__ __forceinline__ void level_groups(uint32_t taddr, long long (&G)[kTcG
   }
 }
 
-// add an output's groups to the row accumulators (integer: exact whatever the order)
-__device__ __forceinline__ void red_groups(long long *yacc, int64_t ldy, int64_t i, const long long (&G)[kTcGroups]) {
+// add an output's groups to row i's accumulators (integer: exact whatever the order).
+// Layout [W][8][cs]: the rows of rank c's shard (cs = n / W rows; one rank: cs = the padded
+// n) are the contiguous block c, so the sharded apply reduce-scatters it as it stands.
+__device__ __forceinline__ void red_groups(long long *yacc, int64_t cs, int64_t i, const long long (&G)[kTcGroups]) {
+  const int64_t c = i / cs;
+  long long *base = yacc + c * kTcGroups * cs + (i - c * cs);
 #pragma unroll
   for (int g = 0; g < kTcGroups; ++g)
-    atomicAdd(reinterpret_cast<unsigned long long *>(yacc + g * ldy + i), (unsigned long long)G[g]);
+    atomicAdd(reinterpret_cast<unsigned long long *>(base + g * cs), (unsigned long long)G[g]);
 }
 
 struct TcArgs {
   const PcgState *state;
   int64_t n;
-  const int64_t *toff;  // [nb + 1] first 128 x 128 tile of each block-row
+  const int64_t *toff;  // [nb + 1] first 128 x 128 tile of each (local) block-row
+  const int32_t *jt;    // sharded plan: the column block of every tile (null: J = I0 + I ..)
+  int32_t I0;           // global index of local block-row 0
   int64_t T;            // tiles
   int32_t nb;
   const int8_t *ks;     // the tile-major slice store
-  long long *yacc;      // [8][ldy] exact level-group sums per row (tri.cuh)
-  int64_t ldy;
+  long long *yacc;      // [W][8][cs] exact level-group sums per row (tri.cuh, red_groups)
+  int64_t cs;
 };
+
+__device__ __forceinline__ int tile_col(const TcArgs &ta, int I, int64_t t) {
+  return ta.jt != nullptr ? ta.jt[t] : ta.I0 + I + (int)(t - ta.toff[I]);
+}
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     symv_tc_kernel(const __grid_constant__ CUtensorMap tmX, const TcArgs ta) {
@@ -210,11 +220,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int64_t t = t0; t < t1; ++t) {
         const bool newI = (t == t0) || (t >= rend);
         while (t >= rend) rend = ta.toff[++I + 1];
-        const int J = I + (int)(t - ta.toff[I]);
+        const int J = tile_col(ta, I, t);
         if (newI) {
           if (nseg >= 2) mbar_wait(&xie[xb], (uint32_t)(((nseg - 2) >> 1) & 1));
           mbar_arrive_expect_tx(&xif[xb], kXBytes);
-          tc::tma_load_2d(sXI + xb * kXBytes, &tmX, I * kT, 0, &xif[xb]);
+          tc::tma_load_2d(sXI + xb * kXBytes, &tmX, (ta.I0 + I) * kT, 0, &xif[xb]);
           xb ^= 1;
           ++nseg;
         }
@@ -269,8 +279,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     for (int64_t t = t0; t < t1; ++t) {
       const bool newI = (t == t0) || (t >= rend);
       while (t >= rend) rend = ta.toff[++I + 1];
-      const int J = I + (int)(t - ta.toff[I]);
-      const bool off = J != I;  // off the diagonal block: the column product too
+      const int J = tile_col(ta, I, t);
+      const bool off = J != ta.I0 + I;  // off the diagonal block: the column product too
       if (newI) {
         if (rows) {
           if (nseg >= 2) mbar_wait(&rowe[rb], (uint32_t)(((nseg - 2) >> 1) & 1));  // row buffer drained
@@ -362,8 +372,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const bool newI = (t == t0) || (t >= rend);
     while (t >= rend) rend = ta.toff[++I + 1];
     if (newI) ++nseg;
-    const int J = I + (int)(t - ta.toff[I]);
-    if (J != I) {  // the tile's column sums K_IJ^T x_I -> rows of block J
+    const int J = tile_col(ta, I, t);
+    if (J != ta.I0 + I) {  // the tile's column sums K_IJ^T x_I -> rows of block J
       mbar_wait(&colf[cb], (uint32_t)((ncol >> 1) & 1));
       tc::fence_after();
       long long G[kTcGroups];
@@ -375,7 +385,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&cole[cb]);
-      red_groups(ta.yacc, ta.ldy, (int64_t)J * kT + 32 * q + lane, G);
+      red_groups(ta.yacc, ta.cs, (int64_t)J * kT + 32 * q + lane, G);
       cb ^= 1;
       ++ncol;
     }
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&rowe[rb]);
-      red_groups(ta.yacc, ta.ldy, (int64_t)I * kT + 32 * q + lane, G);
+      red_groups(ta.yacc, ta.cs, (int64_t)(ta.I0 + I) * kT + 32 * q + lane, G);
       rb ^= 1;
     }
   }
@@ -435,12 +445,14 @@ __global__ void __launch_bounds__(256) slice_x_kernel(const double *__restrict__
 // one ring slot before the SWIZZLE_64B the TMA applies.  eK: max |K| < 2^eK; flag[0] = 1
 // if some entry is not exact.  Block: one tile; thread: 8 consecutive columns of a row per
 // item, 8-byte stores.
-__global__ void __launch_bounds__(256) slice_k_kernel(const double *__restrict__ K, int64_t n, int64_t ld,
-                                                      const int64_t *__restrict__ toff, int nb, int eK,
+__global__ void __launch_bounds__(256) slice_k_kernel(const double *__restrict__ K, int64_t rows, int64_t n,
+                                                      int64_t ld, const int64_t *__restrict__ toff,
+                                                      const int32_t *__restrict__ jt, int nb, int eK,
                                                       int8_t *__restrict__ ks, int *flag) {
+  // K: this rank's rows (local block-row I = rows 128 I ..), all n columns
   const int64_t t = blockIdx.x;
   const int I = find_block_row(toff, nb, t);
-  const int J = I + (int)(t - toff[I]);
+  const int J = jt != nullptr ? jt[t] : I + (int)(t - toff[I]);
   const double sc = ldexp(1.0, -(eK + 1));
   bool bad = false;
 #pragma unroll 1
@@ -450,7 +462,7 @@ __global__ void __launch_bounds__(256) slice_k_kernel(const double *__restrict__
     unsigned long long w[kSK];
 #pragma unroll
     for (int q = 0; q < kSK; ++q) w[q] = 0ull;
-    if (i < n) {
+    if (i < rows) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (j0 + k >= n) break;
@@ -509,15 +521,18 @@ PFN_enc get_enc() {
 
 struct SymvTc {
   int64_t n = 0, ldx = 0;
+  int rank = 0, world = 1;
+  int64_t rows = 0, cs = 0;   // this rank's K rows (n / W); yacc chunk per rank (one rank: ldx)
   int8_t *ks = nullptr, *xs = nullptr;
   int *dexp = nullptr;  // [0] eK, [1] F of the last sliced x, [2] exactness flag
   double *dmax = nullptr;
-  long long *yacc = nullptr;  // [8][ldx] exact level-group sums per row (zero between applies)
+  long long *yacc = nullptr;  // [W][8][cs] exact level-group sums per row (zero between applies)
   CUtensorMap tmX;
-  // the 128 x 128 tile plan for `grid` persistent CTAs
-  int grid = 0, nb = 0;
+  // the 128 x 128 tile plan for `grid` persistent CTAs (sharded: dist_tiles, jt per tile)
+  int grid = 0, nb = 0, I0 = 0;
   int64_t T = 0;
   int64_t *toff = nullptr;
+  int32_t *jt = nullptr;
 };
 
 void symv_tc_free(SymvTc *&p) {
@@ -528,6 +543,7 @@ void symv_tc_free(SymvTc *&p) {
   cudaFree(p->dmax);
   cudaFree(p->yacc);
   cudaFree(p->toff);
+  cudaFree(p->jt);
   delete p;
   p = nullptr;
 }
@@ -536,48 +552,78 @@ void symv_tc_init() {
   cudaFuncSetAttribute(symv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
 }
 
+long long *symv_tc_groups(SymvTc *p, int64_t *cs) {
+  if (cs) *cs = p->cs;
+  return p->yacc;
+}
+const int *symv_tc_exponents(const SymvTc *p) { return p->dexp; }
+
 namespace {
-// block-row I takes tiles J = I .. nb - 1 (row-major order); CTA b the range
-// [T b / G, T (b + 1) / G), G = min(SMs, T)
+// One rank: block-row I takes tiles J = I .. nb - 1 (row-major order).  Sharded (rank r of
+// W): the local block-rows' tile lists of dist_tiles (symv.cu; every pair of symmetric
+// entries once over all ranks, n^2 / (2 W) entries per rank) at 128 x 128.  CTA b takes the
+// range [T b / G, T (b + 1) / G), G = min(SMs, T).
 cudaError_t tc_plan(SymvTc *p, int sms) {
-  const int nb = (int)((p->n + kT - 1) / kT);
-  std::vector<int64_t> toff(nb + 1, 0);
-  for (int I = 0; I < nb; ++I) toff[I + 1] = toff[I] + (nb - I);
+  std::vector<int64_t> toff;
+  std::vector<int32_t> jt;
+  if (p->world == 1) {
+    const int nb = (int)((p->n + kT - 1) / kT);
+    toff.assign(nb + 1, 0);
+    for (int I = 0; I < nb; ++I) toff[I + 1] = toff[I] + (nb - I);
+    p->I0 = 0;
+  } else {
+    std::vector<int32_t> lo, hi;
+    if (!dist_tiles(p->n, kT, kT, p->rank, p->world, toff, jt, lo, hi)) return cudaErrorInvalidValue;
+    p->I0 = (int)(p->rank * (p->rows / kT));
+  }
+  const int nb = (int)toff.size() - 1;
   cudaError_t e;
   if ((e = cudaMalloc(&p->toff, toff.size() * sizeof(int64_t))) != cudaSuccess) return e;
   cudaMemcpy(p->toff, toff.data(), toff.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (!jt.empty()) {
+    if ((e = cudaMalloc(&p->jt, jt.size() * sizeof(int32_t))) != cudaSuccess) return e;
+    cudaMemcpy(p->jt, jt.data(), jt.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  }
   p->nb = nb;
   p->T = toff[nb];
-  p->grid = (int)std::min<int64_t>(sms, p->T);
+  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, p->T));
   return cudaSuccess;
 }
 }  // namespace
 
-// Slice the (bitwise symmetric, single-rank) K into the int8 form; false if some entry is
-// not exactly representable (the fp64 symmetric kernel stays in use then)
-bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const double *rowmax, cudaStream_t s) {
+// Slice this rank's rows of the (bitwise symmetric) K into the int8 form of its tiles; false
+// if some entry is not exactly representable (the fp64 symmetric kernel stays in use then;
+// sharded callers agree on the outcome across ranks).  rowmax: the maxima of all n rows.
+bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const double *rowmax, cudaStream_t s,
+                     int rank, int world) {
   if (n < 1 || n > (1 << 18)) return false;  // |D_st| <= 64 * 64 * n < 2^31 in the int32 accumulators
+  if (world > 1 && (n % world != 0 || (n / world) % (2 * kT) != 0)) return false;  // the dist_tiles shards
   PFN_enc enc = get_enc();
   if (!enc) return false;
   const int64_t ldx = (n + kT - 1) / kT * kT;
-  if (!p || p->n != n) {
+  if (!p || p->n != n || p->rank != rank || p->world != world) {
     symv_tc_free(p);
     p = new SymvTc();
     p->n = n;
     p->ldx = ldx;
+    p->rank = rank;
+    p->world = world;
+    p->rows = n / world;
+    p->cs = world == 1 ? ldx : n / world;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t ygroups = (size_t)kTcGroups * (world == 1 ? ldx : n);
     if (tc_plan(p, sms) != cudaSuccess || cudaMalloc(&p->ks, (size_t)p->T * kSK * kSliceBytes) != cudaSuccess ||
         cudaMalloc(&p->xs, (size_t)kSX * p->ldx) != cudaSuccess || cudaMalloc(&p->dexp, 4 * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&p->dmax, sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&p->yacc, (size_t)kTcGroups * p->ldx * sizeof(long long)) != cudaSuccess) {
+        cudaMalloc(&p->yacc, ygroups * sizeof(long long)) != cudaSuccess) {
       cudaGetLastError();
       symv_tc_free(p);
       return false;
     }
     cudaMemset(p->xs, 0, (size_t)kSX * p->ldx);
-    cudaMemset(p->yacc, 0, (size_t)kTcGroups * p->ldx * sizeof(long long));
+    cudaMemset(p->yacc, 0, ygroups * sizeof(long long));
     // x slices: [16][ldx] bytes, boxes of 128 columns x 16 slices
     cuuint64_t dx[2] = {(cuuint64_t)p->ldx, (cuuint64_t)kSX}, sx[1] = {(cuuint64_t)p->ldx};
     cuuint32_t bx[2] = {kT, kSX}, es[2] = {1, 1};
@@ -598,7 +644,7 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
   std::frexp(hmax, &eK);
   int hexp[3] = {eK, 0, 0};
   cudaMemcpyAsync(p->dexp, hexp, 3 * sizeof(int), cudaMemcpyHostToDevice, s);
-  slice_k_kernel<<<(unsigned)p->T, 256, 0, s>>>(K, n, ld, p->toff, p->nb, eK, p->ks, p->dexp + 2);
+  slice_k_kernel<<<(unsigned)p->T, 256, 0, s>>>(K, p->rows, n, ld, p->toff, p->jt, p->nb, eK, p->ks, p->dexp + 2);
   int flag = 1;
   cudaMemcpyAsync(&flag, p->dexp + 2, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return false;
@@ -607,7 +653,7 @@ bool symv_tc_prepare(SymvTc *&p, const double *K, int64_t n, int64_t ld, const d
 
 // the tile pass of the exact tensor-core apply: x's slices, then the tiles adding every
 // row's exact level groups to yacc; a's tensor-core fields point the finalize (launched by
-// the caller, symv.cu) at them
+// the caller: symv.cu on one rank, pcg_dist.cu after the reduce-scatter) at them
 void launch_symv_tc(SymvTc *p, SymvArgs &a, cudaStream_t s) {
   slice_x_kernel<<<(unsigned)std::min<int64_t>((p->n + 255) / 256, 296), 256, 0, s>>>(
       a.x, p->n, a.xparts, a.nxparts, p->xs, p->ldx, p->dexp + 1, a.state);
@@ -615,14 +661,16 @@ void launch_symv_tc(SymvTc *p, SymvArgs &a, cudaStream_t s) {
   ta.state = a.state;
   ta.n = p->n;
   ta.toff = p->toff;
+  ta.jt = p->jt;
+  ta.I0 = p->I0;
   ta.T = p->T;
   ta.nb = p->nb;
   ta.ks = p->ks;
   ta.yacc = p->yacc;
-  ta.ldy = p->ldx;
+  ta.cs = p->cs;
   symv_tc_kernel<<<p->grid, kTcThreads, kTcSmem, s>>>(p->tmX, ta);
   a.yacc = p->yacc;
-  a.ldy = p->ldx;
+  a.ldy = p->cs;
   a.tc_exp = p->dexp;
 }
 

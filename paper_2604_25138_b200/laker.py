@@ -39,7 +39,7 @@ EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_statu
             "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_get_preconditioner_qm",
             "laker_apply_operator",
             "laker_get_stats", "laker_debug_igemm_s8", "laker_debug_ozaki_gemm", "laker_debug_dist_tiles",
-            "laker_debug_dist_symv_partials", "laker_debug_dist_symv_combine"]
+            "laker_debug_dist_symv_partials", "laker_debug_dist_symv_combine", "laker_debug_tc_groups"]
 
 
 class LakerError(RuntimeError):
@@ -113,6 +113,7 @@ def _load() -> ctypes.CDLL:
         "laker_debug_dist_tiles": [i64, i32, i32, i32, i32, vp, vp, vp, vp, vp],
         "laker_debug_dist_symv_partials": [vp, vp, vp, vp],
         "laker_debug_dist_symv_combine": [vp, vp, vp, vp, vp, vp],
+        "laker_debug_tc_groups": [vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -290,6 +291,10 @@ def laker_debug_dist_symv_partials(ctx, x, rowmax, pairs):
 
 def laker_debug_dist_symv_combine(ctx, x, own, recv, q_loc, pq_pair=None):
     _check(ctx, lib.laker_debug_dist_symv_combine(ctx, _ptr(x), _ptr(own), _ptr(recv), _ptr(q_loc), _ptr(pq_pair)))
+
+
+def laker_debug_tc_groups(ctx, x, rowmax, groups):
+    _check(ctx, lib.laker_debug_tc_groups(ctx, _ptr(x), _ptr(rowmax), _ptr(groups, np.int64)))
 
 
 # ------------------------------------------------------------ convenience

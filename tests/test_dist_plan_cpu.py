@@ -17,9 +17,11 @@ def L():
     return laker
 
 
+@pytest.mark.parametrize("TC", [64, 128])     # the fp64 kernel's 128 x 64 tiles, the tensor-core 128 x 128
 @pytest.mark.parametrize("n,W", [(1024, 1), (2048, 2), (3072, 3), (2048, 4), (2560, 5), (4096, 8), (1536, 6), (7168, 7)])
-def test_plan_covers_each_entry_once_and_balances(L, n, W):
-    nsb = n // TC                     # 64-wide sub-blocks: a tile is 2 x 1 of them
+def test_plan_covers_each_entry_once_and_balances(L, n, W, TC):
+    R = BR // TC                      # column sub-blocks per tile row block
+    nsb = n // TC                     # TC-wide sub-blocks: a tile is R x 1 of them
     count = np.zeros((nsb, nsb), dtype=np.int64)
     tiles = []
     for w in range(W):
@@ -31,11 +33,11 @@ def test_plan_covers_each_entry_once_and_balances(L, n, W):
         for I in range(Lb):
             Ig = w * Lb + I
             for j in jt[toff[I]:toff[I + 1]]:
-                for rsb in (2 * Ig, 2 * Ig + 1):
+                for rsb in range(R * Ig, R * Ig + R):
                     count[rsb, j] += 1               # row contribution K_ij x_j -> y_i
-                    if j // 2 != Ig:
+                    if j // R != Ig:
                         count[j, rsb] += 1           # column contribution K_ij x_i -> y_j
-                if j // 2 != Ig:
+                if j // R != Ig:
                     cols.setdefault(int(j), set()).add(I)
         for j in range(nsb):
             have = cols.get(j, set())
@@ -45,10 +47,10 @@ def test_plan_covers_each_entry_once_and_balances(L, n, W):
     # balance: each rank streams the single-GPU triangle / W, in tiles of BR x TC
     per = (n // W) ** 2 * W / 2 / (BR * TC)
     assert all(abs(t - per) <= n // W // BR for t in tiles), (tiles, per)
-    # W = 1 is the single-GPU plan: block-row I streams column tiles 2I .. n/TC - 1
+    # W = 1 is the single-GPU plan: block-row I streams column tiles R I .. n/TC - 1
     if W == 1:
         p = L.laker_debug_dist_tiles(n, BR, TC, 0, 1)
-        exp = np.concatenate([np.arange(2 * I, nsb) for I in range(n // BR)])
+        exp = np.concatenate([np.arange(R * I, nsb) for I in range(n // BR)])
         assert (p["jt"] == exp).all()
 
 

@@ -43,9 +43,14 @@ def test_collective_path_equals_single(L, cid, n, kind):
             c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, Z=Z, p_layout=L.P_AUTO)
         a, reps, hist = c.pcg_solve(P.y, P.tol, want_history=True)
         q = c.apply_operator(a)
-        res.append((a, reps[0], hist, q))
+        res.append((a, reps[0], hist, q, c.stats()["k_tensor_core"]))
         c.close()
-    (a0, r0, h0, q0), (a1, r1, h1, q1) = res
+    (a0, r0, h0, q0, t0), (a1, r1, h1, q1, t1) = res
+    # the stored symmetric K of the configs takes the exact tensor-core apply on both paths
+    # (the sharded one reduce-scatters its int64 level groups); the sharded path with
+    # n = 1000 (n/W not a multiple of 256) streams full rows
+    stored = kind != "onthefly"
+    assert t0 == int(stored) and t1 == int(stored and P.n % 256 == 0), (t0, t1)
     assert r0["iters"] == r1["iters"] and r0["termination"] == r1["termination"]
     assert (h0 == h1).all() and (a0 == a1).all() and (q0 == q1).all()
     assert r0["true_rel_residual"] == r1["true_rel_residual"]
@@ -173,3 +178,42 @@ def test_collective_block_solve_equals_single(L, kind):
         for j in range(Y.shape[1]):
             ao, ro = O.pcg(K, P.lam, Y[:, j], O.P_JACOBI, d, tol=P.tol)
             assert ro.iters == i1[j] and (ao == A1[:, j]).all()
+
+
+@pytest.mark.parametrize("W", [2, 3, 4, 8])
+def test_tensor_core_groups_of_shards_sum_to_one_rank(L, W):
+    """The exact tensor-core apply on the sharded plan (symv_tc.cu with dist_tiles at
+    128 x 128; B13, §8): every shard's int64 level groups of all rows
+    (laker_debug_tc_groups, detached shards on one GPU) add up, as integers, to the one-rank
+    groups -- each symmetric pair of entries is streamed once over the shards -- so the
+    int64 reduce-scatter of pcg_dist.cu gives every rank exactly the one-rank row sums, and
+    its combine (the finalize's arithmetic) the one-rank apply bitwise."""
+    n = {3: 3072}.get(W, 4096)
+    P = make_problem(3, n=n)
+    full = L.Context(0)
+    full.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    assert full.stats()["k_tensor_core"] == 1
+    rowmax = np.ascontiguousarray(np.abs(full.get_kernel_rows()).max(axis=1))
+    rng = np.random.default_rng(40 + W)
+    xs = [rng.standard_normal(n), np.where(rng.random(n) < 0.5, -1.0, 1.0) * np.exp(rng.uniform(-8, 8, n))]
+    ones = []
+    for x in xs:
+        g = np.zeros(8 * n, dtype=np.int64)
+        L.laker_debug_tc_groups(full.h, x, None, g)
+        ones.append(g)
+    full.close()
+    sums = [np.zeros(8 * n, dtype=np.int64) for _ in xs]
+    for w in range(W):
+        c = L.Context(0, w, W, None)
+        c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+        for x, acc in zip(xs, sums):
+            g = np.zeros(8 * n, dtype=np.int64)
+            L.laker_debug_tc_groups(c.h, x, rowmax, g)
+            acc += g
+        assert c.stats()["k_tensor_core"] == 1
+        c.close()
+    for acc, one in zip(sums, ones):
+        bad = np.flatnonzero(acc != one)
+        assert bad.size == 0, (W, bad.size, bad[:5])
+        assert np.abs(one).max() > 0
+
