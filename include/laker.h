@@ -94,12 +94,13 @@ const char *laker_last_error(laker_ctx ctx);
    stored for the operator lambda I + K; it is never added to K.
    storage MATERIALIZED: rank r stores rows [r n/W, (r+1) n/W) of K in HBM
    (upper-triangle tiles computed once and mirrored, so K is bitwise symmetric).
-   On one rank, when every entry of K lies on the grid 2^(eK-55) of its largest
-   binade (all BASELINE configs), the upper-triangle tiles are also stored as 8
-   int8 digit slices per entry (n^2/2 x 8 bytes more) and every K apply runs
-   exactly on the tcgen05 int8 tensor cores (B13; stats.k_tensor_core),
-   bitwise the fp64 Dot2 result; otherwise the fp64 symmetric kernel is used
-   (LAKER_SYMV_TC=0 forces it, for A/B tests).
+   When every entry of K lies on the grid 2^(eK-55) of its largest binade (all
+   BASELINE configs), the upper-triangle tiles (one rank) or the rank's tiles of the
+   sharded plan (n/W a multiple of 256) are also stored as 8 int8 digit slices per
+   entry (n^2/(2W) x 8 bytes more) and every K apply runs exactly on the tcgen05
+   int8 tensor cores (B13, §8: shards exchange exact int64 row sums by a
+   reduce-scatter; stats.k_tensor_core), bitwise the fp64 Dot2 result; otherwise the
+   fp64 symmetric kernel is used (LAKER_SYMV_TC=0 forces it, for A/B tests).
    storage ON_THE_FLY: only E is kept; every operator apply recomputes the
    entries tile by tile (P:517-519 matvec-only access).
    Errors: INVALID_ARGUMENT (n < 1, d < 1, lambda <= 0, n % world != 0, bad
