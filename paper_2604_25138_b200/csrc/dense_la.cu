@@ -14,53 +14,81 @@ namespace {
 constexpr int NB = 64;
 
 // Factor the 64 x 64 diagonal block at (j0, j0); zero its strict upper part.
-// Right-looking in shared memory, 256 threads as a 16 x 16 grid: step j divides
-// column j by the pivot sqrt(A_jj) (taken by every thread itself), then thread
-// (ty, tx) applies A_ik -= L_ij L_kj to rows i = j+1+ty+16a, columns
-// k = j+1+tx+16b with k <= i -- the textbook operations, two barriers per step.
+// Right-looking, 256 threads as a 16 x 16 grid, the block held in registers: thread
+// (ty, tx) owns A_ik for rows i = ty + 16a, columns k = tx + 16b (a, b < 4).  Step j:
+// every thread takes 1/sqrt(A_jj) from the pivot slot, the owners of column j
+// (tx == j mod 16) scale it into the shared column buffer, then every thread applies
+// A_ik -= L_ij L_kj to its entries with j < k <= i and the owner of A_{j+1,j+1}
+// publishes the next pivot -- the textbook operations (the same per-entry sequence
+// as a shared-memory right-looking loop), two barriers and 8 broadcast loads per step
+// instead of a shared read-modify-write of the whole trailing triangle.
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double *A, int64_t lda, int64_t j0, int *flag) {
-  __shared__ double S[NB][NB + 1];
+  __shared__ double col[NB];
+  __shared__ double pivot;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-#pragma unroll 4
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int r = e / NB, c = e % NB;
-    S[r][c] = A[(j0 + r) * lda + j0 + c];
-  }
+  double v[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) v[a][b] = A[(j0 + ty + 16 * a) * lda + j0 + tx + 16 * b];
+  if (tid == 0) pivot = v[0][0];
   __syncthreads();
-  for (int j = 0; j < NB; ++j) {
-    double d = S[j][j];
-    if (!(d > 0.0)) {
-      if (tid == 0) atomicExch(flag, 1);
-      d = 1.0;
-    }
-    // 1/sqrt(d) directly (hardware approximation + Newton steps, ~1 ulp) and the pivot as
-    // d / sqrt(d): the step's dependent chain was the IEEE sqrt followed by the IEEE
-    // reciprocal; the fit only needs P to ~1e-8 of the oracle's (tests/test_gpu_fit.py)
-    const double rpiv = rsqrt(d);
-    const double piv = __dmul_rn(d, rpiv);
-    // column j below the diagonal (rows j+1+tid), the pivot itself by thread 63
-    if (tid < NB - 1 - j) S[j + 1 + tid][j] = __dmul_rn(S[j + 1 + tid][j], rpiv);
-    __syncthreads();
-    if (tid == NB - 1) S[j][j] = piv;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int i = j + 1 + ty + 16 * a;
-      if (i < NB) {
-        const double lij = S[i][j];
+  for (int jb = 0; jb < 4; ++jb) {
+    for (int jt = 0; jt < 16; ++jt) {
+      const int j = 16 * jb + jt;
+      double d = pivot;
+      if (!(d > 0.0)) {
+        if (tid == 0) atomicExch(flag, 1);
+        d = 1.0;
+      }
+      // 1/sqrt(d) directly (hardware approximation + Newton steps, ~1 ulp) and the pivot as
+      // d / sqrt(d): the step's dependent chain was the IEEE sqrt followed by the IEEE
+      // reciprocal; the fit only needs P to ~1e-8 of the oracle's (tests/test_gpu_fit.py)
+      const double rpiv = rsqrt(d);
+      if (tx == jt) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int k = j + 1 + tx + 16 * b;
-          if (k <= i) S[i][k] = __fma_rn(-lij, S[k][j], S[i][k]);
+        for (int a = 0; a < 4; ++a) {
+          const int i = ty + 16 * a;
+          if (i > j) {
+            const double l = __dmul_rn(v[a][jb], rpiv);
+            v[a][jb] = l;
+            col[i] = l;
+          } else if (i == j) {
+            v[a][jb] = __dmul_rn(d, rpiv);
+          }
         }
       }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = ty + 16 * a;
+        if (i > j) {
+          const double lij = col[i];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int k = tx + 16 * b;
+            if (k > j && k <= i) v[a][b] = __fma_rn(-lij, col[k], v[a][b]);
+          }
+        }
+      }
+      // the next pivot A_{j+1,j+1}: row and column j + 1 are owned by ty == tx == (j+1) mod 16
+      const int jn = j + 1, an = jn >> 4;
+      if (jn < NB && tx == (jn & 15) && ty == (jn & 15)) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if (a == an) pivot = v[a][a];
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
-#pragma unroll 4
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int r = e / NB, c = e % NB;
-    A[(j0 + r) * lda + j0 + c] = c <= r ? S[r][c] : 0.0;
-  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, k = tx + 16 * b;
+      A[(j0 + i) * lda + j0 + k] = k <= i ? v[a][b] : 0.0;
+    }
 }
 
 // Rows [r0, r0 + nrows) of column block j0: X = A L^{-T}, L = A[j0.., j0..] (factored).

@@ -239,7 +239,10 @@ void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s) {
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int64_t tiles_l = ((g.N + 127) / 128) * ((g.M + 127) / 128);
-  if (tiles_l >= 2 * sms || g.lower_only) {
+  // (lower_only -- the Cholesky updates -- included: a small K = 64 update of ~100 128 x 128
+  // tiles is one latency-bound wave; 64 x 64 tiles put 4x the CTAs on the SMs.  Each entry's
+  // DMMA k order is the tile's own, so C is the same for either tile)
+  if (tiles_l >= 2 * sms) {
     dim3 grid((unsigned)((g.N + 127) / 128), (unsigned)((g.M + 127) / 128));
     if (b_kn)
       dgemm_kernel<TileL, true><<<grid, TileL::THREADS, TileL::smem(true), s>>>(g);
@@ -250,7 +253,7 @@ void launch_dgemm(const GemmArgs &g, bool b_kn, cudaStream_t s) {
     // skinny products with a long K (the block solve's Q^T R, M Z: 64 output tiles on 148
     // SMs): split K over ks CTAs per tile, partials summed in a fixed order
     int ks = 1;
-    if (g.N <= 256 && g.tri == 0 && g.K >= 2048 && tiles_s < sms && g_splitk_ws) {
+    if (g.N <= 256 && g.tri == 0 && !g.lower_only && g.K >= 2048 && tiles_s < sms && g_splitk_ws) {
       ks = (int)std::min<int64_t>({(2 * sms + tiles_s - 1) / tiles_s, g.K / 1024,
                                    (int64_t)(kSplitWsDoubles / (size_t)(g.M * g.N))});
       if (ks < 2) ks = 1;

@@ -381,7 +381,8 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
 // route a GemmArgs to the Ozaki path when it is large enough to pay
 bool ozaki_eligible(const GemmArgs &g);
 void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
-                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf = nullptr);
+                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf = nullptr,
+                        int il = 0);
 
 // --------------------------------------------------------------- otf_tc.cu
 // FAST on-the-fly kernel matvec on the tcgen05 int8 tensor cores: the QK^T dot

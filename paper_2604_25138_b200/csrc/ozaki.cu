@@ -367,6 +367,166 @@ __global__ void __launch_bounds__(kLThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------------ level groups, v2
+// The level-group kernel above with the slices stored chunk-interleaved: row r holds,
+// for each 32-wide K chunk kb, the S slices' 32 bytes side by side
+// (out[r][kb S 32 + s 32 + kk]), so one K chunk of 4 slices is ONE 128-byte TMA box row
+// (SWIZZLE_128B, the fused kernel's tile shape) instead of four 32-byte box rows; a
+// 3-stage ring of chunk sets (64 KiB each).  Same slice pairs, same level order, same
+// fp64 epilogue: bitwise the fused kernel's C.
+constexpr int kL2Stages = 3;
+constexpr uint32_t kL2Box = 128 * 128;                 // 16 KiB: 128 rows x 4 slices x 32 B
+constexpr uint32_t kL2Stage = 4 * kL2Box;              // A boxes 0, 1 + B boxes 0, 1
+constexpr size_t kL2Smem = 1024 + kL2Stages * kL2Stage + 256;
+
+__global__ void __launch_bounds__(kLThreads, 1)
+    ozaki_lv2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const FusedArgs f) {
+  constexpr int kGroupM = 12;
+  const int64_t tm = (f.M + kLM - 1) / kLM, tn = (f.N + kLN - 1) / kLN;
+  const int64_t pid = blockIdx.x;
+  const int64_t gsize = (int64_t)kGroupM * tn;
+  const int64_t g0 = (pid / gsize) * kGroupM;
+  const int64_t gm = (tm - g0) < kGroupM ? (tm - g0) : kGroupM;
+  const int64_t m0 = (g0 + (pid % gsize) % gm) * kLM, n0 = ((pid % gsize) / gm) * kLN;
+  if (f.tri == 1 && m0 + kLM - 1 + f.tri_off < n0) return;
+  if (f.tri == 2 && m0 + f.tri_off >= n0 + kLN - 1) return;
+  extern __shared__ unsigned char smem_raw[];
+  const uint32_t base_s = smem_u32(smem_raw);
+  unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);  // [stage][A0 A1 B0 B1]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kL2Stages * kL2Stage);  // [kL2Stages]
+  uint64_t *empty = full + kL2Stages;                                          // [kL2Stages]
+  uint64_t *tfull = empty + kL2Stages;                                         // [4]
+  uint64_t *tempty = tfull + 4;                                                // [4]
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = f.S;
+  const int nkb = (int)(f.Kp / kLK);
+  const int ngrp = (S + 3) / 4;
+
+  if (warp == 0 && lane == 0) {
+    for (int b = 0; b < kL2Stages; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    for (int j = 0; j < 4; ++j) {
+      mbar_init(&tfull[j], 1);
+      mbar_init(&tempty[j], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      int use = 0;
+      for (int g = 0; g < ngrp; ++g) {
+        const int nbox = (S - 4 * g + 3) / 4;  // slices 0 .. S-1-4g of both operands
+        for (int kb = 0; kb < nkb; ++kb, ++use) {
+          if (use >= kL2Stages) mbar_wait(&empty[st], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * nbox) * kL2Box);
+          unsigned char *sb = smem + st * kL2Stage;
+          for (int j = 0; j < nbox; ++j) {
+            const int32_t x = (int32_t)((int64_t)kb * S * kLK + 128 * j);
+            tc::tma_load_2d(sb + j * kL2Box, &tmA, x, (int32_t)m0, &full[st]);
+            tc::tma_load_2d(sb + (2 + j) * kL2Box, &tmB, x, (int32_t)n0, &full[st]);
+          }
+          if (++st == kL2Stages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_i8(kLM, kLN);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int g = 0; g < ngrp; ++g) {
+        const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0;
+        if (g > 0)
+          for (int j = 0; j <= hi - lo; ++j) mbar_wait(&tempty[j], (uint32_t)((g - 1) & 1));
+        tc::fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc::fence_after();
+          const uint32_t sa = smem_u32(smem + st * kL2Stage), sbb = sa + 2 * kL2Box;
+          for (int h = hi; h >= lo; --h) {  // level-major: consecutive MMAs share the accumulator
+            const uint32_t td = tmem + (uint32_t)((hi - h) * kLN);
+            for (int c = 0; c <= h; ++c) {
+              const int t = h - c;
+              const uint64_t ad = tc::sdesc_k_sw128(sa + (uint32_t)((c >> 2) * kL2Box + (c & 3) * 32));
+              const uint64_t bd = tc::sdesc_k_sw128(sbb + (uint32_t)((t >> 2) * kL2Box + (t & 3) * 32));
+              tc::mma_i8(td, ad, bd, idesc, (kb > 0 || c > 0) ? 1u : 0u);
+            }
+          }
+          tc::mma_commit(&empty[st]);
+          if (++st == kL2Stages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+        for (int j = 0; j <= hi - lo; ++j) tc::mma_commit(&tfull[j]);
+      }
+    }
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int64_t row = m0 + q * 32 + lane;
+    double acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+    for (int g = 0; g < ngrp; ++g) {
+      const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0;
+      for (int h = hi; h >= lo; --h) {
+        const int jb = hi - h;
+        mbar_wait(&tfull[jb], (uint32_t)(g & 1));
+        tc::fence_after();
+        const double sc = scalbn(1.0, -12 - 7 * h);
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(tmem + (uint32_t)(jb * kLN + half * 64 + c) + ((uint32_t)(q * 32) << 16), v);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c + j] = __dadd_rn(acc[c + j], __dmul_rn((double)(int32_t)v[j], sc));
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[jb]);
+      }
+    }
+    if (row < f.M) {
+      const int ea = f.ea[row];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int64_t col = n0 + half * 64 + j;
+        bool keep = col < f.N;
+        if (f.tri != 0) {
+          const int64_t gr = row + f.tri_off;
+          keep = keep && (f.tri == 1 ? gr >= col : gr < col);
+        }
+        if (keep) {
+          const double tot = scalbn(acc[j], ea + f.eb[col]);
+          double out = __dmul_rn(f.alpha, tot);
+          if (f.beta != 0.0) out = __dadd_rn(out, __dmul_rn(f.beta, f.Cin[row * f.ldcin + col]));
+          if (f.diag != 0.0 && row - col == f.diag_offset) out = __dadd_rn(out, f.diag);
+          f.C[row * f.ldc + col] = out;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
 // max-exponent of each row of X (element (r, k) = trans ? X[k ld + r] : X[r ld + k]);
 // e[r] = e with max |x| < 2^e (frexp), 0 for an all-zero row
 __global__ void __launch_bounds__(256) ozaki_rowexp_kernel(const double *__restrict__ X, int64_t ld, int64_t rows,
@@ -428,7 +588,8 @@ __global__ void ozaki_bits2exp_kernel(const unsigned long long *__restrict__ mx,
 // staged through shared memory so both the fp64 reads and the int8 writes coalesce
 __global__ void __launch_bounds__(256) ozaki_split_kernel(const double *__restrict__ X, int64_t ld, int64_t rows,
                                                           int64_t K, int trans, const int32_t *__restrict__ e,
-                                                          int S, int rev, int8_t *__restrict__ out, int64_t Kp) {
+                                                          int S, int rev, int8_t *__restrict__ out, int64_t Kp,
+                                                          int il) {
   __shared__ double t[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
@@ -447,10 +608,12 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double *__restri
     const int64_t r = r0 + i, k = k0 + tx;
     if (r >= rows || k >= Kp) continue;
     double x = scalbn(t[i][tx], 6 - e[r]);  // |x| < 64, exact
-    int8_t *o = out + r * ldo + k;
+    // il: chunk-interleaved (ozaki_lv2_kernel), out[r][(k / 32) S 32 + s 32 + k % 32]
+    int8_t *o = out + r * ldo + (il ? (k >> 5) * S * 32 + (k & 31) : k);
+    const int64_t sstride = il ? 32 : Kp;
     for (int s = 0; s < S; ++s) {
       const double d = rint(x);
-      o[(int64_t)(rev ? S - 1 - s : s) * Kp] = (int8_t)(int)d;
+      o[(int64_t)(rev ? S - 1 - s : s) * sstride] = (int8_t)(int)d;
       x = (x - d) * 128.0;  // exact: |x - d| <= 1/2 and x has <= 53 significant bits
     }
   }
@@ -465,7 +628,7 @@ inline int ozaki_S() {
 // scales + digit slices of a rows x K fp64 matrix (K-contiguous, or K x rows if trans):
 // out[r][slot(s) Kp + k], slot(s) = rev ? S-1-s : s; e[r] the row's power-of-two exponent
 void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, int trans, int S, int rev,
-                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf) {
+                        int8_t *out, int32_t *e, int64_t Kp, cudaStream_t s, unsigned long long *mx_buf, int il) {
   if (trans) {
     unsigned long long *mx = mx_buf;
     if (!mx) cudaMallocAsync(&mx, (size_t)rows * sizeof(unsigned long long), s);
@@ -478,7 +641,7 @@ void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, in
     ozaki_rowexp_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(X, ld, rows, K, 0, e);
   }
   ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32)), 256, 0, s>>>(
-      X, ld, rows, K, trans, e, S, rev, out, Kp);
+      X, ld, rows, K, trans, e, S, rev, out, Kp, il);
 }
 
 bool ozaki_eligible(const GemmArgs &g) {
@@ -504,16 +667,40 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   if ((err = cudaMallocAsync(&Bs, lb, s)) != cudaSuccess) return err;
   if ((err = cudaMallocAsync(&ea, (M + N) * sizeof(int32_t), s)) != cudaSuccess) return err;
   eb = ea + M;
-  // the level-group kernel cuts the slice traffic 3x: measured 40.8 vs 49.5 ms on the fit's
-  // directions product (4096 x 16384 x 16384) but 2.87 vs 2.56 ms at 4096^3, so it serves the
-  // large products only (M N K >= 2^40); `kernel` (diagnostic) forces either: 0 fused, 1 group
+  // the level-group kernels cut the slice traffic 3x: the directions product (4096 x 16384 x
+  // 16384) takes 47.9 ms fused, 47.5 with level groups, 40.8 with level groups on
+  // chunk-interleaved slices (v2); at 4096^3 2.55 / 2.84 / 2.80 ms (tools/bench_ozaki_lv.py,
+  // profiles/r02_ozaki_lv2.txt), so v2 serves the large products only (M N K >= 2^40);
+  // `kernel` (diagnostic) forces one: 0 fused, 1 level groups, 2 level groups v2
   const bool big = (double)M * (double)N * (double)K >= 1099511627776.0;
-  const bool lv = S <= kLSmax && (kernel >= 0 ? kernel == 1 : big);
+  const bool lv2 = S <= kLSmax && (kernel >= 0 ? kernel == 2 : big);
+  const bool lv = S <= kLSmax && kernel == 1;
   // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn);
   // (B slices in reverse order for the level-streaming kernels: level h's pairs are a
-  // contiguous K range; forward order for the level-group kernel)
-  launch_ozaki_split(g.A, g.lda, M, K, 0, S, 0, As, ea, Kp, s);
-  launch_ozaki_split(g.B, g.ldb, N, K, b_kn ? 1 : 0, S, lv ? 0 : 1, Bs, eb, Kp, s);
+  // contiguous K range; forward order for the level-group kernels, chunk-interleaved for v2)
+  launch_ozaki_split(g.A, g.lda, M, K, 0, S, 0, As, ea, Kp, s, nullptr, lv2 ? 1 : 0);
+  launch_ozaki_split(g.B, g.ldb, N, K, b_kn ? 1 : 0, S, (lv || lv2) ? 0 : 1, Bs, eb, Kp, s, nullptr, lv2 ? 1 : 0);
+  if (lv2) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ozaki_lv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kL2Smem);
+      attr = true;
+    }
+    CUtensorMap ta, tb;
+    const int64_t ldo = (int64_t)S * Kp;
+    if (!make_tmap_s8(&ta, As, M, ldo, ldo, kLM) || !make_tmap_s8(&tb, Bs, N, ldo, ldo, kLN))
+      return cudaErrorInvalidValue;
+    FusedArgs f{};
+    f.M = M; f.N = N; f.Kp = Kp; f.S = S; f.ea = ea; f.eb = eb; f.C = g.C; f.ldc = g.ldc; f.Cin = g.Cin;
+    f.ldcin = g.ldcin; f.alpha = g.alpha; f.beta = g.beta; f.diag = g.diag; f.diag_offset = g.diag_offset;
+    f.tri = g.tri; f.tri_off = g.tri_off;
+    const unsigned grid = (unsigned)(((N + kLN - 1) / kLN) * ((M + kLM - 1) / kLM));
+    ozaki_lv2_kernel<<<grid, kLThreads, kL2Smem, s>>>(ta, tb, f);
+    cudaFreeAsync(As, s);
+    cudaFreeAsync(Bs, s);
+    cudaFreeAsync(ea, s);
+    return cudaGetLastError();
+  }
   if (lv) {
     static bool attr = false;
     if (!attr) {
