@@ -212,12 +212,21 @@ __global__ void transpose_kernel(const double *__restrict__ A, int64_t rows, int
 constexpr int NB2 = 512;
 
 void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s, int64_t *launches) {
+  cholesky_lower_aug(A, lda, n, n, flag, s, launches);
+}
+
+// Rows [0, m) x columns [0, n) of A, m >= n: the lower Cholesky factor L of the leading
+// n x n block and, in rows [n, m), B L^{-T} for the block B stored there -- the blocked
+// factorization of [[A11, *], [B, *]] run over its first n columns (every panel solve and
+// update also covers rows [n, m); the trailing matrix of rows >= n is never formed).
+void cholesky_lower_aug(double *A, int64_t lda, int64_t n, int64_t m, int *flag, cudaStream_t s,
+                        int64_t *launches) {
   for (int64_t J0 = 0; J0 < n; J0 += NB2) {
     const int64_t Jend = std::min<int64_t>(n, J0 + NB2);
     for (int64_t j0 = J0; j0 < Jend; j0 += NB) {
       potrf_diag_kernel<<<1, 256, 0, s>>>(A, lda, j0, flag);
       ++*launches;
-      const int64_t rest = n - j0 - NB;
+      const int64_t rest = m - j0 - NB;
       if (rest <= 0) break;
       potrf_panel_kernel<<<(unsigned)((rest + kPanelRows - 1) / kPanelRows), kPanelThreads, 0, s>>>(A, lda, j0,
                                                                                                     j0 + NB, rest);
@@ -242,11 +251,11 @@ void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s
       launch_dgemm(g, false, s);
       ++*launches;
     }
-    const int64_t rest = n - Jend;
-    if (rest <= 0) break;
-    GemmArgs g{};  // trailing matrix: A[Jend.., Jend..] -= P P^T with P = A[Jend.., J0 .. Jend)
+    const int64_t rest = m - Jend;
+    if (n - Jend <= 0) break;
+    GemmArgs g{};  // trailing matrix: A[Jend.., Jend..n) -= P P[0:n-Jend]^T with P = A[Jend.., J0 .. Jend)
     g.M = rest;
-    g.N = rest;
+    g.N = n - Jend;
     g.K = Jend - J0;
     g.A = A + Jend * lda + J0;
     g.lda = lda;

@@ -104,25 +104,19 @@ __global__ void scale_cols_sqrt_kernel(const double *R, double *S, int64_t ld, i
     S[r * ld + c] = R[r * ld + c] * __dsqrt_rn(b[c]);
 }
 
-// qf[k] = sum_i X[i][k]^2 (Dot2), k < nr; block (32 columns x 8 row lanes),
-// lanes combined in a fixed order.
-__global__ void col_sumsq_kernel(const double *X, int64_t ld, int64_t rows, int64_t nr, double *qf) {
-  __shared__ dd_pair red[8][32];
-  const int64_t k = (int64_t)blockIdx.x * 32 + threadIdx.x;
+// qf[k] = sum_j X[k][j]^2 over columns [0, cols) for rows k < nr (Dot2 per lane, lanes
+// combined by the fixed xor tree): one warp per row
+__global__ void row_sumsq_kernel(const double *X, int64_t ld, int64_t cols, int64_t nr, double *qf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= nr) return;
   dd_pair acc = {0.0, 0.0};
-  if (k < nr) {
-    for (int64_t i = threadIdx.y; i < rows; i += 8) {
-      const double v = X[i * ld + k];
-      dot2_step(acc, v, v);
-    }
+  for (int64_t j = lane; j < cols; j += 32) {
+    const double v = X[k * ld + j];
+    dot2_step(acc, v, v);
   }
-  red[threadIdx.y][threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.y == 0 && k < nr) {
-    dd_pair t = red[0][threadIdx.x];
-    for (int l = 1; l < 8; ++l) pair_add(t, red[l][threadIdx.x]);
-    qf[k] = pair_value(t);
-  }
+  acc = warp_reduce_pair(acc);
+  if (lane == 0) qf[k] = pair_value(acc);
 }
 
 struct CccpScalars {
@@ -456,7 +450,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   LAKER_CUDA(ctx, mem.alloc(&L3, sq));
   LAKER_CUDA(ctx, mem.alloc(&R, sq));
   LAKER_CUDA(ctx, mem.alloc(&Rt, sq));
-  LAKER_CUDA(ctx, mem.alloc(&T, sq));
+  LAKER_CUDA(ctx, mem.alloc(&T, 2 * sq));  // rows [nrp, 2 nrp): R^T for the augmented Cholesky
   LAKER_CUDA(ctx, mem.alloc(&X, sq));
   LAKER_CUDA(ctx, mem.alloc(&S, sq));
   LAKER_CUDA(ctx, mem.alloc(&qf, nrp));
@@ -668,10 +662,13 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     hs.rho = rho_t;
     hs.a = a;
     LAKER_CUDA(ctx, cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
-    cholesky_lower(T, nrp, nrp, flag, s, &L);
-    LAKER_CUDA(ctx, cudaMemcpyAsync(X, R, sq * 8, cudaMemcpyDeviceToDevice, s));
-    trsm_lower_left(T, nrp, nrp, X, nrp, nrp, s, &L);
-    col_sumsq_kernel<<<dim3(cdiv(nr, 32)), dim3(32, 8), 0, s>>>(X, nrp, nrp, nr, qf);
+    // q_k = || L_t^{-1} r_k ||^2 (T_t = L_t L_t^T, r_k column k of R): the Cholesky of
+    // [[T_t, *], [R^T, *]] over its first N_r columns leaves R^T L_t^{-T} = (L_t^{-1} R)^T in
+    // rows [nrp, 2 nrp) -- the triangular solve done inside the factorization's panel
+    // steps instead of a separate blocked solve (one launch chain instead of two)
+    LAKER_CUDA(ctx, cudaMemcpyAsync(T + sq, Rt, sq * 8, cudaMemcpyDeviceToDevice, s));
+    cholesky_lower_aug(T, nrp, nrp, 2 * nrp, flag, s, &L);
+    row_sumsq_kernel<<<(unsigned)cdiv(nr, 8), 256, 0, s>>>(T + sq, nrp, nrp, nr, qf);
     cccp_update_kernel<<<1, 1024, 0, s>>>(qf, cd, b, bo, db, nr, sc);
     const int qg = (int)std::min<int64_t>(2 * ctx->num_sms, (nr + 7) / 8);
     cccp_quadform_kernel<<<qg, 256, 0, s>>>(Cg, nrp, nr, db, bo, ctx->partials, ctx->counters + kCtrMisc, sc);

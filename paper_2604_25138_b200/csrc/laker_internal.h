@@ -417,6 +417,8 @@ int oz_skinny_max_slices();
 // In-place lower Cholesky of the n x n SPD matrix A (row-major, lda; n % 64 == 0);
 // strict upper triangle zeroed.  *flag (device) set to 1 on a pivot <= 0.
 void cholesky_lower(double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s, int64_t *launches);
+void cholesky_lower_aug(double *A, int64_t lda, int64_t n, int64_t m, int *flag, cudaStream_t s,
+                        int64_t *launches);
 // B <- L^{-1} B  (L n x n lower, n % 64 == 0; B n x ncols row-major, ldb).
 void trsm_lower_left(const double *L, int64_t ldl, int64_t n, double *B, int64_t ldb, int64_t ncols,
                      cudaStream_t s, int64_t *launches);
