@@ -753,6 +753,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     const double sk = std::sqrt(sigma);
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.lda = g.ldb = g.ldc = nrp; g.tri = 1;
+    g.b_sym = true;  // every B below (Y, W, Z) is mirrored, exactly symmetric
     g.A = Zm; g.B = Y; g.C = W; g.alpha = -0.5 * sigma; g.diag = 1.5;
     launch_dgemm(g, true, s);
     launch_mirror_lower(W, nrp, nrp, s);
@@ -797,6 +798,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
     for (int k = 0; k < 8; ++k) {
       GemmArgs g{};
       g.M = nrp; g.N = nrp; g.K = nrp; g.lda = g.ldb = g.ldc = nrp;
+      g.b_sym = true;  // T, Z, W mirrored, exactly symmetric
       g.A = Zm; g.B = T; g.C = Tmp; g.alpha = 1.0 / cscale;   // Z T / c  (full)
       launch_dgemm(g, true, s);
       g.A = Tmp; g.B = Zm; g.C = W; g.alpha = -0.5; g.diag = 1.5; g.tri = 1;  // W = (3I - Z T Z / c) / 2
@@ -896,6 +898,7 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
       g.lda = ldq;
       g.B = ctx->Mf;
       g.ldb = ldq;
+      g.b_sym = true;  // M = Z / sqrt(c) - a^-1/2 I, Z mirrored
       g.C = ctx->QMf;
       g.ldc = ldq;
       g.alpha = 1.0;

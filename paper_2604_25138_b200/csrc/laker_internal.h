@@ -333,6 +333,7 @@ struct GemmArgs {
   bool lower_only;        // skip CTA tiles strictly above the block diagonal
   bool dmma_only = false; // keep the product on the fp64 (DMMA) path, never the int8 emulation
   int oz_slices = 0;      // int8 digit slices of the emulation when it is used (0: ozaki_S())
+  bool b_sym = false;     // B is exactly symmetric (mirrored): the emulation slices op(B) by B's rows
   int tri;                // 0 all; 1 only entries with row + tri_off >= col; 2 only row + tri_off < col
   int64_t tri_off;        // (tiles with no kept entry are skipped; masked entries are not written)
   // internal (launch_dgemm's split-K for skinny products): CTA z covers k in

@@ -619,6 +619,34 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double *__restri
   }
 }
 
+// the same digits for the row-major (non-transposed) case without the shared-memory
+// transpose: 16 rows x 128 k per CTA, each thread 8 consecutive k of one row, written as
+// one 8-byte word per slice (the 32 x 32 kernel above stores single bytes)
+__global__ void __launch_bounds__(256) ozaki_split_rows_kernel(const double *__restrict__ X, int64_t ld,
+                                                               int64_t rows, int64_t K,
+                                                               const int32_t *__restrict__ e, int S, int rev,
+                                                               int8_t *__restrict__ out, int64_t Kp, int il) {
+  const int64_t r = (int64_t)blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int64_t k0 = (int64_t)blockIdx.x * 128 + (threadIdx.x & 15) * 8;
+  if (r >= rows || k0 >= Kp) return;
+  const int sh = 6 - e[r];
+  double x[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = k0 + j < K ? scalbn(X[r * ld + k0 + j], sh) : 0.0;  // |x| < 64, exact
+  int8_t *o = out + r * (int64_t)S * Kp + (il ? (k0 >> 5) * S * 32 + (k0 & 31) : k0);
+  const int64_t sstride = il ? 32 : Kp;
+  for (int s = 0; s < S; ++s) {
+    unsigned long long w = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double d = rint(x[j]);
+      w |= (unsigned long long)(uint8_t)(int8_t)(int)d << (8 * j);
+      x[j] = (x[j] - d) * 128.0;  // exact: |x - d| <= 1/2 and x has <= 53 significant bits
+    }
+    *reinterpret_cast<unsigned long long *>(o + (int64_t)(rev ? S - 1 - s : s) * sstride) = w;
+  }
+}
+
 inline int ozaki_S() {
   return 8;  // B12: fewer slices (5) left P 1e-7 off the oracle's and indefinite at C5
 }
@@ -637,11 +665,13 @@ void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, in
                                                                                                         K, mx);
     ozaki_bits2exp_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(mx, rows, e);
     if (!mx_buf) cudaFreeAsync(mx, s);
+    ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32)), 256, 0, s>>>(
+        X, ld, rows, K, trans, e, S, rev, out, Kp, il);
   } else {
     ozaki_rowexp_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(X, ld, rows, K, 0, e);
+    ozaki_split_rows_kernel<<<dim3((unsigned)((Kp + 127) / 128), (unsigned)((rows + 15) / 16)), 256, 0, s>>>(
+        X, ld, rows, K, e, S, rev, out, Kp, il);
   }
-  ozaki_split_kernel<<<dim3((unsigned)((Kp + 31) / 32), (unsigned)((rows + 31) / 32)), 256, 0, s>>>(
-      X, ld, rows, K, trans, e, S, rev, out, Kp, il);
 }
 
 bool ozaki_eligible(const GemmArgs &g) {
@@ -679,7 +709,9 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   // (B slices in reverse order for the level-streaming kernels: level h's pairs are a
   // contiguous K range; forward order for the level-group kernels, chunk-interleaved for v2)
   launch_ozaki_split(g.A, g.lda, M, K, 0, S, 0, As, ea, Kp, s, nullptr, lv2 ? 1 : 0);
-  launch_ozaki_split(g.B, g.ldb, N, K, b_kn ? 1 : 0, S, (lv || lv2) ? 0 : 1, Bs, eb, Kp, s, nullptr, lv2 ? 1 : 0);
+  // (an exactly symmetric B: op(B)'s columns are B's rows, sliced by the row kernels)
+  launch_ozaki_split(g.B, g.ldb, N, K, (b_kn && !g.b_sym) ? 1 : 0, S, (lv || lv2) ? 0 : 1, Bs, eb, Kp, s, nullptr,
+                     lv2 ? 1 : 0);
   if (lv2) {
     static bool attr = false;
     if (!attr) {
