@@ -239,8 +239,9 @@ laker_status laker_debug_igemm_s8(const int8_t *A, const int8_t *B, int32_t *C, 
 /* Diagnostic: C (M x N) = A (M x K) B (N x K)^T in fp64 emulated on the int8
    tensor cores (Ozaki scheme, csrc/ozaki.cu; `slices` int8 digit slices per
    input, 0 = default 8), fp64 row-major DEVICE pointers, synchronous.  `kernel`:
-   -1 the library's choice, 0 the level-streaming kernel, 1 the level-group kernel
-   (bitwise the same result; the choice exists for that test). */
+   -1 the library's choice, 0 the level-streaming kernel, any other value the
+   level-group kernel on chunk-interleaved slices (bitwise the same result; the
+   choice exists for that test). */
 laker_status laker_debug_ozaki_gemm(const double *A, const double *B, double *C, int64_t M, int64_t N, int64_t K,
                                     int32_t slices, int32_t kernel);
 

@@ -185,19 +185,6 @@ bool make_tmap_s8_k64(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 32-byte rows (K = 32 int8 per box row), SWIZZLE_32B: the level-group Ozaki GEMM chunks
-bool make_tmap_s8_k32(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
-  PFN_encodeTiled_t enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t *>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 void igemm_init() {
   cudaFuncSetAttribute(igemm_s8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIgemmSmem);
 }

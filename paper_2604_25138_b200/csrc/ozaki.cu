@@ -30,7 +30,6 @@
 namespace laker {
 bool make_tmap_s8(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
 bool make_tmap_s8_k64(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
-bool make_tmap_s8_k32(CUtensorMap *tm, const int8_t *base, int64_t rows, int64_t K, int64_t ld, int box_rows);
 namespace {
 
 // ------------------------------------------------------------------ fused levels
@@ -206,174 +205,20 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // ------------------------------------------------------------------ level groups
 // One CTA = one 128 x 128 output tile; the S digit levels in groups of <= 4 (4 TMEM
 // buffers x 128 columns = 512): for each 32-wide K chunk the S (or fewer) A slices and B
-// slices are loaded ONCE (both operands double-buffered per chunk) and every slice pair
-// (c, t) whose level c + t falls in the group is issued, level by level so consecutive
-// MMAs accumulate into the same buffer.  The fused kernel above streams the pairs level
-// by level over the whole K -- A_c and B_t are re-read for every level they meet, 4.5x
-// the slice traffic at S = 8.  Levels are accumulated in the same order (S-1 .. 0) with
-// the same fp64 operations and exact int32 level sums, so C is bitwise the fused kernel's.
+// slices are loaded ONCE and every slice pair (c, t) whose level c + t falls in the group
+// is issued, level by level so consecutive MMAs accumulate into the same buffer.  The
+// fused kernel above streams the pairs level by level over the whole K -- A_c and B_t are
+// re-read for every level they meet, 4.5x the slice traffic at S = 8.  The slices are
+// stored chunk-interleaved: row r holds, for each 32-wide K chunk kb, the S slices' 32
+// bytes side by side (out[r][kb S 32 + s 32 + kk]), so one K chunk of 4 slices is ONE
+// 128-byte TMA box row (SWIZZLE_128B, the fused kernel's tile shape); a 3-stage ring of
+// chunk sets (64 KiB each).  (A first version with separate [s][Kp] slices, four 32-byte
+// box rows per chunk and a 2-deep ring: 47.5 vs 40.8 ms on the directions product.)
+// Levels are accumulated in the same order (S-1 .. 0) with the same fp64 operations and
+// exact int32 level sums, so C is bitwise the fused kernel's.
 constexpr int kLM = 128, kLN = 128, kLK = 32;
 constexpr int kLSmax = 8;
-constexpr uint32_t kLChunk = 128 * kLK;  // 4 KiB: 128 rows x 32 int8 (32B-swizzled)
-constexpr size_t kLSmem = 1024 + 4 * kLSmax * kLChunk + 256;  // [2] A + [2] B chunk sets
 constexpr int kLThreads = 10 * 32;  // producer, MMA, 8 epilogue warps
-
-// K-major, 32-byte swizzle: 8-row x 32-byte atoms (SBO = 256 B), layout type 6
-__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t smem_addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_addr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(256 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)6 << 61;
-  return d;
-}
-
-__global__ void __launch_bounds__(kLThreads, 1)
-    ozaki_lv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const FusedArgs f) {
-  constexpr int kGroupM = 12;
-  const int64_t tm = (f.M + kLM - 1) / kLM, tn = (f.N + kLN - 1) / kLN;
-  const int64_t pid = blockIdx.x;
-  const int64_t gsize = (int64_t)kGroupM * tn;
-  const int64_t g0 = (pid / gsize) * kGroupM;
-  const int64_t gm = (tm - g0) < kGroupM ? (tm - g0) : kGroupM;
-  const int64_t m0 = (g0 + (pid % gsize) % gm) * kLM, n0 = ((pid % gsize) / gm) * kLN;
-  if (f.tri == 1 && m0 + kLM - 1 + f.tri_off < n0) return;
-  if (f.tri == 2 && m0 + f.tri_off >= n0 + kLN - 1) return;
-  extern __shared__ unsigned char smem_raw[];
-  const uint32_t base_s = smem_u32(smem_raw);
-  unsigned char *smem = smem_raw + ((1024 - (base_s & 1023)) & 1023);
-  unsigned char *sA = smem;                                // [2][kLSmax] chunks
-  unsigned char *sB = smem + 2 * kLSmax * kLChunk;         // [2][kLSmax] chunks
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + 2 * kLSmax * kLChunk);  // [2]
-  uint64_t *empty = full + 2;                                               // [2]
-  uint64_t *tfull = empty + 2;                                              // [4]
-  uint64_t *tempty = tfull + 4;                                             // [4]
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = f.S;
-  const int nkb = (int)(f.Kp / kLK);
-  const int ngrp = (S + 3) / 4;
-
-  if (warp == 0 && lane == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], 1);
-    }
-    for (int j = 0; j < 4; ++j) {
-      mbar_init(&tfull[j], 1);
-      mbar_init(&tempty[j], 8);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int use = 0;
-      for (int g = 0; g < ngrp; ++g) {
-        const int ns = S - 4 * g;  // slices 0 .. hi of both operands
-        for (int kb = 0; kb < nkb; ++kb, ++use) {
-          const int bb = use & 1;
-          if (use >= 2) mbar_wait(&empty[bb], (uint32_t)(((use >> 1) - 1) & 1));
-          mbar_arrive_expect_tx(&full[bb], (uint32_t)(2 * ns) * kLChunk);
-          for (int t = 0; t < ns; ++t) {
-            const int32_t kc = (int32_t)(t * f.Kp + (int64_t)kb * kLK);
-            tc::tma_load_2d(sA + (bb * kLSmax + t) * kLChunk, &tmA, kc, (int32_t)m0, &full[bb]);
-            tc::tma_load_2d(sB + (bb * kLSmax + t) * kLChunk, &tmB, kc, (int32_t)n0, &full[bb]);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_i8(kLM, kLN);
-      int use = 0;
-      for (int g = 0; g < ngrp; ++g) {
-        const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0;
-        if (g > 0)
-          for (int j = 0; j <= hi - lo; ++j) mbar_wait(&tempty[j], (uint32_t)((g - 1) & 1));
-        tc::fence_after();
-        for (int kb = 0; kb < nkb; ++kb, ++use) {
-          const int bb = use & 1;
-          mbar_wait(&full[bb], (uint32_t)((use >> 1) & 1));
-          tc::fence_after();
-          const uint64_t ad = sdesc_k_sw32(smem_u32(sA + bb * kLSmax * kLChunk));
-          const uint64_t bd = sdesc_k_sw32(smem_u32(sB + bb * kLSmax * kLChunk));
-          for (int h = hi; h >= lo; --h) {  // level-major: consecutive MMAs share the accumulator
-            const uint32_t td = tmem + (uint32_t)((hi - h) * kLN);
-            for (int c = 0; c <= h; ++c)
-              tc::mma_i8(td, ad + (uint64_t)(c * (kLChunk >> 4)), bd + (uint64_t)((h - c) * (kLChunk >> 4)), idesc,
-                         (kb > 0 || c > 0) ? 1u : 0u);
-          }
-          tc::mma_commit(&empty[bb]);
-        }
-        for (int j = 0; j <= hi - lo; ++j) tc::mma_commit(&tfull[j]);
-      }
-    }
-  } else {
-    const int q = warp & 3, half = (warp - 2) >> 2;
-    const int64_t row = m0 + q * 32 + lane;
-    double acc[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) acc[j] = 0.0;
-    for (int g = 0; g < ngrp; ++g) {
-      const int hi = S - 1 - 4 * g, lo = hi - 3 > 0 ? hi - 3 : 0;
-      for (int h = hi; h >= lo; --h) {
-        const int jb = hi - h;
-        mbar_wait(&tfull[jb], (uint32_t)(g & 1));
-        tc::fence_after();
-        const double sc = scalbn(1.0, -12 - 7 * h);
-#pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t v[32];
-          tc::tmem_ld32(tmem + (uint32_t)(jb * kLN + half * 64 + c) + ((uint32_t)(q * 32) << 16), v);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[c + j] = __dadd_rn(acc[c + j], __dmul_rn((double)(int32_t)v[j], sc));
-        }
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[jb]);
-      }
-    }
-    if (row < f.M) {
-      const int ea = f.ea[row];
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const int64_t col = n0 + half * 64 + j;
-        bool keep = col < f.N;
-        if (f.tri != 0) {
-          const int64_t gr = row + f.tri_off;
-          keep = keep && (f.tri == 1 ? gr >= col : gr < col);
-        }
-        if (keep) {
-          const double tot = scalbn(acc[j], ea + f.eb[col]);
-          double out = __dmul_rn(f.alpha, tot);
-          if (f.beta != 0.0) out = __dadd_rn(out, __dmul_rn(f.beta, f.Cin[row * f.ldcin + col]));
-          if (f.diag != 0.0 && row - col == f.diag_offset) out = __dadd_rn(out, f.diag);
-          f.C[row * f.ldc + col] = out;
-        }
-      }
-    }
-  }
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, 512);
-}
-
-// ------------------------------------------------------------------ level groups, v2
-// The level-group kernel above with the slices stored chunk-interleaved: row r holds,
-// for each 32-wide K chunk kb, the S slices' 32 bytes side by side
-// (out[r][kb S 32 + s 32 + kk]), so one K chunk of 4 slices is ONE 128-byte TMA box row
-// (SWIZZLE_128B, the fused kernel's tile shape) instead of four 32-byte box rows; a
-// 3-stage ring of chunk sets (64 KiB each).  Same slice pairs, same level order, same
-// fp64 epilogue: bitwise the fused kernel's C.
 constexpr int kL2Stages = 3;
 constexpr uint32_t kL2Box = 128 * 128;                 // 16 KiB: 128 rows x 4 slices x 32 B
 constexpr uint32_t kL2Stage = 4 * kL2Box;              // A boxes 0, 1 + B boxes 0, 1
@@ -703,14 +548,13 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
   // profiles/r02_ozaki_lv2.txt), so v2 serves the large products only (M N K >= 2^40);
   // `kernel` (diagnostic) forces one: 0 fused, 1 level groups, 2 level groups v2
   const bool big = (double)M * (double)N * (double)K >= 1099511627776.0;
-  const bool lv2 = S <= kLSmax && (kernel >= 0 ? kernel == 2 : big);
-  const bool lv = S <= kLSmax && kernel == 1;
+  const bool lv2 = S <= kLSmax && (kernel >= 0 ? kernel != 0 : big);
   // scales and digit slices (A rows: K-contiguous; op(B) columns: B rows if !b_kn);
   // (B slices in reverse order for the level-streaming kernels: level h's pairs are a
   // contiguous K range; forward order for the level-group kernels, chunk-interleaved for v2)
   launch_ozaki_split(g.A, g.lda, M, K, 0, S, 0, As, ea, Kp, s, nullptr, lv2 ? 1 : 0);
   // (an exactly symmetric B: op(B)'s columns are B's rows, sliced by the row kernels)
-  launch_ozaki_split(g.B, g.ldb, N, K, (b_kn && !g.b_sym) ? 1 : 0, S, (lv || lv2) ? 0 : 1, Bs, eb, Kp, s, nullptr,
+  launch_ozaki_split(g.B, g.ldb, N, K, (b_kn && !g.b_sym) ? 1 : 0, S, lv2 ? 0 : 1, Bs, eb, Kp, s, nullptr,
                      lv2 ? 1 : 0);
   if (lv2) {
     static bool attr = false;
@@ -728,27 +572,6 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
     f.tri = g.tri; f.tri_off = g.tri_off;
     const unsigned grid = (unsigned)(((N + kLN - 1) / kLN) * ((M + kLM - 1) / kLM));
     ozaki_lv2_kernel<<<grid, kLThreads, kL2Smem, s>>>(ta, tb, f);
-    cudaFreeAsync(As, s);
-    cudaFreeAsync(Bs, s);
-    cudaFreeAsync(ea, s);
-    return cudaGetLastError();
-  }
-  if (lv) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(ozaki_lv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
-      attr = true;
-    }
-    CUtensorMap ta, tb;
-    const int64_t ldo = (int64_t)S * Kp;
-    if (!make_tmap_s8_k32(&ta, As, M, ldo, ldo, kLM) || !make_tmap_s8_k32(&tb, Bs, N, ldo, ldo, kLN))
-      return cudaErrorInvalidValue;
-    FusedArgs f{};
-    f.M = M; f.N = N; f.Kp = Kp; f.S = S; f.ea = ea; f.eb = eb; f.C = g.C; f.ldc = g.ldc; f.Cin = g.Cin;
-    f.ldcin = g.ldcin; f.alpha = g.alpha; f.beta = g.beta; f.diag = g.diag; f.diag_offset = g.diag_offset;
-    f.tri = g.tri; f.tri_off = g.tri_off;
-    const unsigned grid = (unsigned)(((N + kLN - 1) / kLN) * ((M + kLM - 1) / kLM));
-    ozaki_lv_kernel<<<grid, kLThreads, kLSmem, s>>>(ta, tb, f);
     cudaFreeAsync(As, s);
     cudaFreeAsync(Bs, s);
     cudaFreeAsync(ea, s);
