@@ -374,8 +374,8 @@ cudaError_t launch_igemm_epi(const int8_t *A, int64_t lda, const int8_t *B, int6
                              const IgemmEpi &e, cudaStream_t s);
 
 // ---------------------------------------------------------------- ozaki.cu
-// C = alpha A op(B) + beta Cin + diag (GemmArgs semantics, tri honoured; lower_only not
-// supported) in fp64 emulated on the int8 tensor cores: rows scaled by powers of two,
+// C = alpha A op(B) + beta Cin + diag (GemmArgs semantics, tri honoured; lower_only as
+// tri = 1, no entry above the diagonal written) in fp64 emulated on the int8 tensor cores: rows scaled by powers of two,
 // split into S signed 7-bit digit slices, all slice products with s + t <= S - 1
 // (0-based) accumulated exactly in int32 per digit level, levels summed in fp64.
 cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t s, int kernel = -1);

@@ -520,7 +520,9 @@ void launch_ozaki_split(const double *X, int64_t ld, int64_t rows, int64_t K, in
 }
 
 bool ozaki_eligible(const GemmArgs &g) {
-  if (g.lower_only || g.dmma_only) return false;
+  // (lower_only -- the Cholesky trailing updates C -= P P^T -- runs as tri = 1: only the
+  // entries on or below the diagonal are formed and written)
+  if (g.dmma_only) return false;
   // pays above ~2^32 multiply-adds, with K long enough to amortize the slicing and
   // both output dimensions >= 512 (each input is re-sliced per call: a skinny product
   // such as the block solve's K X with 64 right-hand sides would re-slice the large
@@ -569,7 +571,7 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
     FusedArgs f{};
     f.M = M; f.N = N; f.Kp = Kp; f.S = S; f.ea = ea; f.eb = eb; f.C = g.C; f.ldc = g.ldc; f.Cin = g.Cin;
     f.ldcin = g.ldcin; f.alpha = g.alpha; f.beta = g.beta; f.diag = g.diag; f.diag_offset = g.diag_offset;
-    f.tri = g.tri; f.tri_off = g.tri_off;
+    f.tri = g.lower_only ? 1 : g.tri; f.tri_off = g.lower_only ? 0 : g.tri_off;
     const unsigned grid = (unsigned)(((N + kLN - 1) / kLN) * ((M + kLM - 1) / kLM));
     ozaki_lv2_kernel<<<grid, kLThreads, kL2Smem, s>>>(ta, tb, f);
     cudaFreeAsync(As, s);
@@ -590,7 +592,7 @@ cudaError_t launch_ozaki_gemm(const GemmArgs &g, bool b_kn, int S, cudaStream_t 
     FusedArgs f{};
     f.M = M; f.N = N; f.Kp = Kp; f.S = S; f.ea = ea; f.eb = eb; f.C = g.C; f.ldc = g.ldc; f.Cin = g.Cin;
     f.ldcin = g.ldcin; f.alpha = g.alpha; f.beta = g.beta; f.diag = g.diag; f.diag_offset = g.diag_offset;
-    f.tri = g.tri; f.tri_off = g.tri_off;
+    f.tri = g.lower_only ? 1 : g.tri; f.tri_off = g.lower_only ? 0 : g.tri_off;
     const unsigned grid = (unsigned)(((N + kFN - 1) / kFN) * ((M + kFM - 1) / kFM));
     ozaki_fused_kernel<<<grid, kFThreads, kFSmem, s>>>(ta, tb, f);
     cudaFreeAsync(As, s);
