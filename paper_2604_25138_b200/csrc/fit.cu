@@ -605,9 +605,15 @@ laker_status fit_learned(laker_ctx ctx, const laker_fit_opts &o, laker_fit_repor
   }
   // L_tot = L1 L2 L3 (R = L_tot^T)
   {
+    // products of lower-triangular factors are lower triangular: only the tiles on or below
+    // the diagonal are formed (tri = 1; the strict upper parts are zeroed first -- the same
+    // lower entries, exact zeros above)
+    LAKER_CUDA(ctx, cudaMemsetAsync(X, 0, sq * 8, s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(Rt, 0, sq * 8, s));
     GemmArgs g{};
     g.M = nrp; g.N = nrp; g.K = nrp; g.A = L1; g.lda = nrp; g.B = L2; g.ldb = nrp; g.C = X; g.ldc = nrp;
     g.alpha = 1.0;
+    g.tri = 1;
     launch_dgemm(g, true, s);
     g.A = X; g.B = L3; g.C = Rt;
     launch_dgemm(g, true, s);
