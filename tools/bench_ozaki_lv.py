@@ -10,7 +10,8 @@ import torch  # noqa: E402
 
 from paper_2604_25138_b200 import laker as L  # noqa: E402
 
-shapes = [(4096, 4096, 4096), (4096, 4096, 16384), (4096, 16384, 16384), (1000, 777, 1300)]
+shapes = [(4096, 4096, 4096), (4096, 4096, 16384), (4096, 16384, 16384), (3584, 16384, 512), (7680, 3584, 512),
+          (1000, 777, 1300), (130, 4000, 600)]
 kernels = [int(k) for k in os.environ.get("KERNELS", "0,2").split(",")]
 reps = int(os.environ.get("REPS", "5"))
 for M, N, K in shapes:
