@@ -18,12 +18,17 @@ Line citations "P:n" are to /root/reference/PAPER.md (LaTeX of arXiv
       iteration runs on (a_t, b_t) with the N_r x N_r matrix
       T_t = a_t I + R diag(b_t) R^T after one thin QR U = Q R.  Pinned against
       the literal form in tests/test_oracle_fit.py.
+* `block_pcg`: O'Leary's block PCG (1980) for the C4 block-CG variant, plain numpy;
+  pinned by its one-column case (= Alg. 1's PCG, `pcg`), finite termination on a
+  spectrum of k distinct eigenvalues (<= ceil(k/m) steps), an exact preconditioner
+  (one step) and the dense solve (tests/test_oracle_block_cg.py).
 * `reference_solve`: dense Cholesky solve of (lambda I + K) alpha = y, the
   stand-in for the paper's CVXPY reference.
 """
 from __future__ import annotations
 
 import ctypes
+from collections import namedtuple
 import math
 import os
 import subprocess
@@ -40,7 +45,7 @@ __all__ = [
     "TERM_INDEFINITE", "rho_schedule", "nr_schedule", "directions", "cccp_step_literal",
     "cccp_fit_literal",
     "cccp_fit_structured", "FitReport", "reference_solve", "cond_spd", "cond_precond",
-    "objective", "residual", "num_threads",
+    "objective", "residual", "num_threads", "block_pcg", "BlockPcgReport",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -476,3 +481,62 @@ def residual(K, lam: float, alpha, y) -> float:
     """Res = ||(lambda I + G) alpha - y|| / ||y|| (Eq. residual, P:804-808)."""
     r = K @ alpha + lam * alpha - y
     return float(np.linalg.norm(r) / np.linalg.norm(y))
+
+
+BlockPcgReport = namedtuple("BlockPcgReport", "iters termination rel_residual true_rel_residual")
+
+
+def block_pcg(K, lam: float, Y, precond=None, tol: float = 1e-8, max_iters: Optional[int] = None):
+    """Block PCG (O'Leary, "The block conjugate gradient algorithm and related methods",
+    Linear Algebra Appl. 29, 1980, Alg. BPCG) for (lambda I + K) X = Y with the m columns
+    of Y sharing one block Krylov space -- the block-CG variant of C4 (SURVEY §8(f)
+    NEXT-4, reading R13's alternative).  `precond(R)` returns P R (None: P = I).
+    Written out as published, with m x m solves by Cholesky:
+        X0 = 0, R0 = Y, Z0 = P R0, D0 = Z0
+        Q = A D_k;  alpha_k = (D_k^T Q)^{-1} (Z_k^T R_k)
+        X_{k+1} = X_k + D_k alpha_k;  R_{k+1} = R_k - Q alpha_k
+        Z_{k+1} = P R_{k+1};  beta_k = (Z_k^T R_k)^{-1} (Z_{k+1}^T R_{k+1})
+        D_{k+1} = Z_{k+1} + D_k beta_k
+    stopping when every column has ||R_c|| / ||Y_c|| <= tol.  Termination: RESIDUAL_TOL,
+    MAX_ITERS, or BREAKDOWN when an m x m Gram matrix is not numerically positive definite.
+    Plain numpy (test infrastructure, no Dot2: block CG is compared within a tolerance)."""
+    K = np.asarray(K, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    if Y.ndim == 1:
+        Y = Y[:, None]
+    n, m = Y.shape
+    max_iters = 10 * n if max_iters is None else int(max_iters)
+    A = lambda V: K @ V + lam * V  # noqa: E731
+    P = (lambda V: V) if precond is None else precond  # noqa: E731
+    ynorm = np.linalg.norm(Y, axis=0)
+    X = np.zeros((n, m))
+    R = Y.copy()
+    Z = P(R)
+    D = Z.copy()
+    Gzr = Z.T @ R
+    term, it = TERM_MAX_ITERS, 0
+    rel = np.linalg.norm(R, axis=0) / ynorm
+    for it in range(1, max_iters + 1):
+        Q = A(D)
+        try:
+            alpha = sla.cho_solve(sla.cho_factor(D.T @ Q, lower=True), Gzr)
+        except np.linalg.LinAlgError:
+            term = TERM_BREAKDOWN
+            break
+        X = X + D @ alpha
+        R = R - Q @ alpha
+        rel = np.linalg.norm(R, axis=0) / ynorm
+        if np.all(rel <= tol):
+            term = TERM_RESIDUAL_TOL
+            break
+        Z = P(R)
+        Gzr_new = Z.T @ R
+        try:
+            beta = sla.cho_solve(sla.cho_factor(Gzr, lower=True), Gzr_new)
+        except np.linalg.LinAlgError:
+            term = TERM_BREAKDOWN
+            break
+        D = Z + D @ beta
+        Gzr = Gzr_new
+    true = np.linalg.norm(Y - A(X), axis=0) / ynorm
+    return X, BlockPcgReport(it, term, rel, true)
