@@ -199,6 +199,26 @@ laker_status laker_pcg_solve(laker_ctx ctx, int32_t nrhs, const double *Y, doubl
                              const laker_solve_opts *opts, laker_solve_report *reports,
                              double *history);
 
+/* Block-CG variant of the multi-RHS solve (C4): O'Leary's block PCG
+   (Linear Algebra Appl. 29, 1980) -- the nrhs columns of Y share one block Krylov space:
+   X0 = 0, R0 = Y, Z0 = P R0, D0 = Z0; per iteration Q = (lambda I + K) D,
+   alpha = (D^T Q)^{-1} (Z^T R), X += D alpha, R -= Q alpha, Z = P R,
+   beta = (Z_old^T R_old)^{-1} (Z^T R), D = Z + D beta, with the operator / preconditioner
+   products of laker_pcg_solve's block solve and the nrhs x nrhs Gram matrices and SPD
+   solves on the device; stops when every column has ||R_c|| / ||Y_c|| <= tol (R12's
+   test, column-wise).  Not Alg. 1 column by column: compared with the oracle's block PCG
+   (oracle.block_pcg) within a tolerance, never bitwise.  block (dividing nrhs; 0 = nrhs):
+   the columns form nrhs / block independent groups of `block` columns, each its own block
+   recurrence (the Gram matrices masked to their block x block diagonal blocks), all groups
+   sharing every pass over K and P -- one group of 64 right-hand sides can lose rank and
+   break down (C4), groups of 8 do not.  One rank, MATERIALIZED K, 1 <= nrhs <= 64.  Y, alpha, reports (all columns report the shared iteration count)
+   and history (column 0) as laker_pcg_solve.  Errors: INVALID_ARGUMENT, NOT_READY;
+   BREAKDOWN_ZERO_CURVATURE when D^T (lambda I + K) D, INDEFINITE_PRECONDITIONER when
+   Z^T R is not numerically positive definite (last iterate in alpha). */
+laker_status laker_block_cg_solve(laker_ctx ctx, int32_t nrhs, int32_t block, const double *Y, double *alpha,
+                                  const laker_solve_opts *opts, laker_solve_report *reports,
+                                  double *history);
+
 /* --------------------------------------------------------------- (4) predict */
 /* r_hat(x_m) = sum_i exp(scale <eq_m, e_i>) alpha_i (Eq. sc-radio-map-
    reconstruction; Alg.1 l.24), entries recomputed on the

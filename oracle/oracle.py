@@ -486,7 +486,8 @@ def residual(K, lam: float, alpha, y) -> float:
 BlockPcgReport = namedtuple("BlockPcgReport", "iters termination rel_residual true_rel_residual")
 
 
-def block_pcg(K, lam: float, Y, precond=None, tol: float = 1e-8, max_iters: Optional[int] = None):
+def block_pcg(K, lam: float, Y, precond=None, tol: float = 1e-8, max_iters: Optional[int] = None,
+              plain: bool = False):
     """Block PCG (O'Leary, "The block conjugate gradient algorithm and related methods",
     Linear Algebra Appl. 29, 1980, Alg. BPCG) for (lambda I + K) X = Y with the m columns
     of Y sharing one block Krylov space -- the block-CG variant of C4 (SURVEY §8(f)
@@ -499,14 +500,22 @@ def block_pcg(K, lam: float, Y, precond=None, tol: float = 1e-8, max_iters: Opti
         D_{k+1} = Z_{k+1} + D_k beta_k
     stopping when every column has ||R_c|| / ||Y_c|| <= tol.  Termination: RESIDUAL_TOL,
     MAX_ITERS, or BREAKDOWN when an m x m Gram matrix is not numerically positive definite.
-    Plain numpy (test infrastructure, no Dot2: block CG is compared within a tolerance)."""
+    The operator applies A D column by column with `apply` (one Dot2 per row, as Alg. 1's
+    products, R17) unless `plain` (numpy K @ D); Gram matrices and m x m solves plain numpy.
+    Block CG's step count is sensitive to the products' rounding (n = 1024, m = 8, Jacobi:
+    168 steps with Dot2 products, 203 with plain ones), so the GPU is compared within an
+    envelope, never bitwise."""
     K = np.asarray(K, dtype=np.float64)
     Y = np.asarray(Y, dtype=np.float64)
     if Y.ndim == 1:
         Y = Y[:, None]
     n, m = Y.shape
     max_iters = 10 * n if max_iters is None else int(max_iters)
-    A = lambda V: K @ V + lam * V  # noqa: E731
+    if plain:
+        A = lambda V: K @ V + lam * V  # noqa: E731
+    else:
+        A = lambda V: np.column_stack([apply(K, lam, np.ascontiguousarray(V[:, c]))  # noqa: E731
+                                       for c in range(V.shape[1])])
     P = (lambda V: V) if precond is None else precond  # noqa: E731
     ynorm = np.linalg.norm(Y, axis=0)
     X = np.zeros((n, m))

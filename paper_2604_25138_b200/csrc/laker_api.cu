@@ -469,6 +469,30 @@ laker_status laker_fit_preconditioner(laker_ctx ctx, const laker_fit_opts *opts,
   }
 }
 
+laker_status laker_block_cg_solve(laker_ctx ctx, int32_t nrhs, int32_t block, const double *Y, double *alpha,
+                                  const laker_solve_opts *opts, laker_solve_report *reports, double *history) {
+  CHECK_CTX(ctx);
+  if (!ctx->assembled) return set_err(ctx, LAKER_ERR_NOT_READY, "block CG: assemble the kernel first");
+  if (ctx->comm || ctx->world > 1) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "block CG: one rank only");
+  if (ctx->storage != LAKER_STORE_MATERIALIZED) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "block CG needs MATERIALIZED");
+  if (nrhs < 1 || nrhs > 64 || !Y || !alpha || !opts || !(opts->tol > 0.0 && opts->tol < 1.0) || opts->max_iters < 0)
+    return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "block CG: need 1 <= nrhs <= 64, Y, alpha, 0 < tol < 1");
+  if (block < 0 || block > nrhs || (block > 0 && nrhs % block != 0))
+    return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "block CG: block must divide nrhs (0: one block of nrhs)");
+  cudaSetDevice(ctx->device);
+  const int64_t n = ctx->n;
+  DevView yv, av;
+  LAKER_TRY(view_in(ctx, Y, (size_t)n * nrhs, yv));
+  LAKER_TRY(view_out(ctx, alpha, (size_t)n * nrhs, av));
+  laker_status sb = laker::pcg_solve_block(ctx, nrhs, yv.dptr, av.dptr, *opts, reports, history,
+                                             block > 0 ? block : nrhs);
+  if (sb == LAKER_OK || sb == LAKER_ERR_BREAKDOWN_ZERO_CURVATURE || sb == LAKER_ERR_INDEFINITE_PRECONDITIONER) {
+    LAKER_TRY(flush_out(ctx, av));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  return sb;
+}
+
 laker_status laker_pcg_solve(laker_ctx ctx, int32_t nrhs, const double *Y, double *alpha,
                              const laker_solve_opts *opts, laker_solve_report *reports, double *history) {
   CHECK_CTX(ctx);

@@ -452,7 +452,7 @@ laker_status apply_operator_dist(laker_ctx ctx, const double *x, double *y);
 // ------------------------------------------------------------- pcg_block.cu
 // nrhs independent recurrences sharing GEMM-shaped applies (multi-RHS, C4).
 laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *alpha,
-                             const laker_solve_opts &o, laker_solve_report *reps, double *history);
+                             const laker_solve_opts &o, laker_solve_report *reps, double *history, int block_cg = 0);
 // the row-sharded version (ctx->comm): K / P / vectors by row blocks, rank-order combines
 laker_status pcg_solve_block_dist(laker_ctx ctx, int32_t m, const double *Y, double *alpha,
                                   const laker_solve_opts &o, laker_solve_report *reps, double *history);

@@ -469,10 +469,155 @@ __global__ void block_pupdate_kernel(int64_t n, int64_t m, int64_t ldv, const do
   }
 }
 
+// ---------------------------------------------------------------- block CG (O'Leary)
+// The block-CG variant of C4 (O'Leary, Linear Algebra Appl. 29, 1980):
+// the m columns share one block Krylov space, every step needs the m x m Gram matrices
+// D^T Q, Z^T R (and R^T R for the stopping test) and two m x m SPD solves.  Grams: each CTA
+// sums its rows' outer products in a fixed order, partials reduced in CTA order; the
+// solves: one CTA (Cholesky + substitutions); the block updates V +- D C: one pass per row
+// block with the m x m coefficients in shared memory.  m <= 64.
+constexpr int kBcgGrid = 128;
+
+// part[g] = sum over the rows of CTA g of A[i][:]^T B[i][:] (64 x 64, columns >= m zero)
+__global__ void __launch_bounds__(256) bcg_gram_kernel(const double *__restrict__ A, const double *__restrict__ B,
+                                                       int64_t n, int m, int64_t ld, double *__restrict__ part) {
+  __shared__ double As[32][65], Bs[32][65];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double acc[4][4] = {};
+  for (int64_t i0 = (int64_t)blockIdx.x * 32; i0 < n; i0 += (int64_t)gridDim.x * 32) {
+    for (int e = tid; e < 32 * 64; e += 256) {
+      const int r = e >> 6, c = e & 63;
+      const bool ok = i0 + r < n && c < m;
+      As[r][c] = ok ? A[(i0 + r) * ld + c] : 0.0;
+      Bs[r][c] = ok ? B[(i0 + r) * ld + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 0; r < 32; ++r) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[r][4 * ty + u];
+        b[u] = Bs[r][4 * tx + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = __fma_rn(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+  double *o = part + (int64_t)blockIdx.x * 4096;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o[(4 * ty + u) * 64 + 4 * tx + v] = acc[u][v];
+}
+
+// out = the reduced Gram, masked to its bs x bs diagonal blocks (column groups of bs solved
+// as independent block recurrences: a block-diagonal Gram keeps every factor and
+// coefficient block-diagonal)
+__global__ void bcg_gram_reduce_kernel(const double *__restrict__ part, int G, int bs, double *__restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4096) return;
+  double v = 0.0;
+  if ((e >> 6) / bs == (e & 63) / bs)
+    for (int g = 0; g < G; ++g) v = __dadd_rn(v, part[(int64_t)g * 4096 + e]);
+  out[e] = v;
+}
+
+// X = G^{-1} B for the m x m SPD G (64 x 64 storage): Cholesky in shared memory, then one
+// thread per right-hand-side column for the two triangular solves; *fail = 1 when a pivot
+// is not positive (G not numerically positive definite: breakdown)
+// Columns of a converged (frozen) group: their rows / columns of G are replaced by the
+// identity's and their rows of B by zeros, so their coefficients are zero (no update).
+__global__ void __launch_bounds__(256) bcg_spd_solve_kernel(const double *__restrict__ G, const double *__restrict__ B,
+                                                            double *__restrict__ X, int m, int *fail,
+                                                            const int *__restrict__ frozen) {
+  __shared__ double L[64][65];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 4096; e += 256) {
+    const int i = e >> 6, k = e & 63;
+    L[i][k] = (frozen[i] || frozen[k]) ? (i == k ? 1.0 : 0.0) : G[e];
+  }
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    const double d = L[j][j];
+    if (!(d > 0.0)) {
+      if (tid == 0) *fail = 1;
+      return;  // uniform: every thread read the same pivot
+    }
+    const double piv = __dsqrt_rn(d);
+    __syncthreads();
+    if (tid == 0) L[j][j] = piv;
+    if (tid > j && tid < m) L[tid][j] = __ddiv_rn(L[tid][j], piv);
+    __syncthreads();
+    for (int e = tid; e < 4096; e += 256) {
+      const int i = e >> 6, k = e & 63;
+      if (i > j && i < m && k > j && k <= i) L[i][k] = __fma_rn(-L[i][j], L[k][j], L[i][k]);
+    }
+    __syncthreads();
+  }
+  if (tid < 64) {
+    const int c = tid;
+    double y[64];
+    for (int i = 0; i < m; ++i) {
+      double v = (c < m && !frozen[i] && !frozen[c]) ? B[i * 64 + c] : 0.0;
+      for (int k = 0; k < i; ++k) v = __fma_rn(-L[i][k], y[k], v);
+      y[i] = __ddiv_rn(v, L[i][i]);
+    }
+    for (int i = m - 1; i >= 0; --i) {
+      double v = y[i];
+      for (int k = i + 1; k < m; ++k) v = __fma_rn(-L[k][i], y[k], v);
+      y[i] = __ddiv_rn(v, L[i][i]);
+    }
+    for (int i = 0; i < 64; ++i) X[i * 64 + c] = (i < m && c < m) ? y[i] : 0.0;
+  }
+}
+
+// out[i][c] = add[i][c] + sgn sum_{k < m} D[i][k] C[k][c]  (c < m; out may alias add, not D)
+__global__ void __launch_bounds__(256) bcg_update_kernel(double *out, const double *add, const double *__restrict__ D,
+                                                         const double *__restrict__ C, int64_t n, int m, int64_t ld,
+                                                         double sgn) {
+  __shared__ double Cs[64][64];
+  __shared__ double Ds[16][65];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 4096; e += 256) Cs[e >> 6][e & 63] = C[e];
+  const int r = tid >> 4, c0 = (tid & 15) * 4;
+  for (int64_t i0 = (int64_t)blockIdx.x * 16; i0 < n; i0 += (int64_t)gridDim.x * 16) {
+    __syncthreads();
+    for (int e = tid; e < 16 * 64; e += 256) {
+      const int rr = e >> 6, k = e & 63;
+      Ds[rr][k] = (i0 + rr < n && k < m) ? D[(i0 + rr) * ld + k] : 0.0;
+    }
+    __syncthreads();
+    const int64_t i = i0 + r;
+    if (i >= n) continue;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < m; ++k) {
+      const double dk = Ds[r][k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __fma_rn(dk, Cs[k][c0 + u], v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < m) out[i * ld + c0 + u] = __fma_rn(sgn, v[u], add[i * ld + c0 + u]);
+  }
+}
+
+__global__ void bcg_jacobi_kernel(double *__restrict__ th, const double *__restrict__ r,
+                                  const double *__restrict__ dvec, int64_t n, int m, int64_t ld) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m;
+    const int c = (int)(e % m);
+    th[i * ld + c] = __dmul_rn(dvec[i], r[i * ld + c]);
+  }
+}
+
 }  // namespace
 
+
 laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *alpha_out,
-                             const laker_solve_opts &o, laker_solve_report *reps, double *history) {
+                             const laker_solve_opts &o, laker_solve_report *reps, double *history, int block_cg) {
   if (ctx->comm) return pcg_solve_block_dist(ctx, m, Y, alpha_out, o, reps, history);
   if (ctx->world != 1) return set_err(ctx, LAKER_ERR_NOT_READY, "multi-RHS: detached shard (no NCCL communicator)");
   if (ctx->storage != LAKER_STORE_MATERIALIZED) return set_err(ctx, LAKER_ERR_INVALID_ARGUMENT, "multi-RHS needs MATERIALIZED");
@@ -644,6 +789,167 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
     gemm(ctx->Qr, ldq, n, nrp, ctx->f_ainv, wb, R, Th, true);
   };
   const int vg = 2 * ctx->num_sms;
+  if (block_cg) {
+    // ------------------------------------------------ block CG (oracle.block_pcg)
+    // X0 = 0, R0 = Y, Z0 = P R0, D0 = Z0; Q = A D; alpha = (D^T Q)^{-1} (Z^T R);
+    // X += D alpha; R -= Q alpha; stop when every ||R_c|| / ||Y_c|| <= tol; Z = P R;
+    // beta = (Z_old^T R_old)^{-1} (Z^T R); D = Z + D beta.  Products as the batched solve's.
+    double *sm = nullptr, *d2 = nullptr;
+    int *fail = nullptr;  // [0] breakdown flag, [1 .. 64] frozen (converged) columns
+    LAKER_CUDA(ctx, cudaMallocAsync(&sm, ((size_t)kBcgGrid * 4096 + 6 * 4096) * sizeof(double), s));
+    LAKER_CUDA(ctx, cudaMallocAsync(&d2, blk * sizeof(double), s));
+    LAKER_CUDA(ctx, cudaMallocAsync(&fail, 65 * sizeof(int), s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(d2, 0, blk * sizeof(double), s));
+    LAKER_CUDA(ctx, cudaMemsetAsync(fail, 0, 65 * sizeof(int), s));
+    int *frozen = fail + 1;
+    std::vector<int> hfrozen(64, 0);
+    double *gpart = sm, *Gzr = sm + (size_t)kBcgGrid * 4096, *Gnew = Gzr + 4096, *Gpq = Gnew + 4096,
+           *Grr = Gpq + 4096, *Am = Grr + 4096, *Bm = Am + 4096;
+    const int bs = (block_cg > 0 && block_cg < m) ? block_cg : m;  // column groups of bs
+    auto gram = [&](const double *A, const double *B, double *out) {
+      bcg_gram_kernel<<<kBcgGrid, 256, 0, s>>>(A, B, n, m, mp, gpart);
+      bcg_gram_reduce_kernel<<<16, 256, 0, s>>>(gpart, kBcgGrid, bs, out);
+      ctx->stats.kernel_launches += 2;
+    };
+    auto spd_solve = [&](const double *G, const double *B, double *X) {
+      bcg_spd_solve_kernel<<<1, 256, 0, s>>>(G, B, X, m, fail, frozen);
+      ctx->stats.kernel_launches++;
+    };
+    auto upd = [&](double *out, const double *add, const double *D, const double *C, double sgn) {
+      bcg_update_kernel<<<(unsigned)std::min<int64_t>(2 * ctx->num_sms, (n + 15) / 16), 256, 0, s>>>(
+          out, add, D, C, n, m, mp, sgn);
+      ctx->stats.kernel_launches++;
+    };
+    auto precond = [&](const double *R) -> const double * {  // Z = P R
+      if (dense) {
+        apply_p(R, th);
+        return th;
+      }
+      if (pk == LAKER_PRECOND_JACOBI) {
+        bcg_jacobi_kernel<<<vg, 256, 0, s>>>(th, R, ctx->Pdiag, n, m, mp);
+        ctx->stats.kernel_launches++;
+        return th;
+      }
+      return R;
+    };
+    cudaEvent_t b0, b1;
+    cudaEventCreate(&b0);
+    cudaEventCreate(&b1);
+    cudaEventRecord(b0, s);
+    col(kColInit);  // X = 0, R = Y
+    std::vector<double> hg(4096), ynorm(m);
+    gram(rr, rr, Grr);
+    LAKER_CUDA(ctx, cudaMemcpyAsync(hg.data(), Grr, 4096 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    for (int c = 0; c < m; ++c) ynorm[c] = std::sqrt(hg[c * 64 + c]);
+    const double *Z = precond(rr);
+    LAKER_CUDA(ctx, cudaMemcpyAsync(pp, Z, blk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    gram(Z, rr, Gzr);
+    int32_t it = 0, term = LAKER_TERM_MAX_ITERS;
+    std::vector<double> rel(m, 1.0);
+    double *D = pp, *Dn = d2;
+    int hfail = 0;
+    bool zero = false;
+    for (int c = 0; c < m; ++c) zero = zero || !(ynorm[c] > 0.0);
+    if (zero) term = LAKER_TERM_ZERO_RHS;
+    while (!zero && it < max_iters) {
+      if (tcb)
+        gemm_tc(sK, n, ctx->lambda, D, D, qq);
+      else
+        apply(ctx->K, ctx->lambda, D, qq, false);
+      gram(D, qq, Gpq);
+      spd_solve(Gpq, Gzr, Am);
+      upd(al, al, D, Am, 1.0);
+      upd(rr, rr, qq, Am, -1.0);
+      ++it;
+      gram(rr, rr, Grr);
+      LAKER_CUDA(ctx, cudaMemcpyAsync(hg.data(), Grr, 4096 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      LAKER_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+      LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+      if (hfail) {
+        term = LAKER_TERM_BREAKDOWN;
+        break;
+      }
+      bool all = true, newly = false;
+      for (int c = 0; c < m; ++c) {
+        rel[c] = std::sqrt(std::max(hg[c * 64 + c], 0.0)) / ynorm[c];
+        all = all && rel[c] <= o.tol;
+      }
+      for (int g0 = 0; g0 < m; g0 += bs) {  // a group whose columns all converged stops
+        bool gdone = true;
+        for (int c = g0; c < g0 + bs; ++c) gdone = gdone && rel[c] <= o.tol;
+        if (gdone && !hfrozen[g0]) {
+          for (int c = g0; c < g0 + bs; ++c) hfrozen[c] = 1;
+          newly = true;
+        }
+      }
+      if (newly && !all)
+        LAKER_CUDA(ctx, cudaMemcpyAsync(frozen, hfrozen.data(), 64 * sizeof(int), cudaMemcpyHostToDevice, s));
+      if (history) history[it - 1] = rel[0];
+      if (all) {
+        term = LAKER_TERM_RESIDUAL_TOL;
+        break;
+      }
+      Z = precond(rr);
+      gram(Z, rr, Gnew);
+      spd_solve(Gzr, Gnew, Bm);
+      upd(Dn, Z, D, Bm, 1.0);
+      std::swap(D, Dn);
+      std::swap(Gzr, Gnew);
+    }
+    LAKER_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    if (hfail && term != LAKER_TERM_BREAKDOWN) term = LAKER_TERM_INDEFINITE;  // Z^T R not positive definite
+    cudaEventRecord(b1, s);
+    apply(ctx->K, ctx->lambda, al, qq, false);
+    col(kColTrue);
+    LAKER_CUDA(ctx, cudaMemcpy2DAsync(alpha_out, sizeof(double), al, mp * sizeof(double), sizeof(double), n,
+                                      cudaMemcpyDeviceToDevice, s));
+    for (int32_t c = 1; c < m; ++c)
+      LAKER_CUDA(ctx, cudaMemcpy2DAsync(alpha_out + (size_t)c * n, sizeof(double), al + c, mp * sizeof(double),
+                                        sizeof(double), n, cudaMemcpyDeviceToDevice, s));
+    std::vector<double> htr(m);
+    LAKER_CUDA(ctx, cudaMemcpyAsync(htr.data(), trel, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, b0, b1);
+    ctx->stats.solve_ms = ms;
+    for (int32_t c = 0; c < m && reps; ++c) {
+      reps[c].iters = it;
+      reps[c].termination = term;
+      reps[c].rel_residual = zero ? 0.0 : rel[c];
+      reps[c].true_rel_residual = htr[c];
+      reps[c].seconds = ms * 1e-3;
+      reps[c].lanczos_lmin = reps[c].lanczos_lmax = 0.0;
+    }
+    cudaEventDestroy(b0);
+    cudaEventDestroy(b1);
+    cudaFreeAsync(sm, s);
+    cudaFreeAsync(d2, s);
+    cudaFreeAsync(fail, s);
+    cudaFreeAsync(base, s);
+    if (zb) cudaFreeAsync(zb, s);
+    if (rmK) cudaFreeAsync(rmK, s);
+    if (part) cudaFreeAsync(part, s);
+    oz_slices_free(sK, s);
+    oz_slices_free(sQt, s);
+    oz_slices_free(sM, s);
+    oz_slices_free(sQr, s);
+    oz_slices_free(sXn, s);
+    oz_slices_free(sXr, s);
+    if (mxb) cudaFreeAsync(mxb, s);
+    cudaFreeAsync(st, s);
+    cudaFreeAsync(hist, s);
+    cudaFreeAsync(trel, s);
+    cudaFreeAsync(all_done, s);
+    cudaFreeAsync(parts, s);
+    LAKER_CUDA(ctx, cudaStreamSynchronize(s));
+    if (term == LAKER_TERM_BREAKDOWN)
+      return set_err(ctx, LAKER_ERR_BREAKDOWN_ZERO_CURVATURE, "block CG: D^T (lambda I + K) D not positive definite");
+    if (term == LAKER_TERM_INDEFINITE)
+      return set_err(ctx, LAKER_ERR_INDEFINITE_PRECONDITIONER, "block CG: Z^T R not positive definite");
+    return LAKER_OK;
+  }
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
   cudaEventCreate(&ev1);

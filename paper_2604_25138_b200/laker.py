@@ -35,6 +35,7 @@ TERM_RESIDUAL_TOL, TERM_MAX_ITERS, TERM_ZERO_RHS, TERM_BREAKDOWN, TERM_INDEFINIT
 
 EXPORTED = ["laker_get_unique_id", "laker_create", "laker_destroy", "laker_status_string",
             "laker_last_error", "laker_assemble_kernel", "laker_fit_preconditioner", "laker_pcg_solve",
+            "laker_block_cg_solve",
             "laker_predict", "laker_load_kernel_rows", "laker_get_kernel_rows", "laker_set_preconditioner",
             "laker_get_preconditioner_rows", "laker_get_preconditioner_factors", "laker_get_preconditioner_qm",
             "laker_apply_operator",
@@ -99,6 +100,7 @@ def _load() -> ctypes.CDLL:
         "laker_assemble_kernel": [vp, i64, i32, vp, dbl, dbl, st, st],
         "laker_fit_preconditioner": [vp, ctypes.POINTER(FitOpts), ctypes.POINTER(FitReport)],
         "laker_pcg_solve": [vp, i32, vp, vp, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport), vp],
+        "laker_block_cg_solve": [vp, i32, i32, vp, vp, ctypes.POINTER(SolveOpts), ctypes.POINTER(SolveReport), vp],
         "laker_predict": [vp, i64, vp, vp, vp, st],
         "laker_load_kernel_rows": [vp, vp],
         "laker_get_kernel_rows": [vp, vp],
@@ -205,6 +207,18 @@ def laker_pcg_solve(ctx, nrhs: int, Y, alpha, tol: float, max_iters: int = 0, in
     o = SolveOpts(tol, max_iters, 1 if instrument else 0)
     reps = (SolveReport * nrhs)()
     s = lib.laker_pcg_solve(ctx, nrhs, _ptr(Y), _ptr(alpha), ctypes.byref(o), reps, _ptr(history))
+    out = [{f: getattr(r, f) for f, _ in SolveReport._fields_} for r in reps]
+    if s in (8, 9) and not raise_on_breakdown:
+        return out
+    _check(ctx, s)
+    return out
+
+
+def laker_block_cg_solve(ctx, nrhs: int, Y, alpha, tol: float, max_iters: int = 0, history=None,
+                         raise_on_breakdown: bool = True, block: int = 0):
+    o = SolveOpts(tol, max_iters, 0)
+    reps = (SolveReport * nrhs)()
+    s = lib.laker_block_cg_solve(ctx, nrhs, block, _ptr(Y), _ptr(alpha), ctypes.byref(o), reps, _ptr(history))
     out = [{f: getattr(r, f) for f, _ in SolveReport._fields_} for r in reps]
     if s in (8, 9) and not raise_on_breakdown:
         return out
@@ -350,6 +364,19 @@ class Context:
             mi = max_iters if max_iters > 0 else 10 * self.n
             hist = np.zeros(mi)
         reps = laker_pcg_solve(self.h, nrhs, Yc, alpha, tol, max_iters, instrument, hist, raise_on_breakdown)
+        if hist is not None:
+            hist = hist[: reps[0]["iters"]].copy()
+        return alpha, reps, hist
+
+    def block_cg_solve(self, Y, tol, max_iters=0, want_history=False, raise_on_breakdown=True, block=0):
+        """O'Leary block PCG over the columns of Y (n x nrhs, nrhs <= 64) in groups of `block`
+        columns (0: one group): laker_block_cg_solve."""
+        Yc = np.asfortranarray(np.asarray(Y, dtype=np.float64)) if not hasattr(Y, "dim") else Y.contiguous()
+        nrhs = (1 if Yc.ndim == 1 else Yc.shape[1]) if isinstance(Yc, np.ndarray) else \
+            (1 if Yc.dim() == 1 else Yc.shape[0])
+        alpha = np.zeros_like(Yc, order="F") if isinstance(Yc, np.ndarray) else Yc.new_zeros(Yc.shape)
+        hist = np.zeros(max_iters if max_iters > 0 else 10 * self.n) if want_history else None
+        reps = laker_block_cg_solve(self.h, nrhs, Yc, alpha, tol, max_iters, hist, raise_on_breakdown, block)
         if hist is not None:
             hist = hist[: reps[0]["iters"]].copy()
         return alpha, reps, hist
