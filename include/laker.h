@@ -9,6 +9,8 @@
  *   laker_fit_preconditioner Regression Learning (CCCP)  (Alg.1 l.4-14)
  *   laker_pcg_solve          Preconditioned CG           (Alg.1 l.15-22)
  *   laker_predict            Radio Map Reconstruction    (Alg.1 l.23-25)
+ * plus the block-CG variant of the multi-RHS solve (C4), laker_block_cg_solve
+ * (O'Leary 1980, B14).
  *
  * Conventions (all calls):
  *  - Every call returns laker_status; no exception or abort crosses the ABI.
