@@ -167,3 +167,27 @@ def test_block_cg_c4_full_size(L):
         assert r64[0]["termination"] in (L.TERM_RESIDUAL_TOL, L.TERM_BREAKDOWN, L.TERM_INDEFINITE)
     finally:
         c.close()
+
+
+def test_block_cg_c4_exact_one_group(L):
+    """C4 EXACT (Dot2 products), one group of all 64 columns: the shared block Krylov space
+    converges in a few tens of steps (14 measured; the batched Alg. 1 columns need 704-778),
+    every true residual <= 10 tol, every column within 1e-6 of the batched solve's."""
+    P = make_problem(4)
+    c = L.Context(0)
+    try:
+        c.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+        c.fit_preconditioner(L.PRECOND_LEARNED, n_dirs=P.n_dirs, seed=7)
+        Y = np.asfortranarray(P.Y)
+        A, reps, _ = c.block_cg_solve(Y, P.tol)
+        Ab, rb, _ = c.pcg_solve(Y, P.tol)
+        its = reps[0]["iters"]
+        print(f"C4 EXACT block CG (one group of 64): {its} its ({reps[0]['seconds']:.3f} s); batched PCG "
+              f"{min(r['iters'] for r in rb)}-{max(r['iters'] for r in rb)} its ({rb[0]['seconds']:.3f} s)")
+        assert all(r["termination"] == L.TERM_RESIDUAL_TOL for r in reps)
+        assert max(r["true_rel_residual"] for r in reps) <= 10 * P.tol
+        assert its < min(r["iters"] for r in rb)
+        for j in range(Y.shape[1]):
+            assert np.linalg.norm(A[:, j] - Ab[:, j]) / np.linalg.norm(Ab[:, j]) <= 1e-6, j
+    finally:
+        c.close()
