@@ -13,6 +13,10 @@
 // Per-column scalars (delta, beta, termination) come from fixed-order Dot2
 // column reductions; a converged column is frozen (its delta/beta are not
 // applied) while the others continue; the loop ends when every column is done.
+//
+// laker_block_cg_solve runs O'Leary's block PCG instead (B14) through the same
+// operator / preconditioner products: m x m Gram matrices and SPD solves per step, the
+// columns in independent groups of `block`.
 #include <cstdlib>
 
 #include "pcg_kernels.cuh"
