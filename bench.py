@@ -180,9 +180,9 @@ def side_measurements(L, dev):
         c4[name] = {"solve_s": reps[0]["seconds"], "nrhs": len(reps), "iters_min": min(its), "iters_max": max(its),
                     "all_converged": all(r["termination"] == L.TERM_RESIDUAL_TOL for r in reps),
                     "worst_true_rel_residual": max(r["true_rel_residual"] for r in reps)}
-        # the block-CG variant (O'Leary block PCG, B14): FAST in 8 groups of 8 columns
+        # the block-CG variant (O'Leary block PCG, B14): FAST in 4 groups of 16 columns
         # (one group of 64 breaks down under the uncompensated products), EXACT as one group
-        blk = 8 if mode == L.MODE_FAST else 64
+        blk = 16 if mode == L.MODE_FAST else 64
         _, rb, _ = c.block_cg_solve(Y, P4.tol, block=blk, raise_on_breakdown=False)
         c4[name + "_block_cg"] = {"solve_s": rb[0]["seconds"], "nrhs": len(rb), "block": blk, "iters": rb[0]["iters"],
                                   "all_converged": all(r["termination"] == L.TERM_RESIDUAL_TOL for r in rb),

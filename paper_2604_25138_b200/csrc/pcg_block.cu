@@ -757,7 +757,10 @@ laker_status pcg_solve_block(laker_ctx ctx, int32_t m, const double *Y, double *
   // binades, M indefinite-sign) stay on the DMMA GEMM -- sliced, their small entries
   // lost enough precision to make r.theta <= 0 near convergence (tested).
   const char *tcenv = std::getenv("LAKER_BLOCK_TC");
-  const bool tcb = !exact && m <= 64 && !(tcenv && tcenv[0] == '0');
+  // (block CG keeps FAST's K products on the DMMA GEMM: its few, coupled steps are far more
+  // sensitive to the S = 7 digit products -- C4, groups of 16: 90 steps / 0.23 s on DMMA,
+  // 132 steps / 0.27 s with true residuals 6e-8 on the int8 products; B14)
+  const bool tcb = !exact && m <= 64 && !(tcenv && tcenv[0] == '0') && !block_cg;
   const int Stc = oz_skinny_max_slices();
   OzSlices sK, sQt, sM, sQr, sXn, sXr;  // sXn / sXr: RHS-block slices for K-dim n / N_r
   double *part = nullptr;
