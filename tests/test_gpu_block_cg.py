@@ -190,3 +190,25 @@ def test_block_cg_c4_exact_one_group(L):
             assert np.linalg.norm(A[:, j] - Ab[:, j]) / np.linalg.norm(Ab[:, j]) <= 1e-6, j
     finally:
         c.close()
+
+
+def test_block_cg_argument_errors(ctx, L):
+    """INVALID_ARGUMENT (laker.h): a group size not dividing nrhs, more than 64 columns, and
+    ON_THE_FLY storage; the context stays usable."""
+    P = make_problem(4, n=256, nrhs=8, tol=1e-8)
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    Y = np.asfortranarray(P.Y)
+    for bad in (3, -1, 9):
+        with pytest.raises(L.LakerError) as e:
+            ctx.block_cg_solve(Y, P.tol, block=bad)
+        assert e.value.status == 1
+    with pytest.raises(L.LakerError) as e:
+        ctx.block_cg_solve(np.asfortranarray(np.tile(Y, (1, 9))), P.tol)
+    assert e.value.status == 1
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_ON_THE_FLY, L.MODE_EXACT)
+    with pytest.raises(L.LakerError) as e:
+        ctx.block_cg_solve(Y, P.tol)
+    assert e.value.status == 1
+    ctx.assemble_kernel(P.E, P.scale, P.lam, L.STORE_MATERIALIZED, L.MODE_EXACT)
+    _, reps, _ = ctx.block_cg_solve(Y, P.tol, block=4)
+    assert all(r["termination"] == L.TERM_RESIDUAL_TOL for r in reps)
